@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the forward splatting rasterizer (BASELINE.json metric: rendered
+FPS & Mpixel/s at 300k primitives 1245x825; % of binding roofline).
+
+One step = the whole hot path for one view per GPU: snp_project (K1) ->
+snp_bin_sort (K2 count/scan/duplicate, K3 onesweep sort, K4 ranges) ->
+snp_render (K5 + K6), replayed as one captured CUDA graph, with the scene
+resident in HBM.  Workload at N=1: config C3 (300k neural primitives, one
+1245x825 view).  For N>1 every rank renders its own C4 orbit view each step
+(weak scaling, one view per GPU per step, no data-path collective; the scene
+is broadcast once from rank 0 with NCCL).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl snp|reference]
+
+--impl reference times the CPU oracle (the only reference this paper-only task
+has) on a bounded pixel sample of the same workload on the host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rendered FPS & Mpixel/s at 300k primitives 1245×825; % of binding roofline"
+# SURVEY.md 8(d) algorithmic work of K5: 15 FP32 per tested (pixel, listed primitive)
+# pair; 102 FP32 + 28 XU (MUFU) per exact hit.  An XU op occupies 8 FP32 issue
+# slots (16 vs 128 lanes/SM/clk), so work is counted in FP32-lane equivalents.
+FP32_PER_PAIR = 15
+FP32_PER_HIT = 102
+XU_PER_HIT = 28
+XU_WEIGHT = 8
+SMS, FP32_LANES = 148, 128
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p.get("sm_max_mhz", 1965.0)), float(p.get("hbm_gbs", 6536.0)), "measured"
+    except Exception:
+        return 1965.0, 6650.0, "fallback"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_gpu{index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def _scene_tensors(scene, torch, dev):
+    import types
+    ns = types.SimpleNamespace(omega=scene.omega, sh_degree=scene.sh_degree)
+    for f in ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh"):
+        setattr(ns, f, torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).to(dev))
+    return ns
+
+
+def run_snp(args):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2510_08491_b200 import snp
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- workload: C3 scene; rank 0's view is the C3 camera, others take C4 orbit views
+    scene, cams3, bg = synth.make_config("C3")
+    cam = cams3[0]
+    if ws > 1 and rank > 0:
+        c4 = synth.orbit_cameras(64, 4.0, cam.width, cam.height, cam.fx, elev_deg=(15.0, 30.0), az0_deg=30.0)
+        cam = c4[(rank * 64 // ws) % 64]
+    W, H = cam.width, cam.height
+    st = torch.cuda.Stream(device=dev)
+
+    # X1: parameters broadcast once from rank 0 (flat [n, 99] fp32)
+    recs = torch.from_numpy(scene.records()).to(dev)
+    if ws > 1:
+        dist.broadcast(recs, src=0)
+    dscene = _scene_tensors(scene, torch, dev)
+
+    h = snp.create_scene(dscene, local, st)
+    out = torch.empty((1, H, W, 4), device=dev)
+    cams_c = snp.make_cameras([cam])
+    opts_sync = snp.make_opts(bg, 1e-4, sync_check=1)
+    opts = snp.make_opts(bg, 1e-4, sync_check=0)
+    with torch.cuda.stream(st):
+        snp.render_views(h, cams_c, opts_sync, out, st)      # sizes every buffer
+        st.synchronize()
+        # capture the whole step (K1..K6) as one CUDA graph
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            snp.render_views(h, cams_c, opts, out, st)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+
+    def step():
+        g.replay()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats = snp.get_stats(h, st)
+    passes = (32 + int(np.ceil(np.log2(((W + 15) // 16) * ((H + 15) // 16)))) + 7) // 8
+    launches_per_step = 8 + passes
+
+    clk = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    times = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with torch.cuda.stream(st):
+        for i in range(args.steps):
+            flush.zero_()                      # evict L2 between timed steps (untimed)
+            ev[i][0].record(st)
+            step()
+            ev[i][1].record(st)
+    st.synchronize()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if ws > 1:
+        dist.barrier()
+    times = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(times))
+    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    fps = ws * args.steps / (total_ms / 1e3)     # views (frames) per second, all GPUs
+
+    # ---- per-stage timing (same stream, CUDA events, non-graph) for the roofline
+    stage = {"project": [], "bin_sort": [], "render": []}
+    with torch.cuda.stream(st):
+        for _ in range(max(3, min(args.steps, 20))):
+            flush.zero_()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(st)
+            snp.project(h, cams_c, st)
+            e[1].record(st)
+            snp.bin_sort(h, opts, st)
+            e[2].record(st)
+            snp.render(h, opts, out, st)
+            e[3].record(st)
+            st.synchronize()
+            stage["project"].append(e[0].elapsed_time(e[1]))
+            stage["bin_sort"].append(e[1].elapsed_time(e[2]))
+            stage["render"].append(e[2].elapsed_time(e[3]))
+    stats = snp.get_stats(h, st)
+    stage_ms = {k: statistics.median(v) for k, v in stage.items()}
+    sm_mhz_max, _, peak_kind = _peaks()
+    peak = SMS * FP32_LANES * sm_mhz_max * 1e6 / 1e12          # T FP32-lane-op/s
+    work = (FP32_PER_PAIR * stats["tested_pairs"] + (FP32_PER_HIT + XU_WEIGHT * XU_PER_HIT) * stats["hit_pairs"])
+    achieved = work / (stage_ms["render"] / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "render_traffic_bytes.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C ABI with HOST buffers: upload scene from pinned host memory,
+    # render, read the frame back to host; copies inside the timed region
+    host = {}
+    for f in ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh"):
+        host[f] = torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).pin_memory()
+    import types
+    hscene = types.SimpleNamespace(omega=scene.omega, sh_degree=scene.sh_degree, **host)
+    hout = torch.empty((1, H, W, 4)).pin_memory()
+    opts_host = snp.make_opts(bg, 1e-4, out_memory=snp.SNP_MEM_HOST, sync_check=1)
+    h2d = sum(int(v.numel()) * 4 for v in host.values()) + 88
+    d2h = int(hout.numel()) * 4
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        hh = snp.create_scene(hscene, local, st)
+        snp.render_views(hh, cams_c, opts_host, hout, st)
+        snp.destroy(hh)
+
+    e2e_step()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_fps = ws * e2e_steps / float(te.item())
+
+    # X2: gather the last frames to rank 0 once (outside the timed region)
+    if ws > 1:
+        gl = [torch.empty_like(out) for _ in range(ws)] if rank == 0 else None
+        dist.gather(out, gl, dst=0)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(scene, cam, bg, budget_s=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "C3: 300k neural primitives (N=8, omega=30, SH deg 3), 1245x825, "
+                                   "1 view per GPU per step (C4 orbit views on ranks > 0)",
+                       "primitives": scene.n, "width": W, "height": H, "views_per_gpu_per_step": 1,
+                       "parallelism": f"views x{ws}" if ws > 1 else "single GPU",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "graph": "project+bin_sort+render captured as one CUDA graph"},
+            "mpix_per_s": round(fps * W * H / 1e6, 2),
+            "stages_ms": {k: round(v, 5) for k, v in stage_ms.items()},
+            "workload_stats": stats,
+            "roofline": {"bound": "alu", "kernel": "k_render (K5)", "achieved": round(achieved, 4),
+                         "peak": round(peak, 3), "unit": "T FP32-lane-op/s (XU op = 8 lanes)",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz_max:.0f} MHz ({peak_kind} sm_max_mhz)",
+                         "work": f"{FP32_PER_PAIR}*tested_pairs + ({FP32_PER_HIT}+{XU_WEIGHT}*{XU_PER_HIT})*hit_pairs"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_fps, 3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "what": "snp_create_scene from pinned host arrays + snp_render_views to a host frame + "
+                            "snp_destroy, wall clock"},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    snp.destroy(h)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(scene, cam, bg, budget_s=15.0):
+    """The oracle as it stands on the host cores, on a seeded pixel sample of the
+    same view; frames/s = sampled pixels/s / (W*H)."""
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(123)
+    W, H = cam.width, cam.height
+    cores = os.cpu_count() or 1
+    n0 = max(64, 16 * cores)
+    px, py = rng.integers(0, W, n0), rng.integers(0, H, n0)
+    t0 = time.perf_counter()
+    oracle.render_pixels(scene, cam, px, py, bg, nthreads=0)
+    dt0 = time.perf_counter() - t0
+    n = int(min(200_000, max(n0, n0 * budget_s / max(dt0, 1e-3))))
+    px, py = rng.integers(0, W, n), rng.integers(0, H, n)
+    t0 = time.perf_counter()
+    oracle.render_pixels(scene, cam, px, py, bg, nthreads=0)
+    dt = time.perf_counter() - t0
+    pps = n / dt
+    return {"value": pps / (W * H), "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} seeded random pixels of the C3 view ({dt:.1f} s, OpenMP over pixels)",
+            "pixels_per_s": round(pps, 1)}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, as it stands, on the host cores."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import synth
+    scene, cams3, bg = synth.make_config("C3")
+    cam = cams3[0]
+    budget = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(321)
+    W, H = cam.width, cam.height
+    cores = os.cpu_count() or 1
+    n0 = max(64, 16 * cores)
+    t0 = time.perf_counter()
+    oracle.render_pixels(scene, cam, rng.integers(0, W, n0), rng.integers(0, H, n0), bg, nthreads=0)
+    per_px = (time.perf_counter() - t0) / n0
+    n = int(max(n0, budget / max(per_px, 1e-9)))
+    for _ in range(args.warmup):
+        oracle.render_pixels(scene, cam, rng.integers(0, W, 64), rng.integers(0, H, 64), bg, nthreads=0)
+    tot_px, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        px, py = rng.integers(0, W, n), rng.integers(0, H, n)
+        t0 = time.perf_counter()
+        oracle.render_pixels(scene, cam, px, py, bg, nthreads=0)
+        tot_s += time.perf_counter() - t0
+        tot_px += n
+    fps = tot_px / tot_s / (W * H)
+    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C3: 300k neural primitives, 1245x825, 1 view; each step = a seeded "
+                                   f"sample of {n} pixels of that view (CPU oracle)"},
+            "cpu_baseline": {"kind": "oracle", "cores": cores, "value": fps, "unit": "frames/s",
+                             "sample": f"{n} random pixels per step x {args.steps} steps"},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="snp", choices=["snp", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_snp(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * snp.h -- C ABI of the B200 (sm_100a) forward splatting rasterizer for
+ * splattable neural primitives (arXiv 2510.08491).
+ *
+ * Citation key: P:n = PAPER.md line n (section / equation named beside it),
+ * S:n = SPEC.md line n, R<k> = reading k in DESIGN.md "Readings of the paper".
+ *
+ * The problem statement (Sec. 3.1 "Representation"): render the
+ * radiance field given by primitives {P_i}; each P_i is an ellipsoid (centre mu,
+ * scale s along its principal axes, rotation quaternion q) holding a density
+ * field sigma(x) = f((x - mu)/||s||_inf) (Eq. 5), f a one-hidden-layer cosine
+ * MLP of width N with frequency omega (Eq. 6), and a view-dependent colour from
+ * spherical harmonics.  A pixel's colour is Eq. 4 alpha blending
+ * of kappa = 1 - exp(-max(0, I)) (Eq. 9), I the closed-form line integral of
+ * sigma over the ray's segment inside the ellipsoid (Eq. 7-8), over the
+ * depth-sorted primitives the ray hits.
+ *
+ * Pipeline (each call asynchronous on the caller's CUDA stream):
+ *   snp_create_scene  copy + validate primitives           (a1 ingest)
+ *   snp_project       K1 project/cull per (view, primitive) (a2)
+ *   snp_bin_sort      K2 count/scan/duplicate keys, K3 onesweep radix sort,
+ *                     K4 tile ranges                          (a3-a5)
+ *   snp_render        K5 per-pixel integral + blend, K6 exact fallback (a6)
+ *   snp_destroy
+ * Stages must run in this order; re-projecting invalidates later stages.
+ *
+ * Conventions: all arrays are fp32, row-major, structure-of-arrays over
+ * primitives.  Quaternions are (w,x,y,z), normalised on read (R8); scales are
+ * ellipsoid semi-axes in world units (R7).  Camera: pinhole, looks along +z,
+ * x right, y down; R_wc is the world-from-camera rotation; the ray of pixel
+ * (x, y) passes through the pixel centre (x + 0.5, y + 0.5) (R6).
+ *
+ * Errors: every call returns an snp_status.  Argument checks are synchronous
+ * and launch nothing.  CUDA launch/async errors surface as SNP_ERR_CUDA from the
+ * call that observes them.  snp_last_error() returns a thread-local message,
+ * valid until the next snp_* call on that thread.  A scene handle is not
+ * thread-safe; distinct handles are independent.
+ */
+#ifndef SNP_H
+#define SNP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SNP_OK = 0,
+    SNP_ERR_INVALID_ARGUMENT = 1,  /* null pointer, bad size, |q| = 0, s <= 0, non-finite value */
+    SNP_ERR_OUT_OF_MEMORY = 2,
+    SNP_ERR_CUDA = 3,
+    SNP_ERR_UNSUPPORTED = 4,       /* e.g. n_hidden != 8 (P:394 default; other widths are future work) */
+    SNP_ERR_BAD_STATE = 5,         /* stage called out of order */
+    SNP_ERR_CAPACITY = 6           /* key buffer too small in no-sync mode (see snp_render_opts.sync_check) */
+} snp_status;
+
+typedef struct snp_scene_s *snp_scene;  /* opaque, owned by the library */
+
+enum { SNP_MEM_HOST = 0, SNP_MEM_DEVICE = 1 };
+
+/* One primitive = 99 fp32 parameters for N = 8 ("99 parameters in total";
+ * P:751 "41 parameters from its 8-neuron MLP"). */
+typedef struct {
+    int64_t n;               /* number of primitives, >= 0 (0 renders background) */
+    int32_t n_hidden;        /* N_sigma, must be 8 */
+    int32_t sh_degree;       /* 0..3; 3 = four bands, 16 coefficients */
+    float omega;             /* frequency multiplier, 30 in the paper; > 0 */
+    int32_t memory;          /* SNP_MEM_HOST or SNP_MEM_DEVICE (device of the scene) */
+    const float *centers;    /* [n][3]    mu */
+    const float *rotations;  /* [n][4]    q = (w,x,y,z), any nonzero norm */
+    const float *scales;     /* [n][3]    s, ellipsoid semi-axes, > 0 */
+    const float *w1;         /* [n][N][3] W1 of Eq. 6 */
+    const float *b1;         /* [n][N]    b1 */
+    const float *w2;         /* [n][N]    W2 */
+    const float *b2;         /* [n]       b2 */
+    const float *sh;         /* [n][16][3] SH coefficients, coefficient-major, RGB innermost */
+} snp_scene_desc;
+
+typedef struct {
+    float R_wc[9];           /* world-from-camera rotation, row-major */
+    float C_w[3];            /* camera centre = ray origin o */
+    float fx, fy, cx, cy;    /* pinhole intrinsics in pixels, fx, fy > 0 */
+    int32_t width, height;   /* image size, 1..32767 */
+    float t_near, t_far;     /* ray segment [t_n, t_f] of Eq. 1 along the unit ray; 0 <= t_near < t_far */
+} snp_camera;
+
+typedef struct {
+    float background[3];        /* added as T_final * bg (R16) */
+    float transmittance_floor;  /* stop compositing once T < floor; 1e-4 */
+    int32_t tile_row_begin;     /* image-stripe partition: only tile rows r = begin + k*stride */
+    int32_t tile_row_stride;    /*   are binned/rendered; (0, 1) = whole image */
+    int32_t out_memory;         /* snp_render output: SNP_MEM_DEVICE or SNP_MEM_HOST */
+    int32_t sync_check;         /* snp_bin_sort: 1 = synchronise once to size the key buffer
+                                   exactly (default); 0 = never synchronise (CUDA-graph safe):
+                                   an undersized buffer is reported by snp_get_stats and the
+                                   next snp_bin_sort returns SNP_ERR_CAPACITY */
+} snp_render_opts;
+
+typedef struct {
+    uint64_t n_visible;        /* (view, primitive) pairs surviving K1 */
+    uint64_t n_dup;            /* duplicated (tile, primitive) keys of the last bin_sort */
+    uint64_t key_capacity;     /* current key buffer capacity */
+    uint64_t tested_pairs;     /* (pixel, listed primitive) pairs visited by K5 */
+    uint64_t candidate_pairs;  /* pairs passing the silhouette pre-test */
+    uint64_t hit_pairs;        /* exact ray-ellipsoid hits */
+    uint64_t composited;       /* kernels blended into pixels */
+    uint64_t overflow_pixels;  /* pixels re-rendered by the exact fallback K6 */
+    uint64_t capacity_overflow;/* 1 if the last no-sync bin_sort overflowed the key buffer */
+} snp_stats;
+
+/* Library version string. */
+const char *snp_version(void);
+
+/* Copies and validates the primitives: every q must have nonzero
+ * norm, every s > 0 and finite, everything finite.  `device` is the CUDA device
+ * ordinal; `cuda_stream` (cudaStream_t, may be NULL) orders the copies.  The
+ * caller may free its arrays on return.  Device-resident inputs are validated
+ * by one reduction kernel plus one stream synchronisation. */
+snp_status snp_create_scene(const snp_scene_desc *desc, int device, void *cuda_stream, snp_scene *out);
+
+/* K1 for n_views cameras (all with the same width/height, 1 <= n_views <= 4096):
+ * per (view, primitive): frustum cull, exact silhouette bbox -> 16x16 tile rect,
+ * depth lower bound key, and the render record (camera-relative centre in
+ * compensated hi/lo form, whitening matrix, SH colour, omega-scaled MLP).
+ * `cams` is host memory, read before return. */
+snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, void *cuda_stream);
+
+/* K2-K4: keys (view | tile | depth) in primitive order, stable LSD radix sort,
+ * per-(view, tile) ranges.  Uses opts->tile_row_begin/stride and sync_check. */
+snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_stream);
+
+/* K5 (+K6): writes out_rgba[n_views][height][width][4] fp32 (R, G, B, opacity =
+ * 1 - T).  out_rgba is device memory (or host memory when opts->out_memory is
+ * SNP_MEM_HOST; the call then synchronises).  Pixels outside the stripe are
+ * left untouched. */
+snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba, void *cuda_stream);
+
+/* Convenience: snp_project + snp_bin_sort + snp_render. */
+snp_status snp_render_views(snp_scene s, const snp_camera *cams, int32_t n_views,
+                            const snp_render_opts *opts, float *out_rgba, void *cuda_stream);
+
+snp_status snp_destroy(snp_scene s);
+
+/* Thread-local text of the last error. */
+const char *snp_last_error(void);
+
+/* Parity/debug readback into HOST arrays (synchronises the stream; not on the
+ * hot path).  Any pointer may be NULL.  rects [n_views*n][4] int32 tile rect
+ * (tx0, ty0, tx1, ty1) or -1s when culled; depth_keys [n_views*n] (fp32 bits of
+ * the depth lower bound); sorted_keys/sorted_ids up to `capacity` entries;
+ * *n_dup receives the key count; tile_ranges [n_views*tiles][2] = [begin, end). */
+snp_status snp_get_binning(snp_scene s, int32_t *rects, uint32_t *depth_keys, uint64_t *sorted_keys,
+                           uint32_t *sorted_ids, int64_t capacity, int64_t *n_dup,
+                           uint32_t *tile_ranges, void *cuda_stream);
+
+/* Counters of the last project/bin_sort/render (synchronises the stream). */
+snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream);
+
+/* Test hook: caps the per-pixel pending buffer of K5 at `k` entries (1..8) so
+ * that the exact fallback K6 is exercised; 0 restores the default (8). */
+snp_status snp_set_pending_limit(snp_scene s, int32_t k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNP_H */

@@ -1,0 +1,512 @@
+// api.cu -- the C ABI of include/snp.h: argument checks, scene-owned device
+// memory, stage ordering and kernel orchestration on the caller's stream.
+#include <cmath>
+#include <cstdio>
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "snp_internal.cuh"
+
+using namespace snp;
+
+namespace {
+
+thread_local std::string g_err;
+
+snp_status fail(snp_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+#define SNP_CUDA(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t _e = (expr);                                                                    \
+        if (_e != cudaSuccess)                                                                      \
+            return fail(_e == cudaErrorMemoryAllocation ? SNP_ERR_OUT_OF_MEMORY : SNP_ERR_CUDA,     \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                        \
+    } while (0)
+
+enum State { kCreated = 0, kProjected = 1, kBinned = 2 };
+
+// Device buffer that only grows.
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t cap = 0;  // elements
+    cudaError_t ensure(size_t n) {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = n ? n : 1;
+        cudaError_t e = cudaMalloc((void **)&p, want * sizeof(T));
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct snp_scene_s {
+    int device = 0;
+    int64_t n = 0;
+    int32_t sh_degree = 3;
+    float omega = 30.f;
+    // parameters (SoA)
+    DevBuf<float> params;
+    float *centers = nullptr, *rotations = nullptr, *scales = nullptr, *w1 = nullptr, *b1 = nullptr,
+          *w2 = nullptr, *b2 = nullptr, *sh = nullptr;
+    // projection
+    int state = kCreated;
+    int32_t n_views = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, view_bits = 0;
+    std::vector<CamBatch> cams;
+    DevBuf<short4> rects;
+    DevBuf<uint32_t> depth;
+    DevBuf<float4> records;
+    // binning
+    int32_t row_begin = 0, row_stride = 1, stripe_rows = 0;
+    DevBuf<uint64_t> keys0, keys1;
+    DevBuf<uint32_t> vals0, vals1;
+    int64_t key_capacity = 0;
+    DevBuf<uint32_t> partials;
+    DevBuf<uint32_t> sort_scratch;
+    int64_t sort_max_partitions = 0;
+    int sorted_idx = 0;
+    DevBuf<uint32_t> ranges;
+    // render
+    DevBuf<uint32_t> fallback;
+    int64_t fallback_capacity = 0;
+    DevBuf<float> host_out_staging;
+    int32_t pending_limit = 8;
+    // counters
+    DevBuf<unsigned long long> counters;
+    unsigned long long *h_counters = nullptr;  // pinned
+    DevBuf<int> flag;
+};
+
+namespace {
+
+bool finite_all(const float *p, int64_t k) {
+    for (int64_t i = 0; i < k; ++i)
+        if (!std::isfinite(p[i])) return false;
+    return true;
+}
+
+int bits_for(int64_t n) {
+    int b = 0;
+    while (((int64_t)1 << b) < n) ++b;
+    return b;
+}
+
+void fill_args(snp_scene s, ProjectArgs &a) {
+    a.n = s->n;
+    a.sh_degree = s->sh_degree;
+    a.omega = s->omega;
+    a.centers = s->centers; a.rotations = s->rotations; a.scales = s->scales;
+    a.w1 = s->w1; a.b1 = s->b1; a.w2 = s->w2; a.b2 = s->b2; a.sh = s->sh;
+    a.tiles_x = s->tiles_x; a.tiles_y = s->tiles_y;
+    a.rects = s->rects.p; a.depth = s->depth.p; a.records = s->records.p;
+    a.counters = s->counters.p;
+}
+
+snp_status check_scene(snp_scene s) {
+    if (!s) return fail(SNP_ERR_INVALID_ARGUMENT, "scene handle is NULL");
+    cudaError_t e = cudaSetDevice(s->device);
+    if (e != cudaSuccess) return fail(SNP_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    return SNP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *snp_version(void) { return "snp 0.1.0 (sm_100a)"; }
+
+const char *snp_last_error(void) { return g_err.c_str(); }
+
+snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stream, snp_scene *out) {
+    g_err.clear();
+    if (!d || !out) return fail(SNP_ERR_INVALID_ARGUMENT, "desc or out is NULL");
+    *out = nullptr;
+    if (d->n < 0) return fail(SNP_ERR_INVALID_ARGUMENT, "n < 0");
+    if (d->n_hidden != kHidden) return fail(SNP_ERR_UNSUPPORTED, "n_hidden must be 8 (P:394)");
+    if (d->sh_degree < 0 || d->sh_degree > 3) return fail(SNP_ERR_INVALID_ARGUMENT, "sh_degree must be 0..3");
+    if (!(d->omega > 0.f) || !std::isfinite(d->omega)) return fail(SNP_ERR_INVALID_ARGUMENT, "omega must be > 0");
+    if (d->memory != SNP_MEM_HOST && d->memory != SNP_MEM_DEVICE)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "memory must be SNP_MEM_HOST or SNP_MEM_DEVICE");
+    if (d->n >= (int64_t)1 << 31) return fail(SNP_ERR_UNSUPPORTED, "n must be < 2^31");
+    const int64_t n = d->n;
+    const float *src[8] = {d->centers, d->rotations, d->scales, d->w1, d->b1, d->w2, d->b2, d->sh};
+    const int64_t per[8] = {3, 4, 3, 24, 8, 8, 1, 48};
+    if (n > 0)
+        for (int k = 0; k < 8; ++k)
+            if (!src[k]) return fail(SNP_ERR_INVALID_ARGUMENT, "a parameter array is NULL");
+    if (d->memory == SNP_MEM_HOST && n > 0) {
+        for (int64_t i = 0; i < n; ++i) {
+            const float *q = d->rotations + 4 * i;
+            const double qn = (double)q[0] * q[0] + (double)q[1] * q[1] + (double)q[2] * q[2] + (double)q[3] * q[3];
+            if (!(qn > 0.0)) return fail(SNP_ERR_INVALID_ARGUMENT, "zero quaternion at primitive " + std::to_string(i));
+            for (int k = 0; k < 3; ++k)
+                if (!(d->scales[3 * i + k] > 0.f) || !std::isfinite(d->scales[3 * i + k]))
+                    return fail(SNP_ERR_INVALID_ARGUMENT, "non-positive scale at primitive " + std::to_string(i));
+        }
+        for (int k = 0; k < 8; ++k)
+            if (!finite_all(src[k], per[k] * n)) return fail(SNP_ERR_INVALID_ARGUMENT, "non-finite parameter");
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(SNP_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    snp_scene s = new snp_scene_s();
+    s->device = device;
+    s->n = n;
+    s->sh_degree = d->sh_degree;
+    s->omega = d->omega;
+    // one allocation, each array 256-byte aligned
+    size_t off[9];
+    size_t tot = 0;
+    for (int k = 0; k < 8; ++k) {
+        off[k] = tot;
+        tot += ((size_t)(per[k] * n) * sizeof(float) + 255) / 256 * 256;
+    }
+    off[8] = tot;
+    cudaError_t ce = s->params.ensure(tot / sizeof(float) + 64);
+    if (ce == cudaSuccess) ce = s->counters.ensure(kNumCounters);
+    if (ce == cudaSuccess) ce = s->flag.ensure(1);
+    if (ce == cudaSuccess) ce = cudaMallocHost((void **)&s->h_counters, sizeof(unsigned long long) * kNumCounters);
+    if (ce != cudaSuccess) {
+        snp_destroy(s);
+        return fail(ce == cudaErrorMemoryAllocation ? SNP_ERR_OUT_OF_MEMORY : SNP_ERR_CUDA,
+                    std::string("allocation: ") + cudaGetErrorString(ce));
+    }
+    float **dst[8] = {&s->centers, &s->rotations, &s->scales, &s->w1, &s->b1, &s->w2, &s->b2, &s->sh};
+    for (int k = 0; k < 8; ++k) {
+        *dst[k] = reinterpret_cast<float *>(reinterpret_cast<char *>(s->params.p) + off[k]);
+        if (n > 0) {
+            ce = cudaMemcpyAsync(*dst[k], src[k], sizeof(float) * per[k] * n,
+                                 d->memory == SNP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
+            if (ce != cudaSuccess) break;
+        }
+    }
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kNumCounters, st);
+    if (ce == cudaSuccess && d->memory == SNP_MEM_DEVICE && n > 0) {
+        ce = cudaMemsetAsync(s->flag.p, 0, sizeof(int), st);
+        ProjectArgs a{};
+        fill_args(s, a);
+        if (ce == cudaSuccess) ce = launch_validate(a, s->flag.p, st);
+        int bad = 0;
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(&bad, s->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        if (ce == cudaSuccess && bad) {
+            snp_destroy(s);
+            return fail(SNP_ERR_INVALID_ARGUMENT, "invalid primitive (zero quaternion, scale <= 0 or non-finite)");
+        }
+    }
+    if (ce != cudaSuccess) {
+        snp_destroy(s);
+        return fail(SNP_ERR_CUDA, std::string("create: ") + cudaGetErrorString(ce));
+    }
+    *out = s;
+    return SNP_OK;
+}
+
+snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!cams) return fail(SNP_ERR_INVALID_ARGUMENT, "cams is NULL");
+    if (n_views < 1 || n_views > 4096) return fail(SNP_ERR_INVALID_ARGUMENT, "n_views must be 1..4096");
+    const int32_t W = cams[0].width, H = cams[0].height;
+    if (W < 1 || H < 1 || W > 32767 || H > 32767) return fail(SNP_ERR_INVALID_ARGUMENT, "width/height must be 1..32767");
+    for (int v = 0; v < n_views; ++v) {
+        const snp_camera &c = cams[v];
+        if (c.width != W || c.height != H) return fail(SNP_ERR_INVALID_ARGUMENT, "all views must share width/height");
+        bool ok = c.fx > 0.f && c.fy > 0.f && std::isfinite(c.fx) && std::isfinite(c.fy) && std::isfinite(c.cx) &&
+                  std::isfinite(c.cy) && c.t_near >= 0.f && c.t_far > c.t_near && std::isfinite(c.t_far);
+        for (int k = 0; k < 9; ++k) ok = ok && std::isfinite(c.R_wc[k]);
+        for (int k = 0; k < 3; ++k) ok = ok && std::isfinite(c.C_w[k]);
+        if (!ok) return fail(SNP_ERR_INVALID_ARGUMENT, "invalid camera " + std::to_string(v));
+    }
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    s->n_views = n_views;
+    s->W = W;
+    s->H = H;
+    s->tiles_x = (W + kTile - 1) / kTile;
+    s->tiles_y = (H + kTile - 1) / kTile;
+    s->tile_bits = bits_for((int64_t)s->tiles_x * s->tiles_y);
+    s->view_bits = bits_for(n_views);
+    if (32 + s->tile_bits + s->view_bits > 64) return fail(SNP_ERR_UNSUPPORTED, "key exceeds 64 bits");
+    const size_t items = (size_t)n_views * (size_t)s->n;
+    SNP_CUDA(s->rects.ensure(items));
+    SNP_CUDA(s->depth.ensure(items));
+    SNP_CUDA(s->records.ensure(items * 16));
+    s->cams.clear();
+    for (int v0 = 0; v0 < n_views; v0 += kCamsPerLaunch) {
+        CamBatch cb{};
+        cb.view0 = v0;
+        cb.nv = std::min(kCamsPerLaunch, n_views - v0);
+        for (int k = 0; k < cb.nv; ++k) {
+            const snp_camera &c = cams[v0 + k];
+            DevCam &dc = cb.cams[k];
+            std::memcpy(dc.R, c.R_wc, sizeof dc.R);
+            std::memcpy(dc.C, c.C_w, sizeof dc.C);
+            dc.fx = c.fx; dc.fy = c.fy; dc.cx = c.cx; dc.cy = c.cy;
+            dc.W = c.width; dc.H = c.height;
+            dc.t_near = c.t_near; dc.t_far = c.t_far;
+        }
+        s->cams.push_back(cb);
+    }
+    SNP_CUDA(cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kNumCounters, st));
+    ProjectArgs a{};
+    fill_args(s, a);
+    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_project(a, cb, st));
+    s->state = kProjected;
+    return SNP_OK;
+}
+
+snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!opts) return fail(SNP_ERR_INVALID_ARGUMENT, "opts is NULL");
+    if (s->state < kProjected) return fail(SNP_ERR_BAD_STATE, "snp_bin_sort before snp_project");
+    if (opts->tile_row_stride < 1 || opts->tile_row_begin < 0)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "tile_row_stride must be >= 1 and tile_row_begin >= 0");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    s->row_begin = opts->tile_row_begin;
+    s->row_stride = opts->tile_row_stride;
+    s->stripe_rows = s->row_begin < s->tiles_y ? (s->tiles_y - 1 - s->row_begin) / s->row_stride + 1 : 0;
+    const int64_t items = (int64_t)s->n_views * s->n;
+    SNP_CUDA(s->partials.ensure((size_t)bin_scan_blocks(items) + 1));
+    if (s->key_capacity == 0) {
+        // first guess: 4 keys per (view, primitive); sync_check resizes exactly
+        s->key_capacity = std::max<int64_t>(4 * items, 1024);
+    }
+    BinArgs b{};
+    b.n = s->n;
+    b.n_views = s->n_views;
+    b.tiles_x = s->tiles_x;
+    b.tiles_y = s->tiles_y;
+    b.tile_bits = s->tile_bits;
+    b.row_begin = s->row_begin;
+    b.row_stride = s->row_stride;
+    b.rects = s->rects.p;
+    b.depth = s->depth.p;
+    b.partials = s->partials.p;
+    b.counters = s->counters.p;
+    auto alloc_keys = [&](int64_t cap) -> cudaError_t {
+        cudaError_t e;
+        if ((e = s->keys0.ensure((size_t)cap)) != cudaSuccess) return e;
+        if ((e = s->keys1.ensure((size_t)cap)) != cudaSuccess) return e;
+        if ((e = s->vals0.ensure((size_t)cap)) != cudaSuccess) return e;
+        if ((e = s->vals1.ensure((size_t)cap)) != cudaSuccess) return e;
+        return cudaSuccess;
+    };
+    SNP_CUDA(alloc_keys(s->key_capacity));
+    b.capacity = s->key_capacity;
+    SNP_CUDA(launch_count_scan(b, st));
+    if (opts->sync_check) {
+        SNP_CUDA(cudaMemcpyAsync(s->h_counters + kCntDup, s->counters.p + kCntDup, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+        SNP_CUDA(cudaStreamSynchronize(st));
+        const int64_t ndup = (int64_t)s->h_counters[kCntDup];
+        if (ndup > s->key_capacity) {
+            s->key_capacity = ndup + ndup / 4 + 1024;
+            SNP_CUDA(alloc_keys(s->key_capacity));
+            // counters[kCntCapOverflow] was computed against the old capacity
+            SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntCapOverflow, 0, sizeof(unsigned long long), st));
+        }
+        b.capacity = s->key_capacity;
+    }
+    b.keys = s->keys0.p;
+    b.vals = s->vals0.p;
+    SNP_CUDA(launch_dup_only(b, st));
+    // K3: onesweep over the significant bits only
+    const int bits = 32 + s->tile_bits + s->view_bits;
+    const int passes = (bits + 7) / 8;
+    const int64_t maxp = (s->key_capacity + sort_partition_size() - 1) / sort_partition_size();
+    if (maxp > s->sort_max_partitions || !s->sort_scratch.p) {
+        SNP_CUDA(s->sort_scratch.ensure(sort_scratch_words(8, maxp)));
+        s->sort_max_partitions = maxp;
+    }
+    SortScratch sc{};
+    sc.hist = s->sort_scratch.p;
+    sc.lookback = s->sort_scratch.p + 8 * 256;
+    sc.tickets = s->sort_scratch.p + 8 * 256 + (size_t)8 * maxp * 256;
+    sc.max_partitions = s->sort_max_partitions;
+    int final_idx = 0;
+    SNP_CUDA(launch_onesweep(s->keys0.p, s->vals0.p, s->keys1.p, s->vals1.p, s->key_capacity, s->counters.p,
+                             passes, sc, st, &final_idx));
+    s->sorted_idx = final_idx;
+    const uint64_t *sk = final_idx ? s->keys1.p : s->keys0.p;
+    // K4
+    const int64_t slots = (int64_t)s->n_views * s->tiles_x * s->tiles_y;
+    SNP_CUDA(s->ranges.ensure((size_t)slots * 2));
+    SNP_CUDA(launch_tile_ranges(sk, s->counters.p, s->key_capacity, s->tile_bits, s->tiles_x * s->tiles_y,
+                                s->ranges.p, slots, st));
+    s->state = kBinned;
+    return SNP_OK;
+}
+
+snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!opts || !out_rgba) return fail(SNP_ERR_INVALID_ARGUMENT, "opts or out_rgba is NULL");
+    if (s->state < kBinned) return fail(SNP_ERR_BAD_STATE, "snp_render before snp_bin_sort");
+    if (!(opts->transmittance_floor >= 0.f) || !(opts->transmittance_floor < 1.f))
+        return fail(SNP_ERR_INVALID_ARGUMENT, "transmittance_floor must be in [0, 1)");
+    if (opts->out_memory != SNP_MEM_HOST && opts->out_memory != SNP_MEM_DEVICE)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "out_memory must be SNP_MEM_HOST or SNP_MEM_DEVICE");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const size_t out_floats = (size_t)s->n_views * s->W * s->H * 4;
+    float *dout = out_rgba;
+    if (opts->out_memory == SNP_MEM_HOST) {
+        SNP_CUDA(s->host_out_staging.ensure(out_floats));
+        dout = s->host_out_staging.p;
+        SNP_CUDA(cudaMemsetAsync(dout, 0, out_floats * sizeof(float), st));
+    }
+    const int64_t fb_cap = std::min<int64_t>((int64_t)s->n_views * s->W * s->H, (int64_t)1 << 22);
+    if (s->fallback_capacity < fb_cap) {
+        SNP_CUDA(s->fallback.ensure((size_t)fb_cap * 2));
+        s->fallback_capacity = fb_cap;
+    }
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0, sizeof(unsigned long long) * 5, st));
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntFallbackQueue, 0, sizeof(unsigned long long), st));
+    RenderArgs a{};
+    a.tiles_x = s->tiles_x;
+    a.tiles_y = s->tiles_y;
+    a.tiles_per_view = s->tiles_x * s->tiles_y;
+    a.tile_bits = s->tile_bits;
+    a.row_begin = s->row_begin;
+    a.row_stride = s->row_stride;
+    a.stripe_rows = s->stripe_rows;
+    a.n = s->n;
+    a.records = s->records.p;
+    a.keys = s->sorted_idx ? s->keys1.p : s->keys0.p;
+    a.vals = s->sorted_idx ? s->vals1.p : s->vals0.p;
+    a.ranges = s->ranges.p;
+    for (int c = 0; c < 3; ++c) a.bg[c] = opts->background[c];
+    a.t_floor = opts->transmittance_floor;
+    a.pending_limit = s->pending_limit;
+    a.out = dout;
+    a.fallback = s->fallback.p;
+    a.fallback_capacity = s->fallback_capacity;
+    a.counters = s->counters.p;
+    if (s->stripe_rows > 0) {
+        // (an empty scene has empty tile ranges: every pixel gets the background)
+        for (const CamBatch &cb : s->cams) SNP_CUDA(launch_render(a, cb, st));
+        if (s->n > 0) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
+    }
+    if (opts->out_memory == SNP_MEM_HOST) {
+        SNP_CUDA(cudaMemcpyAsync(out_rgba, dout, out_floats * sizeof(float), cudaMemcpyDeviceToHost, st));
+        SNP_CUDA(cudaStreamSynchronize(st));
+    }
+    return SNP_OK;
+}
+
+snp_status snp_render_views(snp_scene s, const snp_camera *cams, int32_t n_views, const snp_render_opts *opts,
+                            float *out_rgba, void *cuda_stream) {
+    snp_status r = snp_project(s, cams, n_views, cuda_stream);
+    if (r != SNP_OK) return r;
+    r = snp_bin_sort(s, opts, cuda_stream);
+    if (r != SNP_OK) return r;
+    return snp_render(s, opts, out_rgba, cuda_stream);
+}
+
+snp_status snp_destroy(snp_scene s) {
+    if (!s) return SNP_OK;
+    cudaSetDevice(s->device);
+    cudaDeviceSynchronize();
+    s->params.release();
+    s->rects.release();
+    s->depth.release();
+    s->records.release();
+    s->keys0.release();
+    s->keys1.release();
+    s->vals0.release();
+    s->vals1.release();
+    s->partials.release();
+    s->sort_scratch.release();
+    s->ranges.release();
+    s->fallback.release();
+    s->host_out_staging.release();
+    s->counters.release();
+    s->flag.release();
+    if (s->h_counters) cudaFreeHost(s->h_counters);
+    delete s;
+    return SNP_OK;
+}
+
+snp_status snp_get_binning(snp_scene s, int32_t *rects, uint32_t *depth_keys, uint64_t *sorted_keys,
+                           uint32_t *sorted_ids, int64_t capacity, int64_t *n_dup, uint32_t *tile_ranges,
+                           void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (s->state < kProjected) return fail(SNP_ERR_BAD_STATE, "nothing projected yet");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    SNP_CUDA(cudaStreamSynchronize(st));
+    const size_t items = (size_t)s->n_views * s->n;
+    if (rects && items) {
+        std::vector<short4> tmp(items);
+        SNP_CUDA(cudaMemcpy(tmp.data(), s->rects.p, items * sizeof(short4), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < items; ++i) {
+            rects[4 * i] = tmp[i].x; rects[4 * i + 1] = tmp[i].y;
+            rects[4 * i + 2] = tmp[i].z; rects[4 * i + 3] = tmp[i].w;
+        }
+    }
+    if (depth_keys && items) SNP_CUDA(cudaMemcpy(depth_keys, s->depth.p, items * 4, cudaMemcpyDeviceToHost));
+    if (s->state >= kBinned) {
+        unsigned long long nd = 0;
+        SNP_CUDA(cudaMemcpy(&nd, s->counters.p + kCntDup, sizeof nd, cudaMemcpyDeviceToHost));
+        if (n_dup) *n_dup = (int64_t)nd;
+        int64_t m = std::min<int64_t>(std::min<int64_t>((int64_t)nd, capacity), s->key_capacity);
+        const uint64_t *sk = s->sorted_idx ? s->keys1.p : s->keys0.p;
+        const uint32_t *sv = s->sorted_idx ? s->vals1.p : s->vals0.p;
+        if (sorted_keys && m > 0) SNP_CUDA(cudaMemcpy(sorted_keys, sk, (size_t)m * 8, cudaMemcpyDeviceToHost));
+        if (sorted_ids && m > 0) SNP_CUDA(cudaMemcpy(sorted_ids, sv, (size_t)m * 4, cudaMemcpyDeviceToHost));
+        const size_t slots = (size_t)s->n_views * s->tiles_x * s->tiles_y;
+        if (tile_ranges) SNP_CUDA(cudaMemcpy(tile_ranges, s->ranges.p, slots * 8, cudaMemcpyDeviceToHost));
+    } else if (n_dup) {
+        *n_dup = -1;
+    }
+    return SNP_OK;
+}
+
+snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!out) return fail(SNP_ERR_INVALID_ARGUMENT, "out is NULL");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    SNP_CUDA(cudaMemcpyAsync(s->h_counters, s->counters.p, sizeof(unsigned long long) * kNumCounters,
+                             cudaMemcpyDeviceToHost, st));
+    SNP_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long *c = s->h_counters;
+    out->n_visible = c[kCntVisible];
+    out->n_dup = c[kCntDup];
+    out->key_capacity = (uint64_t)s->key_capacity;
+    out->tested_pairs = c[kCntTested];
+    out->candidate_pairs = c[kCntCandidate];
+    out->hit_pairs = c[kCntHit];
+    out->composited = c[kCntComposited];
+    out->overflow_pixels = c[kCntOverflow];
+    out->capacity_overflow = c[kCntCapOverflow];
+    return SNP_OK;
+}
+
+snp_status snp_set_pending_limit(snp_scene s, int32_t k) {
+    if (!s) return fail(SNP_ERR_INVALID_ARGUMENT, "scene handle is NULL");
+    if (k < 0 || k > 8) return fail(SNP_ERR_INVALID_ARGUMENT, "pending limit must be 0..8");
+    s->pending_limit = k == 0 ? 8 : k;
+    return SNP_OK;
+}
+
+}  // extern "C"

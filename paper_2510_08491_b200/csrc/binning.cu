@@ -1,0 +1,225 @@
+// binning.cu -- K2 (count, scan, warp-aggregated key duplication) and K4
+// (tile ranges).  Key layout (R19): view << (tile_bits + 32) |
+// tile << 32 | bits(L), L the fp32 depth lower bound from K1; value = primitive
+// index.  Emission order: view, primitive, stripe rows, columns -- the order the
+// stable sort (K3) then preserves among equal keys.  The paper itself names no
+// tiles; "depth-sorted" is realised per ray in K5 on top of this order.
+#include "snp_internal.cuh"
+
+namespace snp {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;                       // items per thread (blocked)
+constexpr int kScanTile = kScanThreads * kScanItems;  // 2048 items per block
+
+struct ItemInfo {
+    uint32_t count;
+    int32_t x0, w, r_first;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const BinArgs &a, int64_t o) {
+    ItemInfo it{0, 0, 0, 0};
+    short4 r = a.rects[o];
+    if (r.x < 0) return it;
+    int32_t y0 = r.y, y1 = r.w;
+    int32_t first = y0 > a.row_begin ? y0 : a.row_begin;
+    int32_t k = (first - a.row_begin + a.row_stride - 1) / a.row_stride;
+    int32_t rf = a.row_begin + k * a.row_stride;
+    if (rf > y1) return it;
+    int32_t rows = (y1 - rf) / a.row_stride + 1;
+    it.x0 = r.x;
+    it.w = r.z - r.x + 1;
+    it.r_first = rf;
+    it.count = (uint32_t)(rows * it.w);
+    return it;
+}
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *smem_warp, uint32_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) smem_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < (kScanThreads / 32) ? smem_warp[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+            if (lane >= d) w += y;
+        }
+        if (lane < (kScanThreads / 32)) smem_warp[lane] = w;
+    }
+    __syncthreads();
+    total = smem_warp[kScanThreads / 32 - 1];
+    uint32_t before = wid ? smem_warp[wid - 1] : 0;
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_count_reduce(BinArgs a) {
+    __shared__ uint32_t sw[32];
+    const int64_t total_items = a.n * a.n_views;
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+        if (base + k < total_items) s += item_info(a, base + k).count;
+    uint32_t tot;
+    block_exclusive_scan(s, sw, tot);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = tot;
+}
+
+// Single block: exclusive scan of the block partials; total -> counters[kCntDup].
+__global__ void __launch_bounds__(1024) k_scan_partials(BinArgs a, int64_t nblocks) {
+    __shared__ uint32_t sw[32];
+    __shared__ unsigned long long carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < nblocks; b0 += 1024) {
+        int64_t b = b0 + threadIdx.x;
+        uint32_t v = b < nblocks ? a.partials[b] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) sw[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = sw[lane];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= d) w += y;
+            }
+            sw[lane] = w;
+        }
+        __syncthreads();
+        uint32_t before = wid ? sw[wid - 1] : 0;
+        unsigned long long c = carry;
+        if (b < nblocks) a.partials[b] = (uint32_t)(c + before + x - v);
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c + sw[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        unsigned long long tot = carry;
+        a.counters[kCntDup] = tot;
+        a.counters[kCntCapOverflow] = tot > (unsigned long long)a.capacity ? 1ull : 0ull;
+    }
+}
+
+// Recomputes counts, forms per-item offsets, and emits keys warp-aggregated:
+// the 256 items of a warp own a contiguous output range; lanes walk it 32 keys
+// at a time (coalesced 8-byte key + 4-byte value stores), each lane finding its
+// key's item by binary search over the warp's item offsets in shared memory.
+__global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
+    __shared__ uint32_t sw[32];
+    __shared__ uint32_t s_off[kScanTile + 8];   // per item exclusive offset (block-relative)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t total_items = a.n * a.n_views;
+    const int64_t blk0 = (int64_t)blockIdx.x * kScanTile;
+    const int64_t base = blk0 + (int64_t)threadIdx.x * kScanItems;
+    uint32_t cnt[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        cnt[k] = (base + k < total_items) ? item_info(a, base + k).count : 0u;
+        s += cnt[k];
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan(s, sw, tot);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        s_off[threadIdx.x * kScanItems + k] = ex;
+        ex += cnt[k];
+    }
+    if (threadIdx.x == kScanThreads - 1) s_off[kScanTile] = ex;   // block total
+    __syncthreads();
+    const uint64_t gbase = a.partials[blockIdx.x];
+    // warp wid owns items [wid*256, wid*256+256) of this block
+    const int i0 = wid * 32 * kScanItems;
+    const uint32_t wbeg = s_off[i0];
+    const uint32_t wend = (wid == kScanThreads / 32 - 1) ? s_off[kScanTile] : s_off[i0 + 32 * kScanItems];
+    const uint64_t view_shift = (uint64_t)a.tile_bits + 32;
+    for (uint32_t e = wbeg + lane; e < wend; e += 32) {
+        // largest item j in [i0, i0+256) with s_off[j] <= e (and count > 0)
+        int lo = i0, hi = i0 + 32 * kScanItems - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (s_off[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        const int64_t o = blk0 + lo;
+        const ItemInfo it = item_info(a, o);
+        const uint32_t k = e - s_off[lo];
+        const int32_t ri = (int32_t)(k / (uint32_t)it.w);
+        const int32_t c = (int32_t)(k - (uint32_t)ri * (uint32_t)it.w);
+        const int32_t row = it.r_first + ri * a.row_stride;
+        const uint64_t view = (uint64_t)(o / a.n);
+        const uint32_t prim = (uint32_t)(o - (int64_t)view * a.n);
+        const uint64_t tile = (uint64_t)row * (uint64_t)a.tiles_x + (uint64_t)(it.x0 + c);
+        const uint64_t key = (view << view_shift) | (tile << 32) | (uint64_t)a.depth[o];
+        const uint64_t g = gbase + e;
+        if (g < (uint64_t)a.capacity) {
+            a.keys[g] = key;
+            a.vals[g] = prim;
+        }
+    }
+}
+
+__global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
+                              int32_t tile_bits, int32_t tiles, uint32_t *ranges) {
+    int64_t n = (int64_t)counters[kCntDup];
+    if (n > capacity) n = capacity;
+    const uint64_t tmask = (1ull << tile_bits) - 1ull;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t vt = keys[i] >> 32;
+        const uint64_t slot = (vt >> tile_bits) * (uint64_t)tiles + (vt & tmask);
+        if (i == 0 || (keys[i - 1] >> 32) != vt) ranges[2 * slot] = (uint32_t)i;
+        if (i == n - 1 || (keys[i + 1] >> 32) != vt) ranges[2 * slot + 1] = (uint32_t)(i + 1);
+    }
+}
+
+}  // namespace
+
+int64_t bin_scan_blocks(int64_t items) { return (items + kScanTile - 1) / kScanTile; }
+
+cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st) {
+    const int64_t items = a.n * a.n_views;
+    const int64_t nb = bin_scan_blocks(items);
+    if (nb == 0) {
+        cudaError_t e = cudaMemsetAsync(a.counters + kCntDup, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        return cudaMemsetAsync(a.counters + kCntCapOverflow, 0, sizeof(unsigned long long), st);
+    }
+    k_count_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(a);
+    k_scan_partials<<<1, 1024, 0, st>>>(a, nb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dup_only(const BinArgs &a, cudaStream_t st) {
+    const int64_t nb = bin_scan_blocks(a.n * a.n_views);
+    if (nb == 0) return cudaSuccess;
+    k_scan_dup<<<(unsigned)nb, kScanThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
+                               int32_t tile_bits, int32_t tiles, uint32_t *ranges, int64_t n_slots,
+                               cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(ranges, 0, sizeof(uint32_t) * 2 * (size_t)n_slots, st);
+    if (e != cudaSuccess) return e;
+    if (capacity == 0) return cudaSuccess;
+    int64_t blocks = (capacity + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_tile_ranges<<<(unsigned)blocks, 256, 0, st>>>(keys, counters, capacity, tile_bits, tiles, ranges);
+    return cudaGetLastError();
+}
+
+}  // namespace snp

@@ -1,0 +1,327 @@
+// project.cu -- K1: per (view, primitive) projection, cull, binning geometry
+// and render record.  Compiled with -fmad=false: the FP64 binning geometry
+// below follows the fixed operation order of DESIGN.md "Binning definition"
+// so that tile rects and depth keys are bit-exact with
+// the CPU oracle's definition.  Every product/sum is written left to right.
+//
+// Paper anchors: P:235 (ellipsoid mu, s, q), P:249 (||s||_inf normalisation,
+// Eq. 5), P:253-283 (MLP, Eq. 6), P:286/P:394 (SH colour), P:298-299 (analytic
+// line-ellipsoid intersection), P:368 ("perspectively accurate").
+#include <math.h>
+
+#include "snp_internal.cuh"
+
+namespace snp {
+namespace {
+
+__device__ __forceinline__ bool quat_rot(const float *q4, double R[9]) {
+    double q0 = q4[0], q1 = q4[1], q2 = q4[2], q3 = q4[3];
+    double nq = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    if (!(nq > 0.0)) return false;
+    double w = q0 / nq, x = q1 / nq, y = q2 / nq, z = q3 / nq;
+    R[0] = 1.0 - 2.0 * (y * y + z * z);
+    R[1] = 2.0 * (x * y - w * z);
+    R[2] = 2.0 * (x * z + w * y);
+    R[3] = 2.0 * (x * y + w * z);
+    R[4] = 1.0 - 2.0 * (x * x + z * z);
+    R[5] = 2.0 * (y * z - w * x);
+    R[6] = 2.0 * (x * z - w * y);
+    R[7] = 2.0 * (y * z + w * x);
+    R[8] = 1.0 - 2.0 * (x * x + y * y);
+    return true;
+}
+
+// Real SH basis, degrees 0..3 (Condon-Shortley phase, m = -l..l; 3DGS convention).
+__device__ __forceinline__ void sh_rgb(int degree, const float *sh, double x, double y, double z,
+                                       float rgb[3]) {
+    double Y[16];
+    const double xx = x * x, yy = y * y, zz = z * z;
+    Y[0] = 0.28209479177387814;
+    Y[1] = -0.4886025119029199 * y;
+    Y[2] = 0.4886025119029199 * z;
+    Y[3] = -0.4886025119029199 * x;
+    Y[4] = 1.0925484305920792 * (x * y);
+    Y[5] = -1.0925484305920792 * (y * z);
+    Y[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+    Y[7] = -1.0925484305920792 * (x * z);
+    Y[8] = 0.5462742152960396 * (xx - yy);
+    Y[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+    Y[10] = 2.890611442640554 * (x * y) * z;
+    Y[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+    Y[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    Y[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+    Y[14] = 1.445305721320277 * z * (xx - yy);
+    Y[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+    const int nc = (degree + 1) * (degree + 1);
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (i < nc) {
+            acc[0] += Y[i] * (double)sh[3 * i + 0];
+            acc[1] += Y[i] * (double)sh[3 * i + 1];
+            acc[2] += Y[i] * (double)sh[3 * i + 2];
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double v = acc[c] + 0.5;
+        rgb[c] = (float)(v > 0.0 ? v : 0.0);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_project(ProjectArgs a, CamBatch cb) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int vloc = blockIdx.y;
+    const int64_t view = cb.view0 + vloc;
+    const DevCam &cam = cb.cams[vloc];
+    bool visible = false;
+    if (i < a.n) {
+        const int64_t o = view * a.n + i;
+        short4 rect = make_short4(-1, -1, -1, -1);
+        uint32_t dep = 0;
+        double R[9];
+        const float mu0 = a.centers[3 * i], mu1 = a.centers[3 * i + 1], mu2 = a.centers[3 * i + 2];
+        const float s0f = a.scales[3 * i], s1f = a.scales[3 * i + 1], s2f = a.scales[3 * i + 2];
+        float4 qv = reinterpret_cast<const float4 *>(a.rotations)[i];
+        float q4[4] = {qv.x, qv.y, qv.z, qv.w};
+        double Rc[9], S[9], m[3];
+        double zmin = 0.0;
+        bool keep = quat_rot(q4, R);
+        // ---------------- binning geometry (FP64, fixed order, bit-exact definition)
+        if (keep) {
+            double W[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) W[k] = (double)cam.R[k];
+            double dx = (double)mu0 - (double)cam.C[0];
+            double dy = (double)mu1 - (double)cam.C[1];
+            double dz = (double)mu2 - (double)cam.C[2];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) m[j] = W[0 * 3 + j] * dx + W[1 * 3 + j] * dy + W[2 * 3 + j] * dz;
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    Rc[3 * j + k] = W[0 * 3 + j] * R[0 * 3 + k] + W[1 * 3 + j] * R[1 * 3 + k] + W[2 * 3 + j] * R[2 * 3 + k];
+            const double s0 = s0f, s1 = s1f, s2 = s2f;
+            const double ss0 = s0 * s0, ss1 = s1 * s1, ss2 = s2 * s2;
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int l = 0; l < 3; ++l)
+                    S[3 * j + l] = Rc[3 * j + 0] * ss0 * Rc[3 * l + 0] + Rc[3 * j + 1] * ss1 * Rc[3 * l + 1]
+                                 + Rc[3 * j + 2] * ss2 * Rc[3 * l + 2];
+            const double sz = sqrt(S[8]);
+            zmin = m[2] - sz;
+            const double zmax = m[2] + sz;
+            if (!(zmax > 0.0)) keep = false;
+            const double fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
+            const double Wd = (double)cam.W, Hd = (double)cam.H;
+            const double pn[4][3] = {{fx, 0.0, cx}, {-fx, 0.0, Wd - cx}, {0.0, fy, cy}, {0.0, -fy, Hd - cy}};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double *nn = pn[k];
+                double dot = nn[0] * m[0] + nn[1] * m[1] + nn[2] * m[2];
+                double quad = nn[0] * (nn[0] * S[0] + nn[1] * S[1] + nn[2] * S[2])
+                            + nn[1] * (nn[0] * S[3] + nn[1] * S[4] + nn[2] * S[5])
+                            + nn[2] * (nn[0] * S[6] + nn[1] * S[7] + nn[2] * S[8]);
+                if (dot + sqrt(quad) < 0.0) keep = false;
+            }
+            if (keep) {
+                double xlo = -INFINITY, xhi = INFINITY, ylo = -INFINITY, yhi = INFINITY;
+                const double aq = m[2] * m[2] - S[8];
+                if (zmin > 0.0 && aq > 0.0) {
+                    double bx = m[0] * m[2] - S[2];
+                    double cxq = m[0] * m[0] - S[0];
+                    double discx = bx * bx - aq * cxq;
+                    if (!(discx > 0.0)) discx = 0.0;
+                    double rx = sqrt(discx);
+                    xlo = fx * ((bx - rx) / aq) + cx;
+                    xhi = fx * ((bx + rx) / aq) + cx;
+                    double by = m[1] * m[2] - S[5];
+                    double cyq = m[1] * m[1] - S[4];
+                    double discy = by * by - aq * cyq;
+                    if (!(discy > 0.0)) discy = 0.0;
+                    double ry = sqrt(discy);
+                    ylo = fy * ((by - ry) / aq) + cy;
+                    yhi = fy * ((by + ry) / aq) + cy;
+                }
+                const double eps = 1.0 / 256.0;
+                double px0 = ceil(xlo - 0.5 - eps), px1 = floor(xhi - 0.5 + eps);
+                double py0 = ceil(ylo - 0.5 - eps), py1 = floor(yhi - 0.5 + eps);
+                if (px0 < 0.0) px0 = 0.0;
+                if (py0 < 0.0) py0 = 0.0;
+                if (px1 > Wd - 1.0) px1 = Wd - 1.0;
+                if (py1 > Hd - 1.0) py1 = Hd - 1.0;
+                if (!(px0 <= px1) || !(py0 <= py1)) keep = false;
+                if (keep) {
+                    rect = make_short4((short)((int)px0 / kTile), (short)((int)py0 / kTile),
+                                       (short)((int)px1 / kTile), (short)((int)py1 / kTile));
+                    double smax = s0;
+                    if (s1 > smax) smax = s1;
+                    if (s2 > smax) smax = s2;
+                    double L = (double)cam.t_near;
+                    double l1 = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]) - smax;
+                    if (l1 > L) L = l1;
+                    if (zmin > L) L = zmin;
+                    dep = __float_as_uint(__double2float_rd(L));
+                }
+            }
+        }
+        a.rects[o] = rect;
+        a.depth[o] = dep;
+        visible = keep;
+        // ---------------- render record (only for visible pairs)
+        if (keep) {
+            const double s0 = s0f, s1 = s1f, s2 = s2f;
+            double smax = s0;
+            if (s1 > smax) smax = s1;
+            if (s2 > smax) smax = s2;
+            // silhouette conic in pixel space (tangent cone of the ellipsoid from the camera
+            // centre), used by K5 only as a conservative pre-test before the exact intersection
+            float cx0 = 0.f, cy0 = 0.f, ca = 0.f, cb2 = 0.f, cc = 0.f;
+            {
+                double P[9];
+                const double is0 = 1.0 / (s0 * s0), is1 = 1.0 / (s1 * s1), is2 = 1.0 / (s2 * s2);
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+#pragma unroll
+                    for (int l = 0; l < 3; ++l)
+                        P[3 * j + l] = Rc[3 * j] * is0 * Rc[3 * l] + Rc[3 * j + 1] * is1 * Rc[3 * l + 1]
+                                     + Rc[3 * j + 2] * is2 * Rc[3 * l + 2];
+                double w[3];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) w[j] = P[3 * j] * m[0] + P[3 * j + 1] * m[1] + P[3 * j + 2] * m[2];
+                const double c0 = m[0] * w[0] + m[1] * w[1] + m[2] * w[2] - 1.0;
+                if (zmin > 0.0 && c0 > 0.0) {
+                    double Q[9];
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+#pragma unroll
+                        for (int l = 0; l < 3; ++l) Q[3 * j + l] = c0 * P[3 * j + l] - w[j] * w[l];
+                    const double A00 = Q[0], A01 = Q[1], A11 = Q[4], l0 = Q[2], l1 = Q[5], kq = Q[8];
+                    const double det = A00 * A11 - A01 * A01;
+                    if (det > 0.0 && A00 > 0.0) {
+                        const double u0 = -(A11 * l0 - A01 * l1) / det;
+                        const double v0 = -(A00 * l1 - A01 * l0) / det;
+                        const double qc = kq + l0 * u0 + l1 * v0;
+                        if (qc < 0.0) {
+                            const double fx = cam.fx, fy = cam.fy;
+                            const double an = A00 / (-qc) / (fx * fx);
+                            const double bn = A01 / (-qc) / (fx * fy);
+                            const double cn = A11 / (-qc) / (fy * fy);
+                            const double x0 = fx * u0 + (double)cam.cx, y0 = fy * v0 + (double)cam.cy;
+                            const double lmax = 0.5 * (an + cn) + sqrt(0.25 * (an - cn) * (an - cn) + bn * bn);
+                            const double delta = ldexp(fabs(x0) + fabs(y0) + 1.0, -21);
+                            const double e = 1.0 + delta * sqrt(lmax);
+                            const double thr = e * e * (1.0 + 1e-5) + 1e-6;
+                            if (isfinite(x0) && isfinite(y0) && isfinite(thr) && fabs(x0) < 1e7 && fabs(y0) < 1e7) {
+                                cx0 = (float)x0;
+                                cy0 = (float)y0;
+                                ca = (float)(an / thr);
+                                cb2 = (float)(2.0 * bn / thr);
+                                cc = (float)(cn / thr);
+                            }
+                        }
+                    }
+                }
+            }
+            // camera-relative centre, compensated (hi + lo)
+            const double mw0 = (double)mu0 - (double)cam.C[0];
+            const double mw1 = (double)mu1 - (double)cam.C[1];
+            const double mw2 = (double)mu2 - (double)cam.C[2];
+            const float mh0 = (float)mw0, mh1 = (float)mw1, mh2 = (float)mw2;
+            const float ml0 = (float)(mw0 - (double)mh0), ml1 = (float)(mw1 - (double)mh1),
+                        ml2 = (float)(mw2 - (double)mh2);
+            // colour at dir = normalize(mu - C) (R14)
+            float rgb[3];
+            {
+                double nd = sqrt(mw0 * mw0 + mw1 * mw1 + mw2 * mw2);
+                double x = 0.0, y = 0.0, z = 1.0;
+                if (nd > 0.0) { x = mw0 / nd; y = mw1 / nd; z = mw2 / nd; }
+                sh_rgb(a.sh_degree, a.sh + 48 * i, x, y, z, rgb);
+            }
+            // whitening Wh = diag(1/s) R^T (world -> unit-sphere frame)
+            float Wh[9];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double sk = k == 0 ? s0 : (k == 1 ? s1 : s2);
+#pragma unroll
+                for (int j = 0; j < 3; ++j) Wh[3 * k + j] = (float)(R[3 * j + k] / sk);
+            }
+            float4 *rec = a.records + o * 16;
+            const float b2 = a.b2[i];
+            rec[kRecConic] = make_float4(cx0, cy0, ca, cb2);
+            rec[kRecConicRgb] = make_float4(cc, rgb[0], rgb[1], rgb[2]);
+            rec[kRecMh] = make_float4(mh0, mh1, mh2, b2);
+            rec[kRecMl] = make_float4(ml0, ml1, ml2, Wh[0]);
+            rec[kRecWh0] = make_float4(Wh[1], Wh[2], Wh[3], Wh[4]);
+            rec[kRecWh1] = make_float4(Wh[5], Wh[6], Wh[7], Wh[8]);
+            // MLP (Eq. 6) with the Eq. 5 normalisation folded in: W1' = omega W1 / ||s||_inf
+            const double om = (double)a.omega;
+            const float4 *w1v = reinterpret_cast<const float4 *>(a.w1 + (int64_t)24 * i);
+            const float4 *b1v = reinterpret_cast<const float4 *>(a.b1 + (int64_t)8 * i);
+            const float4 *w2v = reinterpret_cast<const float4 *>(a.w2 + (int64_t)8 * i);
+            float w1[24], b1[8];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                float4 t = w1v[k];
+                w1[4 * k] = t.x; w1[4 * k + 1] = t.y; w1[4 * k + 2] = t.z; w1[4 * k + 3] = t.w;
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                float4 t = b1v[k];
+                b1[4 * k] = t.x; b1[4 * k + 1] = t.y; b1[4 * k + 2] = t.z; b1[4 * k + 3] = t.w;
+            }
+            const double sc = om / smax;
+#pragma unroll
+            for (int k = 0; k < kHidden; ++k)
+                rec[kRecUnits + k] = make_float4((float)(sc * w1[3 * k]), (float)(sc * w1[3 * k + 1]),
+                                                 (float)(sc * w1[3 * k + 2]), (float)(om * b1[k]));
+            rec[kRecW2] = w2v[0];
+            rec[kRecW2 + 1] = w2v[1];
+        }
+    }
+    // warp-aggregated visible count
+    unsigned vb = __ballot_sync(0xffffffffu, visible);
+    if ((threadIdx.x & 31) == 0 && vb) atomicAdd(a.counters + kCntVisible, (unsigned long long)__popc(vb));
+}
+
+// Input validation: q nonzero, s > 0, every value finite.
+__global__ void k_validate(ProjectArgs a, int *bad) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    int b = 0;
+    float qn = 0.f;
+    for (int k = 0; k < 4; ++k) {
+        float q = a.rotations[4 * i + k];
+        if (!isfinite(q)) b = 1;
+        qn += q * q;
+    }
+    if (!(qn > 0.f)) b = 1;
+    for (int k = 0; k < 3; ++k) {
+        float s = a.scales[3 * i + k], c = a.centers[3 * i + k];
+        if (!(s > 0.f) || !isfinite(s) || !isfinite(c)) b = 1;
+    }
+    for (int k = 0; k < 24; ++k) if (!isfinite(a.w1[24 * i + k])) b = 1;
+    for (int k = 0; k < 8; ++k) if (!isfinite(a.b1[8 * i + k]) || !isfinite(a.w2[8 * i + k])) b = 1;
+    if (!isfinite(a.b2[i])) b = 1;
+    for (int k = 0; k < 48; ++k) if (!isfinite(a.sh[48 * i + k])) b = 1;
+    if (b) atomicExch(bad, 1);
+}
+
+}  // namespace
+
+cudaError_t launch_project(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
+    if (a.n == 0) return cudaSuccess;
+    dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)cams.nv);
+    k_project<<<grid, 256, 0, st>>>(a, cams);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const ProjectArgs &a, int *d_bad, cudaStream_t st) {
+    if (a.n == 0) return cudaSuccess;
+    k_validate<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a, d_bad);
+    return cudaGetLastError();
+}
+
+}  // namespace snp

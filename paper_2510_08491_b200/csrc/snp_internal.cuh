@@ -1,0 +1,120 @@
+// snp_internal.cuh -- shared definitions of the CUDA path (product code).
+// Nothing here is shared with oracle/: the two sides are independent.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/snp.h"
+
+namespace snp {
+
+constexpr int kTile = 16;                 // BASELINE north_star: 16x16 tiles (R18)
+constexpr int kHidden = 8;                // N_sigma = 8
+constexpr int kCamsPerLaunch = 32;        // cameras passed by value per launch
+constexpr int kRecordFloats = 64;         // one render record = 256 B = 16 float4
+
+// Camera as the kernels see it (by value in the launch parameters).
+struct DevCam {
+    float R[9];      // world-from-camera, row-major
+    float C[3];
+    float fx, fy, cx, cy;
+    int32_t W, H;
+    float t_near, t_far;
+};
+
+struct CamBatch {
+    int32_t view0;   // global index of cams[0]
+    int32_t nv;      // cameras in this launch
+    DevCam cams[kCamsPerLaunch];
+};
+
+// Render record of one (view, primitive), 16 float4:
+//  f4[0]  = x0, y0, a, 2b        silhouette conic, pixel space, margin folded in:
+//  f4[1]  = c, r, g, b           candidate iff a dx^2 + 2b dx dy + c dy^2 <= 1
+//  f4[2]  = mh.x, mh.y, mh.z, b2 m = mu - C (world) as hi + lo floats
+//  f4[3]  = ml.x, ml.y, ml.z, Wh00
+//  f4[4]  = Wh01, Wh02, Wh10, Wh11   Wh = diag(1/s) R^T (world -> unit-sphere frame)
+//  f4[5]  = Wh12, Wh20, Wh21, Wh22
+//  f4[6+k]= W1'_k.x, W1'_k.y, W1'_k.z, omega*b1_k   W1'_k = omega W1_k / ||s||_inf  (k < 8)
+//  f4[14] = W2_0..3, f4[15] = W2_4..7
+enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecWh0 = 4,
+                  kRecWh1 = 5, kRecUnits = 6, kRecW2 = 14 };
+
+// Device-side counters (one 64-bit slot each), see snp_stats.
+enum Counter { kCntVisible = 0, kCntDup = 1, kCntTested = 2, kCntCandidate = 3, kCntHit = 4,
+               kCntComposited = 5, kCntOverflow = 6, kCntCapOverflow = 7, kCntFallbackQueue = 8,
+               kNumCounters = 16 };
+
+struct ProjectArgs {
+    int64_t n;
+    int32_t sh_degree;
+    float omega;
+    const float *centers, *rotations, *scales, *w1, *b1, *w2, *b2, *sh;
+    int32_t tiles_x, tiles_y;
+    short4 *rects;          // [V*n] tile rect or (-1,-1,-1,-1)
+    uint32_t *depth;        // [V*n] fp32 bits of the depth lower bound
+    float4 *records;        // [V*n*16]
+    unsigned long long *counters;
+};
+
+// ---- host-side launchers (each .cu owns its kernels) ----
+cudaError_t launch_validate(const ProjectArgs &a, int *d_bad, cudaStream_t st);
+cudaError_t launch_project(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st);
+
+struct BinArgs {
+    int64_t n;              // primitives per view
+    int32_t n_views;
+    int32_t tiles_x, tiles_y, tile_bits;
+    int32_t row_begin, row_stride;
+    const short4 *rects;    // [V*n]
+    const uint32_t *depth;  // [V*n]
+    uint64_t *keys;         // [capacity]
+    uint32_t *vals;         // [capacity]
+    int64_t capacity;
+    uint32_t *partials;     // scan scratch [num_blocks + 1]
+    unsigned long long *counters;
+};
+int64_t bin_scan_blocks(int64_t items);
+cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st);   // counts + scan -> counters[kCntDup]
+cudaError_t launch_dup_only(const BinArgs &a, cudaStream_t st);     // needs launch_count_scan first
+cudaError_t launch_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
+                               int32_t tile_bits, int32_t tiles, uint32_t *ranges, int64_t n_slots,
+                               cudaStream_t st);
+
+struct SortScratch {
+    uint32_t *hist;         // [passes][256]
+    uint32_t *lookback;     // [passes][max_partitions][256]
+    uint32_t *tickets;      // [passes]
+    int64_t max_partitions;
+};
+int64_t sort_partition_size();
+size_t sort_scratch_words(int passes, int64_t max_partitions);
+// Sorts keys/vals (n read from counters[kCntDup], clamped to capacity) by bits
+// [0, 8*passes).  Ping-pongs between (k0,v0) and (k1,v1); returns in *final_idx
+// which buffer (0 or 1) holds the result.
+cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
+                            const unsigned long long *counters, int passes, SortScratch scratch,
+                            cudaStream_t st, int *final_idx);
+
+struct RenderArgs {
+    int32_t tiles_x, tiles_y, tiles_per_view;
+    int32_t tile_bits;
+    int32_t row_begin, row_stride, stripe_rows;
+    int64_t n;                     // primitives per view (record index = view*n + id)
+    const float4 *records;
+    const uint64_t *keys;          // sorted
+    const uint32_t *vals;          // sorted primitive ids
+    const uint32_t *ranges;        // [V*T][2]
+    float bg[3];
+    float t_floor;
+    int32_t pending_limit;
+    float *out;                    // [V][H][W][4]
+    uint32_t *fallback;            // [capacity] packed (view, pixel) of overflowed pixels
+    int64_t fallback_capacity;
+    unsigned long long *counters;
+};
+cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_t st);
+cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
+
+}  // namespace snp

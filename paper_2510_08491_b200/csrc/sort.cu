@@ -1,0 +1,231 @@
+// sort.cu -- K3: hand-written onesweep LSD radix sort of (u64 key, u32 value)
+// pairs, 8-bit digits, stable (BASELINE north_star: "a hand-written onesweep
+// LSD radix sort over 64-bit tile|depth keys").  Realises the tile-granular
+// part of "depth-sorted"; the exact per-ray order is restored in K5.
+//
+// Structure (one global histogram pass + one pass per digit):
+//   k_hist   : all digit histograms in one read of the keys (smem atomics)
+//   k_pass   : per partition of kPart keys (partition id from an atomic ticket,
+//              so every lower partition is already resident -> forward
+//              progress on sm_100a); warp-level match-any ranking (stable),
+//              decoupled look-back over partitions per digit, smem shuffle to
+//              block-sorted order, then coalesced-run scatter.
+#include "snp_internal.cuh"
+
+namespace snp {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kIpt = 12;                     // keys per thread
+constexpr int kPart = kThreads * kIpt;       // 3072 keys per partition
+constexpr int kWarpKeys = kPart / kWarps;    // 384 keys per warp (warp-striped)
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1u;
+
+__device__ __forceinline__ int64_t sort_n(const unsigned long long *counters, int64_t capacity) {
+    int64_t n = (int64_t)counters[kCntDup];
+    return n > capacity ? capacity : n;
+}
+
+__global__ void __launch_bounds__(kThreads) k_hist(const uint64_t *keys, int64_t capacity,
+                                                   const unsigned long long *counters, int passes,
+                                                   uint32_t *hist) {
+    __shared__ uint32_t h[8][256];
+    for (int i = threadIdx.x; i < passes * 256; i += kThreads) h[i >> 8][i & 255] = 0;
+    __syncthreads();
+    const int64_t n = sort_n(counters, capacity);
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+        const uint64_t k = keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += kThreads) {
+        uint32_t v = h[i >> 8][i & 255];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
+    return *reinterpret_cast<const volatile uint32_t *>(p);
+}
+
+__global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin,
+                                                   uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
+                                                   int64_t capacity, const unsigned long long *counters, int pass,
+                                                   const uint32_t *hist, uint32_t *lookback, uint32_t *tickets) {
+    __shared__ uint64_t s_keys[kPart];
+    __shared__ uint32_t s_vals[kPart];
+    __shared__ uint32_t s_wh[kWarps][256];     // per-warp digit counts -> per-warp exclusive offsets
+    __shared__ uint32_t s_goff[256];           // global start of digit (over all keys)
+    __shared__ uint32_t s_bstart[256];         // block-local start of digit
+    __shared__ uint32_t s_excl[256];           // keys of this digit in earlier partitions
+    __shared__ uint32_t s_scan[kWarps];
+    __shared__ int s_part;
+
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int shift = 8 * pass;
+    if (threadIdx.x == 0) s_part = (int)atomicAdd(tickets + pass, 1u);
+    for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&s_wh[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t n = sort_n(counters, capacity);
+    const int64_t part = s_part;
+    const int64_t nparts = (n + kPart - 1) / kPart;
+    if (part >= nparts) return;
+    const int64_t pbase = part * kPart;
+
+    // ---- load (warp-striped: item k of lane l is key pbase + wid*384 + k*32 + l)
+    uint64_t key[kIpt];
+    uint32_t val[kIpt];
+    uint32_t rank[kIpt];
+#pragma unroll
+    for (int k = 0; k < kIpt; ++k) {
+        const int64_t idx = pbase + wid * kWarpKeys + k * 32 + lane;
+        if (idx < n) {
+            key[k] = kin[idx];
+            val[k] = vin[idx];
+        } else {
+            key[k] = ~0ull;  // digit 255, placed after every valid key of this partition
+            val[k] = 0;
+        }
+    }
+    // ---- stable warp ranking with match-any
+    const uint32_t lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < kIpt; ++k) {
+        const uint32_t d = (uint32_t)(key[k] >> shift) & 255u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader) {
+            base = s_wh[wid][d];
+            s_wh[wid][d] = base + __popc(peers);
+        }
+        base = __shfl_sync(0xffffffffu, base, leader);
+        rank[k] = base + __popc(peers & lt_mask);
+        __syncwarp();
+    }
+    __syncthreads();
+    // ---- per digit: exclusive over warps, block count, block-local digit start
+    const int d = threadIdx.x;  // kThreads == 256 == radix
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        uint32_t c = s_wh[w][d];
+        s_wh[w][d] = cnt;
+        cnt += c;
+    }
+    // invalid tail keys (digit 255) must not be published
+    if (d == 255) {
+        const int64_t valid = n - pbase < kPart ? n - pbase : kPart;
+        cnt -= (uint32_t)(kPart - valid);
+    }
+    // publish aggregate early, then decoupled look-back
+    uint32_t *lb = lookback + ((int64_t)pass * 0) ;  // caller offsets lookback per pass
+    if (part == 0) {
+        atomicExch(lb + d, kFlagInc | cnt);
+        s_excl[d] = 0;
+    } else {
+        atomicExch(lb + part * 256 + d, kFlagAgg | cnt);
+        uint32_t sum = 0;
+        int64_t q = part - 1;
+        while (true) {
+            uint32_t v = ld_volatile(lb + q * 256 + d);
+            if ((v & ~kValMask) == 0) continue;          // not yet published: spin
+            sum += v & kValMask;
+            if (v & kFlagInc) break;
+            --q;
+        }
+        atomicExch(lb + part * 256 + d, kFlagInc | (sum + cnt));
+        s_excl[d] = sum;
+    }
+    // block-wide exclusive scan of cnt over digits (d = threadIdx.x); the tail
+    // correction above only shrinks digit 255, the last, so starts are unaffected
+    {
+        uint32_t x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_scan[wid] = x;
+        __syncthreads();
+        uint32_t before = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) before += (w < wid) ? s_scan[w] : 0u;
+        s_bstart[d] = before + x - cnt;
+        // global digit offsets: exclusive scan of hist[pass][*]
+        const uint32_t hv = hist[pass * 256 + d];
+        uint32_t y2 = hv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t z = __shfl_up_sync(0xffffffffu, y2, o);
+            if (lane >= o) y2 += z;
+        }
+        __syncthreads();
+        if (lane == 31) s_scan[wid] = y2;
+        __syncthreads();
+        uint32_t b2 = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) b2 += (w < wid) ? s_scan[w] : 0u;
+        s_goff[d] = b2 + y2 - hv;
+    }
+    __syncthreads();
+    // ---- shuffle into block-sorted order in shared memory
+#pragma unroll
+    for (int k = 0; k < kIpt; ++k) {
+        const uint32_t dd = (uint32_t)(key[k] >> shift) & 255u;
+        const uint32_t pos = s_bstart[dd] + s_wh[wid][dd] + rank[k];
+        s_keys[pos] = key[k];
+        s_vals[pos] = val[k];
+    }
+    __syncthreads();
+    // ---- scatter runs of equal digits to their global positions
+    const int valid = (int)(n - pbase < kPart ? n - pbase : kPart);
+    for (int i = threadIdx.x; i < valid; i += kThreads) {
+        const uint64_t kk = s_keys[i];
+        const uint32_t dd = (uint32_t)(kk >> shift) & 255u;
+        const uint32_t dest = s_goff[dd] + s_excl[dd] + (uint32_t)i - s_bstart[dd];
+        kout[dest] = kk;
+        vout[dest] = s_vals[i];
+    }
+}
+
+}  // namespace
+
+int64_t sort_partition_size() { return kPart; }
+
+size_t sort_scratch_words(int passes, int64_t max_partitions) {
+    return (size_t)passes * 256 + (size_t)passes * (size_t)max_partitions * 256 + (size_t)passes;
+}
+
+cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
+                            const unsigned long long *counters, int passes, SortScratch sc,
+                            cudaStream_t st, int *final_idx) {
+    *final_idx = 0;
+    if (capacity == 0 || passes == 0) return cudaSuccess;
+    const int64_t maxp = (capacity + kPart - 1) / kPart;
+    if (maxp > sc.max_partitions) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 256 * passes, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * 256 * (size_t)maxp * passes, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(sc.tickets, 0, sizeof(uint32_t) * passes, st);
+    if (e != cudaSuccess) return e;
+    int64_t hb = (capacity + kThreads * 16 - 1) / (kThreads * 16);
+    if (hb > 148 * 4) hb = 148 * 4;
+    k_hist<<<(unsigned)hb, kThreads, 0, st>>>(k0, capacity, counters, passes, sc.hist);
+    uint64_t *kin = k0, *kout = k1;
+    uint32_t *vin = v0, *vout = v1;
+    for (int p = 0; p < passes; ++p) {
+        k_pass<<<(unsigned)maxp, kThreads, 0, st>>>(kin, vin, kout, vout, capacity, counters, p, sc.hist,
+                                                    sc.lookback + (size_t)p * (size_t)maxp * 256, sc.tickets);
+        uint64_t *tk = kin; kin = kout; kout = tk;
+        uint32_t *tv = vin; vin = vout; vout = tv;
+    }
+    *final_idx = passes & 1;
+    return cudaGetLastError();
+}
+
+}  // namespace snp

@@ -1,0 +1,233 @@
+"""Thin ctypes binding of ``include/snp.h`` (argument marshalling only).
+
+Every step of the hot path runs in ``libsnp.so`` (hand-written CUDA for
+sm_100a); this module only converts arrays/tensors to pointers, cameras and
+options to the C structs, and statuses to exceptions.  There is no CPU
+fallback: if the library is missing or no CUDA device is present the calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsnp.so")
+
+SNP_OK = 0
+STATUS = {0: "SNP_OK", 1: "SNP_ERR_INVALID_ARGUMENT", 2: "SNP_ERR_OUT_OF_MEMORY", 3: "SNP_ERR_CUDA",
+          4: "SNP_ERR_UNSUPPORTED", 5: "SNP_ERR_BAD_STATE", 6: "SNP_ERR_CAPACITY"}
+SNP_MEM_HOST = 0
+SNP_MEM_DEVICE = 1
+
+EXPORTS = ("snp_version", "snp_create_scene", "snp_project", "snp_bin_sort", "snp_render",
+           "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
+           "snp_set_pending_limit")
+
+
+class SnpError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class SceneDesc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_hidden", C.c_int32), ("sh_degree", C.c_int32),
+                ("omega", C.c_float), ("memory", C.c_int32)] + \
+               [(f, C.c_void_p) for f in ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh")]
+
+
+class Camera(C.Structure):
+    _fields_ = [("R_wc", C.c_float * 9), ("C_w", C.c_float * 3), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("t_near", C.c_float), ("t_far", C.c_float)]
+
+
+class RenderOpts(C.Structure):
+    _fields_ = [("background", C.c_float * 3), ("transmittance_floor", C.c_float),
+                ("tile_row_begin", C.c_int32), ("tile_row_stride", C.c_int32),
+                ("out_memory", C.c_int32), ("sync_check", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in ("n_visible", "n_dup", "key_capacity", "tested_pairs",
+                                          "candidate_pairs", "hit_pairs", "composited",
+                                          "overflow_pixels", "capacity_overflow")]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Loads libsnp.so; raises if it has not been built (no fallback exists)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+                                  "(there is no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            vp = C.c_void_p
+            L.snp_version.restype = C.c_char_p
+            L.snp_last_error.restype = C.c_char_p
+            L.snp_create_scene.argtypes = [C.POINTER(SceneDesc), C.c_int, vp, C.POINTER(vp)]
+            L.snp_project.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp]
+            L.snp_bin_sort.argtypes = [vp, C.POINTER(RenderOpts), vp]
+            L.snp_render.argtypes = [vp, C.POINTER(RenderOpts), vp, vp]
+            L.snp_render_views.argtypes = [vp, C.POINTER(Camera), C.c_int32, C.POINTER(RenderOpts), vp, vp]
+            L.snp_destroy.argtypes = [vp]
+            L.snp_get_binning.argtypes = [vp, vp, vp, vp, vp, C.c_int64, C.POINTER(C.c_int64), vp, vp]
+            L.snp_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
+            L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
+            for f in EXPORTS:
+                if f not in ("snp_version", "snp_last_error"):
+                    getattr(L, f).restype = C.c_int
+            _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != SNP_OK:
+        raise SnpError(status, lib().snp_last_error().decode())
+
+
+def _ptr(x):
+    """Pointer of a numpy array (host) or a torch tensor (host or device)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _is_device(x):
+    return hasattr(x, "is_cuda") and x.is_cuda
+
+
+FIELDS = ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh")
+
+
+def create_scene(scene, device=0, stream=None, n_hidden=8, sh_degree=None, omega=None):
+    """``scene`` has float32 C-contiguous arrays ``centers [n,3] ... sh [n,16,3]``
+    (numpy = host memory, torch CUDA tensors = device memory)."""
+    arrs = []
+    for f in FIELDS:
+        a = getattr(scene, f)
+        if not _is_device(a):
+            a = np.ascontiguousarray(a, dtype=np.float32)
+        else:
+            a = a.contiguous().float()
+        arrs.append(a)
+    mem = SNP_MEM_DEVICE if _is_device(arrs[0]) else SNP_MEM_HOST
+    n = int(arrs[0].shape[0])
+    desc = SceneDesc(n, n_hidden, int(getattr(scene, "sh_degree", 3) if sh_degree is None else sh_degree),
+                     float(getattr(scene, "omega", 30.0) if omega is None else omega), mem,
+                     *[_ptr(a) for a in arrs])
+    h = C.c_void_p()
+    _check(lib().snp_create_scene(C.byref(desc), int(device), _stream(stream), C.byref(h)))
+    return h.value
+
+
+def make_cameras(cams):
+    arr = (Camera * len(cams))()
+    for i, c in enumerate(cams):
+        R = np.asarray(c.R_wc, np.float32).reshape(9)
+        Cw = np.asarray(c.C_w, np.float32).reshape(3)
+        arr[i] = Camera((C.c_float * 9)(*R.tolist()), (C.c_float * 3)(*Cw.tolist()), float(c.fx), float(c.fy),
+                        float(c.cx), float(c.cy), int(c.width), int(c.height), float(c.t_near), float(c.t_far))
+    return arr
+
+
+def make_opts(background=(0.0, 0.0, 0.0), transmittance_floor=1e-4, tile_row_begin=0, tile_row_stride=1,
+              out_memory=SNP_MEM_DEVICE, sync_check=1):
+    return RenderOpts((C.c_float * 3)(*[float(b) for b in background]), float(transmittance_floor),
+                      int(tile_row_begin), int(tile_row_stride), int(out_memory), int(sync_check))
+
+
+def project(h, cams, stream=None):
+    arr = cams if isinstance(cams, C.Array) else make_cameras(cams)
+    _check(lib().snp_project(h, arr, len(arr), _stream(stream)))
+
+
+def bin_sort(h, opts, stream=None):
+    _check(lib().snp_bin_sort(h, C.byref(opts), _stream(stream)))
+
+
+def render(h, opts, out, stream=None):
+    _check(lib().snp_render(h, C.byref(opts), _ptr(out), _stream(stream)))
+
+
+def render_views(h, cams, opts, out, stream=None):
+    arr = cams if isinstance(cams, C.Array) else make_cameras(cams)
+    _check(lib().snp_render_views(h, arr, len(arr), C.byref(opts), _ptr(out), _stream(stream)))
+
+
+def destroy(h):
+    if h:
+        _check(lib().snp_destroy(h))
+
+
+def set_pending_limit(h, k):
+    _check(lib().snp_set_pending_limit(h, int(k)))
+
+
+def get_stats(h, stream=None):
+    s = Stats()
+    _check(lib().snp_get_stats(h, C.byref(s), _stream(stream)))
+    return {f: int(getattr(s, f)) for f, _ in Stats._fields_}
+
+
+def get_binning(h, n, n_views, tiles, stream=None):
+    """Host copies of (rects [V*n,4] int32, depth [V*n] u32, sorted keys, sorted ids, ranges [V*tiles,2])."""
+    L = lib()
+    rects = np.zeros((n_views * n, 4), np.int32)
+    depth = np.zeros(n_views * n, np.uint32)
+    ranges = np.zeros((n_views * tiles, 2), np.uint32)
+    nd = C.c_int64(0)
+    _check(L.snp_get_binning(h, rects.ctypes.data, depth.ctypes.data, None, None, 0, C.byref(nd),
+                             ranges.ctypes.data, _stream(stream)))
+    m = max(int(nd.value), 0)
+    keys = np.zeros(max(m, 1), np.uint64)
+    ids = np.zeros(max(m, 1), np.uint32)
+    _check(L.snp_get_binning(h, None, None, keys.ctypes.data, ids.ctypes.data, m, C.byref(nd), None,
+                             _stream(stream)))
+    return rects, depth, keys[:m], ids[:m], ranges
+
+
+class Renderer:
+    """Convenience owner of one scene handle (torch tensors for device outputs)."""
+
+    def __init__(self, scene, device=0, stream=None):
+        self.h = create_scene(scene, device, stream)
+        self.device = device
+
+    def render(self, cams, out, background=(0, 0, 0), transmittance_floor=1e-4, stream=None, **kw):
+        opts = make_opts(background, transmittance_floor, **kw)
+        render_views(self.h, cams, opts, out, stream)
+        return out
+
+    def stats(self, stream=None):
+        return get_stats(self.h, stream)
+
+    def close(self):
+        if self.h:
+            destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
