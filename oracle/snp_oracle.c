@@ -561,13 +561,17 @@ int orc_bin_one(const double mu[3], const double qin[4], const double s[3], cons
     prect[0] = (int32_t)px0; prect[1] = (int32_t)py0; prect[2] = (int32_t)px1; prect[3] = (int32_t)py1;
     rect[0] = prect[0] / ORC_TILE; rect[1] = prect[1] / ORC_TILE;
     rect[2] = prect[2] / ORC_TILE; rect[3] = prect[3] / ORC_TILE;
-    /* depth lower bound: t_in >= t_near, t_in >= |m| - smax, t_in >= z_min (R19) */
-    double smax = s[0];
-    if (s[1] > smax) smax = s[1];
-    if (s[2] > smax) smax = s[2];
+    /* depth lower bound L <= t_in of every ray (R19): t_in >= t_near, t_in >= z_min, and */
     double L = cam->t_near;
-    double l1 = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]) - smax;
-    if (l1 > L) L = l1;
+    /* t >= u.x >= u.m - sqrt(u^T S u) for u = m/|m| (support function of E) */
+    double nm = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]);
+    double mSm = m[0] * (m[0] * S[0] + m[1] * S[1] + m[2] * S[2])
+               + m[1] * (m[0] * S[3] + m[1] * S[4] + m[2] * S[5])
+               + m[2] * (m[0] * S[6] + m[1] * S[7] + m[2] * S[8]);
+    if (nm > 0.0 && mSm >= 0.0) {
+        double l1 = nm - sqrt(mSm) / nm;
+        if (l1 > L) L = l1;
+    }
     if (zmin > L) L = zmin;
     *depth = orc_f32_bits_round_down(L);
     if (Lout) *Lout = L;

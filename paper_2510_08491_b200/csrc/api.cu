@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -83,6 +84,7 @@ struct snp_scene_s {
     // render
     DevBuf<uint32_t> fallback;
     int64_t fallback_capacity = 0;
+    DevBuf<float4> fb_scratch;
     DevBuf<float> host_out_staging;
     int32_t pending_limit = 8;
     // counters
@@ -377,6 +379,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
         SNP_CUDA(s->fallback.ensure((size_t)fb_cap * 2));
         s->fallback_capacity = fb_cap;
     }
+    SNP_CUDA(s->fb_scratch.ensure((size_t)fallback_scratch_float4()));
     SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0, sizeof(unsigned long long) * 5, st));
     SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntFallbackQueue, 0, sizeof(unsigned long long), st));
     RenderArgs a{};
@@ -395,9 +398,14 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     for (int c = 0; c < 3; ++c) a.bg[c] = opts->background[c];
     a.t_floor = opts->transmittance_floor;
     a.pending_limit = s->pending_limit;
+    {
+        const char *dbg = std::getenv("SNP_DEBUG");
+        a.debug_flags = dbg ? std::atoi(dbg) : 0;
+    }
     a.out = dout;
     a.fallback = s->fallback.p;
     a.fallback_capacity = s->fallback_capacity;
+    a.fb_scratch = s->fb_scratch.p;
     a.counters = s->counters.p;
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
@@ -436,6 +444,7 @@ snp_status snp_destroy(snp_scene s) {
     s->sort_scratch.release();
     s->ranges.release();
     s->fallback.release();
+    s->fb_scratch.release();
     s->host_out_staging.release();
     s->counters.release();
     s->flag.release();

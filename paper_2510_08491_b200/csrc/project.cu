@@ -156,12 +156,17 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a, CamBatch cb) {
                 if (keep) {
                     rect = make_short4((short)((int)px0 / kTile), (short)((int)py0 / kTile),
                                        (short)((int)px1 / kTile), (short)((int)py1 / kTile));
-                    double smax = s0;
-                    if (s1 > smax) smax = s1;
-                    if (s2 > smax) smax = s2;
+                    // depth lower bound L <= t_in of every ray (R19)
                     double L = (double)cam.t_near;
-                    double l1 = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]) - smax;
-                    if (l1 > L) L = l1;
+                    /* t >= u.x >= u.m - sqrt(u^T S u) for u = m/|m| (support function of E) */
+                    double nm = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]);
+                    double mSm = m[0] * (m[0] * S[0] + m[1] * S[1] + m[2] * S[2])
+                               + m[1] * (m[0] * S[3] + m[1] * S[4] + m[2] * S[5])
+                               + m[2] * (m[0] * S[6] + m[1] * S[7] + m[2] * S[8]);
+                    if (nm > 0.0 && mSm >= 0.0) {
+                        double l1 = nm - sqrt(mSm) / nm;
+                        if (l1 > L) L = l1;
+                    }
                     if (zmin > L) L = zmin;
                     dep = __float_as_uint(__double2float_rd(L));
                 }

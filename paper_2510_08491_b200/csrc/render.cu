@@ -26,15 +26,25 @@ namespace snp {
 namespace {
 
 constexpr int kThreads = 256;       // one 16x16 tile, one pixel per thread
+constexpr int kWarps = kThreads / 32;
 constexpr int kBatch = 64;          // records per stage
-constexpr int kStages = 3;
+constexpr int kStages = 2;
 constexpr int kPendMax = 8;         // per-pixel pending buffer (max occupancy 4-10)
+constexpr int kFbGrid = 148 * 2;    // K6 blocks
+constexpr int kFbCap = 1024;        // K6 stored hits per warp
 
 struct __align__(16) Smem {
-    float4 rec[kStages][kBatch][16];          // 48 KB
+    float4 rec[kStages][kBatch][16];          // 32 KB of records (TMA bulk-staged)
     float L[kStages][kBatch + 1];             // depth lower bounds (+ the next batch's first)
     uint32_t id[kStages][kBatch];
     unsigned long long bar[kStages];
+    uint32_t submask[kWarps][2];              // records whose conic box touches warp w's 8x4 block
+    uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs:
+    uint8_t ql[kWarps][64];                   //   (record slot j, owner lane)
+    float r_th[kWarps][32], r_tl[kWarps][32], r_k[kWarps][32], r_L[kWarps][32];
+    float r_r[kWarps][32], r_g[kWarps][32], r_b[kWarps][32];
+    uint32_t r_id[kWarps][32], r_j[kWarps][32];
+    uint32_t own[kWarps][32];                 // per owner lane: mask of result slots it owns
     float p_thi[kPendMax][kThreads];          // pending hits, SoA, column per thread
     float p_tlo[kPendMax][kThreads];
     float p_kap[kPendMax][kThreads];
@@ -181,7 +191,7 @@ struct PixelState {
     uint32_t composited;
 };
 
-// Emit every pending hit with t_in < L (strictly), smallest first.
+// Emit every pending hit with t_in < L (strictly), smallest first (Eq. 4 front to back).
 __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_floor) {
     const int tid = threadIdx.x;
     while (ps.npend > 0) {
@@ -203,10 +213,48 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_
     }
 }
 
+// Insert one hit into the pixel's pending buffer (kept in descending (t_in, id)
+// order, smallest at npend-1).  L = key of the hit's own entry: every hit not yet
+// seen has t_in >= L, so pending hits below L may be emitted to make room.
+__device__ __forceinline__ void insert_hit(Smem &sm, PixelState &ps, float th, float tl, uint32_t id, float kap,
+                                           float r, float g, float b, float L, int plimit, float t_floor) {
+    const int tid = threadIdx.x;
+    if (ps.npend >= plimit) emit(sm, ps, L, t_floor);
+    if (ps.done) return;
+    if (ps.npend >= plimit) {
+        ps.overflow = true;   // K6 re-renders this pixel exactly
+        ps.done = true;
+        return;
+    }
+    int k = ps.npend;
+    while (k > 0) {
+        const float ph = sm.p_thi[k - 1][tid], pl = sm.p_tlo[k - 1][tid];
+        const uint32_t pid = sm.p_id[k - 1][tid];
+        if (!before(ph, pl, pid, th, tl, id)) break;
+        sm.p_thi[k][tid] = ph;
+        sm.p_tlo[k][tid] = pl;
+        sm.p_id[k][tid] = pid;
+        sm.p_kap[k][tid] = sm.p_kap[k - 1][tid];
+        sm.p_r[k][tid] = sm.p_r[k - 1][tid];
+        sm.p_g[k][tid] = sm.p_g[k - 1][tid];
+        sm.p_b[k][tid] = sm.p_b[k - 1][tid];
+        --k;
+    }
+    sm.p_thi[k][tid] = th;
+    sm.p_tlo[k][tid] = tl;
+    sm.p_id[k][tid] = id;
+    sm.p_kap[k][tid] = kap;
+    sm.p_r[k][tid] = r;
+    sm.p_g[k][tid] = g;
+    sm.p_b[k][tid] = b;
+    ++ps.npend;
+}
+
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     const int vloc = blockIdx.y;
     const int64_t view = cb.view0 + vloc;
     const DevCam &cam = cb.cams[vloc];
@@ -226,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    // producer: warps 0-1 stage batch b into slot b % kStages
+    // producer (warps 0-1): one cp.async.bulk per 256-byte record into slot b % kStages
     auto issue = [&](int b) {
         const int slot = b % kStages;
         const uint32_t e0 = beg + (uint32_t)b * kBatch;
@@ -245,14 +293,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             sm.L[slot][cnt] = nx < end ? __uint_as_float((uint32_t)a.keys[nx]) : INFINITY;
         }
     };
-    int issued = nb < kStages ? nb : kStages;   // batches issued so far (uniform)
+    int issued = nb < kStages ? nb : kStages;
     if (tid < 64)
         for (int b = 0; b < issued; ++b) issue(b);
 
-    const Ray ray = inside ? make_ray(cam, x, y) : Ray{0, 0, 1, 0, 0, 0, 0, 0};
+    const Ray ray = inside ? make_ray(cam, x, y) : Ray{0, 0, 1, 0, 0, 0, cam.t_near, cam.t_far};
     const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
+    // this thread's pre-pass pairs: record pj against the 8x4 blocks of warps ps0 and ps0 + 4
+    const int pj = tid & 63, ps0 = tid >> 6;
+    const float bx0 = (float)(tx * kTile + (ps0 & 1) * 8) + 0.5f, by0 = (float)(ty * kTile + (ps0 >> 1) * 4) + 0.5f;
+    const float by1 = by0 + 8.0f;  // block ps0 + 4 sits two block-rows (8 px) lower
     PixelState ps{1.f, 0.f, 0.f, 0.f, 0, !inside, false, 0u};
-    uint32_t tested_end = end;       // entries visited by this pixel = tested_end - beg
+    uint32_t tested_end = end;
     uint32_t n_cand = 0, n_hit = 0;
     const int plimit = a.pending_limit;
     __syncthreads();
@@ -263,50 +315,124 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         mbar_wait(&sm.bar[slot], (uint32_t)((b / kStages) & 1));
         const uint32_t e0 = beg + (uint32_t)b * kBatch;
         const int cnt = (int)min((uint32_t)kBatch, end - e0);
-        for (int j = 0; j < cnt; ++j) {
-            const float4 *rec = &sm.rec[slot][j][0];
-            const float4 c0 = rec[kRecConic];
-            const float cc = rec[kRecConicRgb].x;
-            const float dx = pxf - c0.x, dy = pyf - c0.y;
-            const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
-            const bool cand = !ps.done && q <= 1.0f;
-            if (__any_sync(0xffffffffu, cand)) {
-                float th, tl, kap;
-                bool hit = false;
-                if (cand) {
-                    ++n_cand;
-                    hit = exact_hit(rec, ray, th, tl, kap);
-                }
-                if (hit) {
-                    ++n_hit;
-                    const uint32_t id = sm.id[slot][j];
-                    if (ps.npend >= plimit) emit(sm, ps, sm.L[slot][j], a.t_floor);
-                    if (!ps.done && ps.npend >= plimit) {
-                        ps.overflow = true;
-                        ps.done = true;
-                    }
-                    if (!ps.done) {
-                        int k = ps.npend;
-                        while (k > 0) {   // keep descending order: smallest at npend-1
-                            const float ph = sm.p_thi[k - 1][tid], pl = sm.p_tlo[k - 1][tid];
-                            const uint32_t pid = sm.p_id[k - 1][tid];
-                            if (!before(ph, pl, pid, th, tl, id)) break;
-                            sm.p_thi[k][tid] = ph; sm.p_tlo[k][tid] = pl; sm.p_id[k][tid] = pid;
-                            sm.p_kap[k][tid] = sm.p_kap[k - 1][tid];
-                            sm.p_r[k][tid] = sm.p_r[k - 1][tid];
-                            sm.p_g[k][tid] = sm.p_g[k - 1][tid];
-                            sm.p_b[k][tid] = sm.p_b[k - 1][tid];
-                            --k;
-                        }
-                        const float4 rgb = rec[kRecConicRgb];
-                        sm.p_thi[k][tid] = th; sm.p_tlo[k][tid] = tl; sm.p_id[k][tid] = id;
-                        sm.p_kap[k][tid] = kap;
-                        sm.p_r[k][tid] = rgb.y; sm.p_g[k][tid] = rgb.z; sm.p_b[k][tid] = rgb.w;
-                        ++ps.npend;
-                    }
-                    if (ps.done && tested_end == end) tested_end = e0 + j + 1;
+        // ---- pre-pass: which records can touch each warp's 8x4 pixel block
+        {
+            bool t0 = false, t1 = false;
+            if (pj < cnt) {
+                const float4 c0 = sm.rec[slot][pj][kRecConic];
+                const float cc = sm.rec[slot][pj][kRecConicRgb].x;
+                const float hb = 0.5f * c0.w;
+                const float det = fmaf(c0.z, cc, -hb * hb);
+                if (det > 0.f) {
+                    const float rx = sqrtf(cc / det) * 1.001f + 1e-3f;
+                    const float ry = sqrtf(c0.z / det) * 1.001f + 1e-3f;
+                    const bool ox = c0.x + rx >= bx0 && c0.x - rx <= bx0 + 7.0f;
+                    t0 = ox && c0.y + ry >= by0 && c0.y - ry <= by0 + 3.0f;
+                    t1 = ox && c0.y + ry >= by1 && c0.y - ry <= by1 + 3.0f;
+                } else {
+                    t0 = t1 = true;   // no conic (straddles the camera plane / camera inside)
                 }
             }
+            if (a.debug_flags & 1) t0 = t1 = pj < cnt;
+            const uint32_t m0 = __ballot_sync(0xffffffffu, t0);
+            const uint32_t m1 = __ballot_sync(0xffffffffu, t1);
+            if (lane == 0) {
+                sm.submask[ps0][wid & 1] = m0;
+                sm.submask[ps0 + 4][wid & 1] = m1;
+            }
+        }
+        __syncthreads();
+        // ---- per warp: candidate pairs -> compaction queue -> 32-wide exact rounds
+        if (!__all_sync(0xffffffffu, ps.done)) {
+            unsigned long long m = (unsigned long long)sm.submask[wid][0] |
+                                   ((unsigned long long)sm.submask[wid][1] << 32);
+            int qcount = 0;
+            auto round = [&](int n) {
+                __syncwarp();
+                const bool valid = lane < n;
+                const int owner = valid ? sm.ql[wid][lane] : lane;
+                const int j = valid ? sm.qj[wid][lane] : 0;
+                Ray ro;
+                ro.dhx = __shfl_sync(0xffffffffu, ray.dhx, owner);
+                ro.dhy = __shfl_sync(0xffffffffu, ray.dhy, owner);
+                ro.dhz = __shfl_sync(0xffffffffu, ray.dhz, owner);
+                ro.dlx = __shfl_sync(0xffffffffu, ray.dlx, owner);
+                ro.dly = __shfl_sync(0xffffffffu, ray.dly, owner);
+                ro.dlz = __shfl_sync(0xffffffffu, ray.dlz, owner);
+                ro.t_near = cam.t_near;   // uniform: lanes outside the image carry a dummy ray
+                ro.t_far = cam.t_far;
+                sm.own[wid][lane] = 0u;
+                bool hit = false;
+                if (valid) {
+                    float th, tl, kap;
+                    const float4 *rec = &sm.rec[slot][j][0];
+                    hit = exact_hit(rec, ro, th, tl, kap);
+                    if (hit) {
+                        const float4 rgb = rec[kRecConicRgb];
+                        sm.r_th[wid][lane] = th;
+                        sm.r_tl[wid][lane] = tl;
+                        sm.r_k[wid][lane] = kap;
+                        sm.r_L[wid][lane] = sm.L[slot][j];
+                        sm.r_r[wid][lane] = rgb.y;
+                        sm.r_g[wid][lane] = rgb.z;
+                        sm.r_b[wid][lane] = rgb.w;
+                        sm.r_id[wid][lane] = sm.id[slot][j];
+                        sm.r_j[wid][lane] = (uint32_t)j;
+                    }
+                }
+                const uint32_t peers = __match_any_sync(0xffffffffu, hit ? owner : 64 + lane);
+                __syncwarp();
+                if (hit && lane == __ffs(peers) - 1) sm.own[wid][owner] = peers;
+                __syncwarp();
+                uint32_t mine = sm.own[wid][lane];
+                n_hit += __popc(mine);
+                while (mine) {   // in queue order == record order for this pixel
+                    const int k = __ffs(mine) - 1;
+                    mine &= mine - 1u;
+                    if (ps.done) continue;
+                    insert_hit(sm, ps, sm.r_th[wid][k], sm.r_tl[wid][k], sm.r_id[wid][k], sm.r_k[wid][k],
+                               sm.r_r[wid][k], sm.r_g[wid][k], sm.r_b[wid][k], sm.r_L[wid][k], plimit,
+                               a.t_floor);
+                    if (ps.done && tested_end == end) tested_end = e0 + sm.r_j[wid][k] + 1;
+                }
+                __syncwarp();
+            };
+            while (m) {
+                const int j = __ffsll(m) - 1;
+                m &= m - 1ull;
+                const float4 c0 = sm.rec[slot][j][kRecConic];
+                const float cc = sm.rec[slot][j][kRecConicRgb].x;
+                const float dx = pxf - c0.x, dy = pyf - c0.y;
+                const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
+                const bool cand = !ps.done && q <= 1.0f;
+                const uint32_t cm = __ballot_sync(0xffffffffu, cand);
+                if (cm) {
+                    if (cand) {
+                        const int pos = qcount + __popc(cm & lt_mask);
+                        sm.qj[wid][pos] = (uint8_t)j;
+                        sm.ql[wid][pos] = (uint8_t)lane;
+                        ++n_cand;
+                    }
+                    qcount += __popc(cm);
+                    if (qcount >= 32) {
+                        round(32);
+                        const int rem = qcount - 32;
+                        uint8_t vj = 0, vl = 0;
+                        if (lane < rem) {
+                            vj = sm.qj[wid][32 + lane];
+                            vl = sm.ql[wid][32 + lane];
+                        }
+                        __syncwarp();
+                        if (lane < rem) {
+                            sm.qj[wid][lane] = vj;
+                            sm.ql[wid][lane] = vl;
+                        }
+                        __syncwarp();
+                        qcount = rem;
+                    }
+                }
+            }
+            if (qcount > 0) round(qcount);
         }
         if (!ps.done) {
             emit(sm, ps, sm.L[slot][cnt], a.t_floor);
@@ -334,14 +460,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 a.fallback[2 * slot + 1] = (uint32_t)(y * cam.W + x);
             }
         } else {
-            float4 o = make_float4(fmaf(ps.T, a.bg[0], ps.cr), fmaf(ps.T, a.bg[1], ps.cg),
-                                   fmaf(ps.T, a.bg[2], ps.cb), 1.0f - ps.T);
+            const float4 o = make_float4(fmaf(ps.T, a.bg[0], ps.cr), fmaf(ps.T, a.bg[1], ps.cg),
+                                         fmaf(ps.T, a.bg[2], ps.cb), 1.0f - ps.T);
             reinterpret_cast<float4 *>(a.out)[((size_t)view * cam.H + y) * cam.W + x] = o;
         }
     }
     // counters: one atomic per warp per counter
-    unsigned long long tested = inside ? (unsigned long long)(tested_end - beg) : 0ull;
-    unsigned long long v[5] = {tested, n_cand, n_hit, ps.composited, (unsigned long long)ps.overflow};
+    const unsigned long long tested = inside ? (unsigned long long)(tested_end - beg) : 0ull;
+    const unsigned long long v[5] = {tested, n_cand, n_hit, ps.composited, (unsigned long long)ps.overflow};
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
         unsigned long long s = v[c];
@@ -351,13 +477,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     }
 }
 
-// K6: exact per-pixel fallback by repeated selection (no buffer): each round
-// finds, over the whole tile list, the hit with the smallest (t_in, id) after
-// the last composited one, then blends it.  One warp per pixel.
+__device__ __forceinline__ bool fb_hit(const float4 *rec, const Ray &ray, float pxf, float pyf, float &th,
+                                       float &tl, float &kap) {
+    const float4 c0 = rec[kRecConic];
+    const float cc = rec[kRecConicRgb].x;
+    const float dx = pxf - c0.x, dy = pyf - c0.y;
+    const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
+    if (!(q <= 1.0f)) return false;
+    return exact_hit(rec, ray, th, tl, kap);
+}
+
+// K6: exact per-pixel fallback (one warp per overflowed pixel).  Phase A stores
+// every hit of the tile list once (t_in hi/lo, kappa, id) in a per-warp scratch;
+// phase B blends them by repeated selection of the next smallest (t_in, id).
+// If a pixel has more than kFbCap hits, phase B recomputes hits instead of
+// reading the scratch (same result, slower).
 __global__ void __launch_bounds__(256) k_fallback(RenderArgs a, CamBatch cb) {
     const int lane = threadIdx.x & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float4 *scratch = a.fb_scratch + gw * kFbCap;
     int64_t nq = (int64_t)a.counters[kCntFallbackQueue];
     if (nq > a.fallback_capacity) nq = a.fallback_capacity;
     for (int64_t qi = gw; qi < nq; qi += nw) {
@@ -372,6 +512,25 @@ __global__ void __launch_bounds__(256) k_fallback(RenderArgs a, CamBatch cb) {
         const float4 *recs = a.records + (size_t)view * (size_t)a.n * 16;
         const Ray ray = make_ray(cam, x, y);
         const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
+        // phase A
+        int count = 0;
+        for (uint32_t e0 = beg; e0 < end; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            float th = 0.f, tl = 0.f, kap = 0.f;
+            uint32_t id = 0;
+            bool hit = false;
+            if (e < end) {
+                id = a.vals[e];
+                hit = fb_hit(recs + (size_t)id * 16, ray, pxf, pyf, th, tl, kap);
+            }
+            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+            const int pos = count + __popc(hm & lt_mask);
+            if (hit && pos < kFbCap) scratch[pos] = make_float4(th, tl, kap, __uint_as_float(id));
+            count += __popc(hm);
+        }
+        __syncwarp();
+        const bool stored = count <= kFbCap;
+        // phase B
         float T = 1.f, cr = 0.f, cg = 0.f, cbl = 0.f;
         float lh = -INFINITY, ll = 0.f;
         uint32_t lid = 0;
@@ -380,19 +539,26 @@ __global__ void __launch_bounds__(256) k_fallback(RenderArgs a, CamBatch cb) {
         while (true) {
             float bh = INFINITY, bl = 0.f, bk = 0.f;
             uint32_t bid = 0xffffffffu;
-            uint32_t bidx = 0xffffffffu;
-            for (uint32_t e = beg + lane; e < end; e += 32) {
-                const uint32_t id = a.vals[e];
-                const float4 *rec = recs + (size_t)id * 16;
-                const float4 c0 = rec[kRecConic];
-                const float cc = rec[kRecConicRgb].x;
-                const float dx = pxf - c0.x, dy = pyf - c0.y;
-                const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
-                if (!(q <= 1.0f)) continue;
-                float th, tl, kap;
-                if (!exact_hit(rec, ray, th, tl, kap)) continue;
-                if (!first && !before(lh, ll, lid, th, tl, id)) continue;
-                if (before(th, tl, id, bh, bl, bid)) { bh = th; bl = tl; bid = id; bk = kap; bidx = e; }
+            bool found = false;
+            if (stored) {
+                for (int k = lane; k < count; k += 32) {
+                    const float4 h = scratch[k];
+                    const uint32_t id = __float_as_uint(h.w);
+                    if (!first && !before(lh, ll, lid, h.x, h.y, id)) continue;
+                    if (!found || before(h.x, h.y, id, bh, bl, bid)) {
+                        bh = h.x; bl = h.y; bid = id; bk = h.z; found = true;
+                    }
+                }
+            } else {
+                for (uint32_t e = beg + lane; e < end; e += 32) {
+                    const uint32_t id = a.vals[e];
+                    float th, tl, kap;
+                    if (!fb_hit(recs + (size_t)id * 16, ray, pxf, pyf, th, tl, kap)) continue;
+                    if (!first && !before(lh, ll, lid, th, tl, id)) continue;
+                    if (!found || before(th, tl, id, bh, bl, bid)) {
+                        bh = th; bl = tl; bid = id; bk = kap; found = true;
+                    }
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -400,10 +566,12 @@ __global__ void __launch_bounds__(256) k_fallback(RenderArgs a, CamBatch cb) {
                 const float ol = __shfl_xor_sync(0xffffffffu, bl, o);
                 const uint32_t oid = __shfl_xor_sync(0xffffffffu, bid, o);
                 const float ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                const uint32_t oidx = __shfl_xor_sync(0xffffffffu, bidx, o);
-                if (before(oh, ol, oid, bh, bl, bid)) { bh = oh; bl = ol; bid = oid; bk = ok; bidx = oidx; }
+                const bool of = __shfl_xor_sync(0xffffffffu, found, o);
+                if (of && (!found || before(oh, ol, oid, bh, bl, bid))) {
+                    bh = oh; bl = ol; bid = oid; bk = ok; found = true;
+                }
             }
-            if (bidx == 0xffffffffu) break;
+            if (!found) break;
             const float4 rgb = recs[(size_t)bid * 16 + kRecConicRgb];
             const float w = T * bk;
             cr = fmaf(w, rgb.y, cr);
@@ -419,10 +587,13 @@ __global__ void __launch_bounds__(256) k_fallback(RenderArgs a, CamBatch cb) {
                 make_float4(fmaf(T, a.bg[0], cr), fmaf(T, a.bg[1], cg), fmaf(T, a.bg[2], cbl), 1.f - T);
             atomicAdd(a.counters + kCntComposited, ncomp);
         }
+        __syncwarp();
     }
 }
 
 }  // namespace
+
+int64_t fallback_scratch_float4() { return (int64_t)kFbGrid * 256 / 32 * kFbCap; }
 
 cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_t st) {
     static bool attr_set = false;
@@ -439,9 +610,7 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_
 }
 
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
-    for (int i = 0; i < n_batches; ++i) {
-        k_fallback<<<148 * 2, 256, 0, st>>>(a, cams[i]);
-    }
+    for (int i = 0; i < n_batches; ++i) k_fallback<<<kFbGrid, 256, 0, st>>>(a, cams[i]);
     return cudaGetLastError();
 }
 

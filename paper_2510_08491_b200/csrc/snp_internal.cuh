@@ -109,11 +109,14 @@ struct RenderArgs {
     float bg[3];
     float t_floor;
     int32_t pending_limit;
+    int32_t debug_flags;           // SNP_DEBUG env bits (1: no sub-tile culling); 0 in production
     float *out;                    // [V][H][W][4]
-    uint32_t *fallback;            // [capacity] packed (view, pixel) of overflowed pixels
+    uint32_t *fallback;            // [capacity][2] (view, pixel) of overflowed pixels
     int64_t fallback_capacity;
+    float4 *fb_scratch;            // K6 per-warp stored hits [fallback_scratch_float4()]
     unsigned long long *counters;
 };
+int64_t fallback_scratch_float4();
 cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_t st);
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
 
