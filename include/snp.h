@@ -113,11 +113,19 @@ typedef struct {
 const char *snp_version(void);
 
 /* Copies and validates the primitives: every q must have nonzero
- * norm, every s > 0 and finite, everything finite.  `device` is the CUDA device
- * ordinal; `cuda_stream` (cudaStream_t, may be NULL) orders the copies.  The
- * caller may free its arrays on return.  Device-resident inputs are validated
- * by one reduction kernel plus one stream synchronisation. */
+ * norm, every s > 0, every value finite.  `device` is the CUDA device ordinal;
+ * `cuda_stream` (cudaStream_t, may be NULL) orders the copies.  Structural
+ * checks (NULL, n < 0, n_hidden, sh_degree, omega) run on the host and launch
+ * nothing; the values are validated on the device after the copy (one
+ * reduction kernel + one stream synchronisation) and a bad primitive returns
+ * SNP_ERR_INVALID_ARGUMENT naming its index.  The caller may free its arrays on
+ * return. */
 snp_status snp_create_scene(const snp_scene_desc *desc, int device, void *cuda_stream, snp_scene *out);
+
+/* Replaces the parameter values of an existing scene (same n; same validation
+ * and memory rules as snp_create_scene) without reallocating.  Later stages must
+ * be re-run (snp_project first). */
+snp_status snp_update_scene(snp_scene s, const snp_scene_desc *desc, void *cuda_stream);
 
 /* K1 for n_views cameras (all with the same width/height, 1 <= n_views <= 4096):
  * per (view, primitive): frustum cull, exact silhouette bbox -> 16x16 tile rect,
@@ -157,8 +165,8 @@ snp_status snp_get_binning(snp_scene s, int32_t *rects, uint32_t *depth_keys, ui
 /* Counters of the last project/bin_sort/render (synchronises the stream). */
 snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream);
 
-/* Test hook: caps the per-pixel pending buffer of K5 at `k` entries (1..8) so
- * that the exact fallback K6 is exercised; 0 restores the default (8). */
+/* Test hook: caps the per-pixel pending buffer of K5 at `k` entries (1..16) so
+ * that the exact fallback K6 is exercised; 0 restores the default (16). */
 snp_status snp_set_pending_limit(snp_scene s, int32_t k);
 
 #ifdef __cplusplus

@@ -86,20 +86,15 @@ struct snp_scene_s {
     int64_t fallback_capacity = 0;
     DevBuf<float4> fb_scratch;
     DevBuf<float> host_out_staging;
-    int32_t pending_limit = 8;
+    int32_t pending_limit = 16;
     // counters
     DevBuf<unsigned long long> counters;
     unsigned long long *h_counters = nullptr;  // pinned
     DevBuf<int> flag;
+    int *h_flag = nullptr;                     // pinned
 };
 
 namespace {
-
-bool finite_all(const float *p, int64_t k) {
-    for (int64_t i = 0; i < k; ++i)
-        if (!std::isfinite(p[i])) return false;
-    return true;
-}
 
 int bits_for(int64_t n) {
     int b = 0;
@@ -133,10 +128,32 @@ const char *snp_version(void) { return "snp 0.1.0 (sm_100a)"; }
 
 const char *snp_last_error(void) { return g_err.c_str(); }
 
-snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stream, snp_scene *out) {
-    g_err.clear();
-    if (!d || !out) return fail(SNP_ERR_INVALID_ARGUMENT, "desc or out is NULL");
-    *out = nullptr;
+// Copies the parameters into the scene's device buffers and validates them on
+// the device (one reduction kernel + one stream synchronisation).
+static snp_status upload_and_validate(snp_scene s, const snp_scene_desc *d, cudaStream_t st) {
+    static const int64_t per[8] = {3, 4, 3, 24, 8, 8, 1, 48};
+    const float *src[8] = {d->centers, d->rotations, d->scales, d->w1, d->b1, d->w2, d->b2, d->sh};
+    float *dst[8] = {s->centers, s->rotations, s->scales, s->w1, s->b1, s->w2, s->b2, s->sh};
+    const int64_t n = s->n;
+    if (n == 0) return SNP_OK;
+    const cudaMemcpyKind kind = d->memory == SNP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    for (int k = 0; k < 8; ++k) SNP_CUDA(cudaMemcpyAsync(dst[k], src[k], sizeof(float) * per[k] * n, kind, st));
+    const int init[2] = {0, 0x7fffffff};
+    SNP_CUDA(cudaMemcpyAsync(s->flag.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+    ProjectArgs a{};
+    fill_args(s, a);
+    SNP_CUDA(launch_validate(a, s->flag.p, st));
+    SNP_CUDA(cudaMemcpyAsync(s->h_flag, s->flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    SNP_CUDA(cudaStreamSynchronize(st));
+    const int bad = s->h_flag[0], idx = s->h_flag[1];
+    if (bad & 2) return fail(SNP_ERR_INVALID_ARGUMENT, "zero quaternion at primitive " + std::to_string(idx));
+    if (bad & 4) return fail(SNP_ERR_INVALID_ARGUMENT, "non-positive scale at primitive " + std::to_string(idx));
+    if (bad) return fail(SNP_ERR_INVALID_ARGUMENT, "non-finite parameter at primitive " + std::to_string(idx));
+    return SNP_OK;
+}
+
+static snp_status check_desc(const snp_scene_desc *d) {
+    if (!d) return fail(SNP_ERR_INVALID_ARGUMENT, "desc is NULL");
     if (d->n < 0) return fail(SNP_ERR_INVALID_ARGUMENT, "n < 0");
     if (d->n_hidden != kHidden) return fail(SNP_ERR_UNSUPPORTED, "n_hidden must be 8 (P:394)");
     if (d->sh_degree < 0 || d->sh_degree > 3) return fail(SNP_ERR_INVALID_ARGUMENT, "sh_degree must be 0..3");
@@ -144,24 +161,21 @@ snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stre
     if (d->memory != SNP_MEM_HOST && d->memory != SNP_MEM_DEVICE)
         return fail(SNP_ERR_INVALID_ARGUMENT, "memory must be SNP_MEM_HOST or SNP_MEM_DEVICE");
     if (d->n >= (int64_t)1 << 31) return fail(SNP_ERR_UNSUPPORTED, "n must be < 2^31");
-    const int64_t n = d->n;
     const float *src[8] = {d->centers, d->rotations, d->scales, d->w1, d->b1, d->w2, d->b2, d->sh};
-    const int64_t per[8] = {3, 4, 3, 24, 8, 8, 1, 48};
-    if (n > 0)
+    if (d->n > 0)
         for (int k = 0; k < 8; ++k)
             if (!src[k]) return fail(SNP_ERR_INVALID_ARGUMENT, "a parameter array is NULL");
-    if (d->memory == SNP_MEM_HOST && n > 0) {
-        for (int64_t i = 0; i < n; ++i) {
-            const float *q = d->rotations + 4 * i;
-            const double qn = (double)q[0] * q[0] + (double)q[1] * q[1] + (double)q[2] * q[2] + (double)q[3] * q[3];
-            if (!(qn > 0.0)) return fail(SNP_ERR_INVALID_ARGUMENT, "zero quaternion at primitive " + std::to_string(i));
-            for (int k = 0; k < 3; ++k)
-                if (!(d->scales[3 * i + k] > 0.f) || !std::isfinite(d->scales[3 * i + k]))
-                    return fail(SNP_ERR_INVALID_ARGUMENT, "non-positive scale at primitive " + std::to_string(i));
-        }
-        for (int k = 0; k < 8; ++k)
-            if (!finite_all(src[k], per[k] * n)) return fail(SNP_ERR_INVALID_ARGUMENT, "non-finite parameter");
-    }
+    return SNP_OK;
+}
+
+snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stream, snp_scene *out) {
+    g_err.clear();
+    if (!out) return fail(SNP_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    snp_status r = check_desc(d);
+    if (r != SNP_OK) return r;
+    const int64_t n = d->n;
+    static const int64_t per[8] = {3, 4, 3, 24, 8, 8, 1, 48};
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return fail(SNP_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
     cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -171,50 +185,48 @@ snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stre
     s->sh_degree = d->sh_degree;
     s->omega = d->omega;
     // one allocation, each array 256-byte aligned
-    size_t off[9];
+    size_t off[8];
     size_t tot = 0;
     for (int k = 0; k < 8; ++k) {
         off[k] = tot;
         tot += ((size_t)(per[k] * n) * sizeof(float) + 255) / 256 * 256;
     }
-    off[8] = tot;
     cudaError_t ce = s->params.ensure(tot / sizeof(float) + 64);
     if (ce == cudaSuccess) ce = s->counters.ensure(kNumCounters);
-    if (ce == cudaSuccess) ce = s->flag.ensure(1);
+    if (ce == cudaSuccess) ce = s->flag.ensure(2);
     if (ce == cudaSuccess) ce = cudaMallocHost((void **)&s->h_counters, sizeof(unsigned long long) * kNumCounters);
+    if (ce == cudaSuccess) ce = cudaMallocHost((void **)&s->h_flag, 2 * sizeof(int));
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kNumCounters, st);
     if (ce != cudaSuccess) {
         snp_destroy(s);
         return fail(ce == cudaErrorMemoryAllocation ? SNP_ERR_OUT_OF_MEMORY : SNP_ERR_CUDA,
                     std::string("allocation: ") + cudaGetErrorString(ce));
     }
     float **dst[8] = {&s->centers, &s->rotations, &s->scales, &s->w1, &s->b1, &s->w2, &s->b2, &s->sh};
-    for (int k = 0; k < 8; ++k) {
-        *dst[k] = reinterpret_cast<float *>(reinterpret_cast<char *>(s->params.p) + off[k]);
-        if (n > 0) {
-            ce = cudaMemcpyAsync(*dst[k], src[k], sizeof(float) * per[k] * n,
-                                 d->memory == SNP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
-            if (ce != cudaSuccess) break;
-        }
-    }
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kNumCounters, st);
-    if (ce == cudaSuccess && d->memory == SNP_MEM_DEVICE && n > 0) {
-        ce = cudaMemsetAsync(s->flag.p, 0, sizeof(int), st);
-        ProjectArgs a{};
-        fill_args(s, a);
-        if (ce == cudaSuccess) ce = launch_validate(a, s->flag.p, st);
-        int bad = 0;
-        if (ce == cudaSuccess) ce = cudaMemcpyAsync(&bad, s->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st);
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
-        if (ce == cudaSuccess && bad) {
-            snp_destroy(s);
-            return fail(SNP_ERR_INVALID_ARGUMENT, "invalid primitive (zero quaternion, scale <= 0 or non-finite)");
-        }
-    }
-    if (ce != cudaSuccess) {
+    for (int k = 0; k < 8; ++k) *dst[k] = reinterpret_cast<float *>(reinterpret_cast<char *>(s->params.p) + off[k]);
+    r = upload_and_validate(s, d, st);
+    if (r != SNP_OK) {
+        std::string msg = g_err;
         snp_destroy(s);
-        return fail(SNP_ERR_CUDA, std::string("create: ") + cudaGetErrorString(ce));
+        g_err = msg;
+        return r;
     }
     *out = s;
+    return SNP_OK;
+}
+
+snp_status snp_update_scene(snp_scene s, const snp_scene_desc *d, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    r = check_desc(d);
+    if (r != SNP_OK) return r;
+    if (d->n != s->n) return fail(SNP_ERR_INVALID_ARGUMENT, "snp_update_scene: n differs from the scene's");
+    s->sh_degree = d->sh_degree;
+    s->omega = d->omega;
+    r = upload_and_validate(s, d, (cudaStream_t)cuda_stream);
+    if (r != SNP_OK) return r;
+    s->state = kCreated;   // parameters changed: project again
     return SNP_OK;
 }
 
@@ -449,6 +461,7 @@ snp_status snp_destroy(snp_scene s) {
     s->counters.release();
     s->flag.release();
     if (s->h_counters) cudaFreeHost(s->h_counters);
+    if (s->h_flag) cudaFreeHost(s->h_flag);
     delete s;
     return SNP_OK;
 }
@@ -513,8 +526,8 @@ snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream) {
 
 snp_status snp_set_pending_limit(snp_scene s, int32_t k) {
     if (!s) return fail(SNP_ERR_INVALID_ARGUMENT, "scene handle is NULL");
-    if (k < 0 || k > 8) return fail(SNP_ERR_INVALID_ARGUMENT, "pending limit must be 0..8");
-    s->pending_limit = k == 0 ? 8 : k;
+    if (k < 0 || k > 16) return fail(SNP_ERR_INVALID_ARGUMENT, "pending limit must be 0..16");
+    s->pending_limit = k == 0 ? 16 : k;
     return SNP_OK;
 }
 

@@ -69,7 +69,7 @@ __device__ __forceinline__ void sh_rgb(int degree, const float *sh, double x, do
     }
 }
 
-__global__ void __launch_bounds__(256) k_project(ProjectArgs a, CamBatch cb) {
+__global__ void __launch_bounds__(256, 2) k_project(ProjectArgs a, CamBatch cb) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int vloc = blockIdx.y;
     const int64_t view = cb.view0 + vloc;
@@ -292,26 +292,31 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a, CamBatch cb) {
 }
 
 // Input validation: q nonzero, s > 0, every value finite.
+// bad[0] |= 1 non-finite, 2 zero quaternion, 4 scale <= 0; bad[1] = min bad index.
 __global__ void k_validate(ProjectArgs a, int *bad) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     int b = 0;
-    float qn = 0.f;
+    double qn = 0.0;
     for (int k = 0; k < 4; ++k) {
         float q = a.rotations[4 * i + k];
-        if (!isfinite(q)) b = 1;
-        qn += q * q;
+        if (!isfinite(q)) b |= 1;
+        qn += (double)q * (double)q;
     }
-    if (!(qn > 0.f)) b = 1;
+    if (!(qn > 0.0)) b |= 2;
     for (int k = 0; k < 3; ++k) {
         float s = a.scales[3 * i + k], c = a.centers[3 * i + k];
-        if (!(s > 0.f) || !isfinite(s) || !isfinite(c)) b = 1;
+        if (!isfinite(s) || !isfinite(c)) b |= 1;
+        if (!(s > 0.f)) b |= 4;
     }
-    for (int k = 0; k < 24; ++k) if (!isfinite(a.w1[24 * i + k])) b = 1;
-    for (int k = 0; k < 8; ++k) if (!isfinite(a.b1[8 * i + k]) || !isfinite(a.w2[8 * i + k])) b = 1;
-    if (!isfinite(a.b2[i])) b = 1;
-    for (int k = 0; k < 48; ++k) if (!isfinite(a.sh[48 * i + k])) b = 1;
-    if (b) atomicExch(bad, 1);
+    for (int k = 0; k < 24; ++k) if (!isfinite(a.w1[24 * i + k])) b |= 1;
+    for (int k = 0; k < 8; ++k) if (!isfinite(a.b1[8 * i + k]) || !isfinite(a.w2[8 * i + k])) b |= 1;
+    if (!isfinite(a.b2[i])) b |= 1;
+    for (int k = 0; k < 48; ++k) if (!isfinite(a.sh[48 * i + k])) b |= 1;
+    if (b) {
+        atomicOr(bad, b);
+        atomicMin(bad + 1, (int)i);
+    }
 }
 
 }  // namespace

@@ -27,31 +27,28 @@ namespace {
 
 constexpr int kThreads = 256;       // one 16x16 tile, one pixel per thread
 constexpr int kWarps = kThreads / 32;
-constexpr int kBatch = 64;          // records per stage
-constexpr int kStages = 2;
-constexpr int kPendMax = 8;         // per-pixel pending buffer (max occupancy 4-10)
-constexpr int kFbGrid = 148 * 2;    // K6 blocks
-constexpr int kFbCap = 1024;        // K6 stored hits per warp
+constexpr int kBatch = 32;          // records per stage (one per producer lane)
+constexpr int kStages = 4;          // TMA ring depth; warps may run up to kStages batches apart
+constexpr int kPend = 16;           // per-pixel pending hits (unsorted)
+constexpr int kFbGrid = 148 * 2;    // K6 blocks (one overflowed pixel per block at a time)
 
 struct __align__(16) Smem {
-    float4 rec[kStages][kBatch][16];          // 32 KB of records (TMA bulk-staged)
+    float4 rec[kStages][kBatch][16];          // 32 KB of records, cp.async.bulk-staged
     float L[kStages][kBatch + 1];             // depth lower bounds (+ the next batch's first)
     uint32_t id[kStages][kBatch];
-    unsigned long long bar[kStages];
-    uint32_t submask[kWarps][2];              // records whose conic box touches warp w's 8x4 block
+    unsigned long long full[kStages];         // TMA transaction barriers (1 arrival + bytes)
+    unsigned long long empty[kStages];        // slot released by all kWarps consumer warps
     uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs:
     uint8_t ql[kWarps][64];                   //   (record slot j, owner lane)
-    float r_th[kWarps][32], r_tl[kWarps][32], r_k[kWarps][32], r_L[kWarps][32];
-    float r_r[kWarps][32], r_g[kWarps][32], r_b[kWarps][32];
-    uint32_t r_id[kWarps][32], r_j[kWarps][32];
-    uint32_t own[kWarps][32];                 // per owner lane: mask of result slots it owns
-    float p_thi[kPendMax][kThreads];          // pending hits, SoA, column per thread
-    float p_tlo[kPendMax][kThreads];
-    float p_kap[kPendMax][kThreads];
-    float p_r[kPendMax][kThreads];
-    float p_g[kPendMax][kThreads];
-    float p_b[kPendMax][kThreads];
-    uint32_t p_id[kPendMax][kThreads];
+    float p_thi[kPend][kThreads];             // pending hits, unsorted, one column per pixel
+    float p_tlo[kPend][kThreads];
+    float p_kap[kPend][kThreads];
+    uint32_t p_id[kPend][kThreads];
+    int32_t p_n[kThreads];                    // pending count (appended to by any lane of the warp)
+    int32_t p_ovf[kThreads];                  // a hit was dropped: pixel goes to K6
+    int32_t warps_done;
+    int32_t stop;
+    int32_t issued_final;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -64,15 +61,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, u
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_test(unsigned long long *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
     asm volatile(
@@ -185,69 +193,48 @@ __device__ __forceinline__ bool before(float ah, float al, uint32_t aid, float b
 
 struct PixelState {
     float T, cr, cg, cb;
-    int npend;
     bool done;
     bool overflow;
     uint32_t composited;
 };
 
-// Emit every pending hit with t_in < L (strictly), smallest first (Eq. 4 front to back).
-__device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_floor) {
+// Blend, front to back, every pending hit of this thread's pixel with t_in < L
+// (strictly): every hit not yet appended has t_in >= L (R19), so these are
+// exactly the next hits of the ray in (t_in, id) order (Eq. 4).
+__device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_floor, const float4 *recs) {
     const int tid = threadIdx.x;
-    while (ps.npend > 0) {
-        const int k = ps.npend - 1;
-        const float th = sm.p_thi[k][tid], tl = sm.p_tlo[k][tid];
-        if (!(th < L || (th == L && tl < 0.f))) break;
-        const float kap = sm.p_kap[k][tid];
+    int n = sm.p_n[tid];
+    while (n > 0) {
+        int kmin = 0;
+        float mh = sm.p_thi[0][tid], ml = sm.p_tlo[0][tid];
+        uint32_t mid = sm.p_id[0][tid];
+        for (int k = 1; k < n; ++k) {
+            const float h = sm.p_thi[k][tid], l = sm.p_tlo[k][tid];
+            const uint32_t id = sm.p_id[k][tid];
+            if (before(h, l, id, mh, ml, mid)) { mh = h; ml = l; mid = id; kmin = k; }
+        }
+        if (!(mh < L || (mh == L && ml < 0.f))) break;
+        const float kap = sm.p_kap[kmin][tid];
+        const float4 rgb = __ldg(recs + (size_t)mid * 16 + kRecConicRgb);
         const float w = ps.T * kap;
-        ps.cr = fmaf(w, sm.p_r[k][tid], ps.cr);
-        ps.cg = fmaf(w, sm.p_g[k][tid], ps.cg);
-        ps.cb = fmaf(w, sm.p_b[k][tid], ps.cb);
+        ps.cr = fmaf(w, rgb.y, ps.cr);
+        ps.cg = fmaf(w, rgb.z, ps.cg);
+        ps.cb = fmaf(w, rgb.w, ps.cb);
         ps.T *= (1.0f - kap);
-        ps.npend = k;
         ++ps.composited;
+        --n;
+        if (kmin != n) {
+            sm.p_thi[kmin][tid] = sm.p_thi[n][tid];
+            sm.p_tlo[kmin][tid] = sm.p_tlo[n][tid];
+            sm.p_kap[kmin][tid] = sm.p_kap[n][tid];
+            sm.p_id[kmin][tid] = sm.p_id[n][tid];
+        }
         if (ps.T < t_floor) {
             ps.done = true;
             break;
         }
     }
-}
-
-// Insert one hit into the pixel's pending buffer (kept in descending (t_in, id)
-// order, smallest at npend-1).  L = key of the hit's own entry: every hit not yet
-// seen has t_in >= L, so pending hits below L may be emitted to make room.
-__device__ __forceinline__ void insert_hit(Smem &sm, PixelState &ps, float th, float tl, uint32_t id, float kap,
-                                           float r, float g, float b, float L, int plimit, float t_floor) {
-    const int tid = threadIdx.x;
-    if (ps.npend >= plimit) emit(sm, ps, L, t_floor);
-    if (ps.done) return;
-    if (ps.npend >= plimit) {
-        ps.overflow = true;   // K6 re-renders this pixel exactly
-        ps.done = true;
-        return;
-    }
-    int k = ps.npend;
-    while (k > 0) {
-        const float ph = sm.p_thi[k - 1][tid], pl = sm.p_tlo[k - 1][tid];
-        const uint32_t pid = sm.p_id[k - 1][tid];
-        if (!before(ph, pl, pid, th, tl, id)) break;
-        sm.p_thi[k][tid] = ph;
-        sm.p_tlo[k][tid] = pl;
-        sm.p_id[k][tid] = pid;
-        sm.p_kap[k][tid] = sm.p_kap[k - 1][tid];
-        sm.p_r[k][tid] = sm.p_r[k - 1][tid];
-        sm.p_g[k][tid] = sm.p_g[k - 1][tid];
-        sm.p_b[k][tid] = sm.p_b[k - 1][tid];
-        --k;
-    }
-    sm.p_thi[k][tid] = th;
-    sm.p_tlo[k][tid] = tl;
-    sm.p_id[k][tid] = id;
-    sm.p_kap[k][tid] = kap;
-    sm.p_r[k][tid] = r;
-    sm.p_g[k][tid] = g;
-    sm.p_b[k][tid] = b;
-    ++ps.npend;
+    sm.p_n[tid] = n;
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
@@ -261,91 +248,116 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     const int tx = blockIdx.x % a.tiles_x;
     const int ty = a.row_begin + (blockIdx.x / a.tiles_x) * a.row_stride;
     const int tile = ty * a.tiles_x + tx;
-    const int x = tx * kTile + (wid & 1) * 8 + (lane & 7);
-    const int y = ty * kTile + (wid >> 1) * 4 + (lane >> 3);
+    const int bx = tx * kTile + (wid & 1) * 8, by = ty * kTile + (wid >> 1) * 4;   // warp's 8x4 block
+    const int x = bx + (lane & 7);
+    const int y = by + (lane >> 3);
     const bool inside = x < cam.W && y < cam.H;
     const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
     const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
     const int nb = (int)((end - beg + kBatch - 1) / kBatch);
     const float4 *recs = a.records + (size_t)view * (size_t)a.n * 16;
 
-    if (tid == 0)
-        for (int s = 0; s < kStages; ++s) mbar_init(&sm.bar[s], 1);
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], kWarps);
+        }
+        sm.warps_done = 0;
+        sm.stop = 0;
+        sm.issued_final = nb;
+    }
+    sm.p_n[tid] = 0;
+    sm.p_ovf[tid] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    // producer (warps 0-1): one cp.async.bulk per 256-byte record into slot b % kStages
+    // ---- producer (warp 0): one cp.async.bulk per 256-byte record of batch b into slot b % kStages
     auto issue = [&](int b) {
         const int slot = b % kStages;
         const uint32_t e0 = beg + (uint32_t)b * kBatch;
         const uint32_t cnt = min((uint32_t)kBatch, end - e0);
-        if (tid == 0) mbar_arrive_expect_tx(&sm.bar[slot], cnt * 256u);
-        __syncwarp();
-        const int j = tid;  // tid < 64
-        if ((uint32_t)j < cnt) {
-            const uint32_t id = a.vals[e0 + j];
-            sm.id[slot][j] = id;
-            sm.L[slot][j] = __uint_as_float((uint32_t)a.keys[e0 + j]);
-            bulk_g2s(&sm.rec[slot][j][0], recs + (size_t)id * 16, 256u, &sm.bar[slot]);
+        if ((uint32_t)lane < cnt) {
+            const uint32_t id = a.vals[e0 + lane];
+            sm.id[slot][lane] = id;
+            sm.L[slot][lane] = __uint_as_float((uint32_t)a.keys[e0 + lane]);
+            bulk_g2s(&sm.rec[slot][lane][0], recs + (size_t)id * 16, 256u, &sm.full[slot]);
         }
-        if (j == 0) {
+        if (lane == 0) {
             const uint32_t nx = e0 + cnt;
             sm.L[slot][cnt] = nx < end ? __uint_as_float((uint32_t)a.keys[nx]) : INFINITY;
         }
+        // the arrive (release) publishes id/L, written by this warp, with the phase
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&sm.full[slot], cnt * 256u);
     };
-    int issued = nb < kStages ? nb : kStages;
-    if (tid < 64)
-        for (int b = 0; b < issued; ++b) issue(b);
+    int next_issue = 0;
+    if (wid == 0) {
+        for (; next_issue < nb && next_issue < kStages; ++next_issue) issue(next_issue);
+    }
 
     const Ray ray = inside ? make_ray(cam, x, y) : Ray{0, 0, 1, 0, 0, 0, cam.t_near, cam.t_far};
     const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
-    // this thread's pre-pass pairs: record pj against the 8x4 blocks of warps ps0 and ps0 + 4
-    const int pj = tid & 63, ps0 = tid >> 6;
-    const float bx0 = (float)(tx * kTile + (ps0 & 1) * 8) + 0.5f, by0 = (float)(ty * kTile + (ps0 >> 1) * 4) + 0.5f;
-    const float by1 = by0 + 8.0f;  // block ps0 + 4 sits two block-rows (8 px) lower
-    PixelState ps{1.f, 0.f, 0.f, 0.f, 0, !inside, false, 0u};
+    const float bx0 = (float)bx + 0.5f, by0 = (float)by + 0.5f;
+    PixelState ps{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
     uint32_t tested_end = end;
     uint32_t n_cand = 0, n_hit = 0;
-    const int plimit = a.pending_limit;
-    __syncthreads();
+    bool warp_done = false;
+    const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
 
-    int b = 0;
-    for (; b < nb; ++b) {
+    for (int b = 0; b < nb; ++b) {
         const int slot = b % kStages;
-        mbar_wait(&sm.bar[slot], (uint32_t)((b / kStages) & 1));
+        // producer duties: issue what fits; block only for the batch needed now
+        if (wid == 0) {
+            while (next_issue < nb && next_issue < b + kStages) {
+                if (*(volatile int32_t *)&sm.warps_done == kWarps) {
+                    if (lane == 0) {
+                        *(volatile int32_t *)&sm.issued_final = next_issue;
+                        __threadfence_block();
+                        *(volatile int32_t *)&sm.stop = 1;
+                    }
+                    __syncwarp();
+                    break;
+                }
+                const int ns = next_issue % kStages;
+                const uint32_t eph = (uint32_t)((next_issue / kStages - 1) & 1);
+                if (next_issue == b) {
+                    while (!mbar_try(&sm.empty[ns], eph)) {}
+                } else if (!mbar_test(&sm.empty[ns], eph)) {
+                    break;
+                }
+                issue(next_issue);
+                ++next_issue;
+            }
+        }
+        // wait for the records (or for the stop signal past the last issued batch)
+        {
+            bool ready = false;
+            while (!(ready = mbar_try(&sm.full[slot], (uint32_t)((b / kStages) & 1)))) {
+                if (*(volatile int32_t *)&sm.stop && b >= *(volatile int32_t *)&sm.issued_final) break;
+            }
+            if (!ready) break;
+        }
         const uint32_t e0 = beg + (uint32_t)b * kBatch;
         const int cnt = (int)min((uint32_t)kBatch, end - e0);
-        // ---- pre-pass: which records can touch each warp's 8x4 pixel block
-        {
-            bool t0 = false, t1 = false;
-            if (pj < cnt) {
-                const float4 c0 = sm.rec[slot][pj][kRecConic];
-                const float cc = sm.rec[slot][pj][kRecConicRgb].x;
+        if (!warp_done) {
+            // records whose conic box touches this warp's 8x4 block
+            bool touch = false;
+            if (lane < cnt) {
+                const float4 c0 = sm.rec[slot][lane][kRecConic];
+                const float cc = sm.rec[slot][lane][kRecConicRgb].x;
                 const float hb = 0.5f * c0.w;
                 const float det = fmaf(c0.z, cc, -hb * hb);
                 if (det > 0.f) {
                     const float rx = sqrtf(cc / det) * 1.001f + 1e-3f;
                     const float ry = sqrtf(c0.z / det) * 1.001f + 1e-3f;
-                    const bool ox = c0.x + rx >= bx0 && c0.x - rx <= bx0 + 7.0f;
-                    t0 = ox && c0.y + ry >= by0 && c0.y - ry <= by0 + 3.0f;
-                    t1 = ox && c0.y + ry >= by1 && c0.y - ry <= by1 + 3.0f;
+                    touch = c0.x + rx >= bx0 && c0.x - rx <= bx0 + 7.0f && c0.y + ry >= by0 &&
+                            c0.y - ry <= by0 + 3.0f;
                 } else {
-                    t0 = t1 = true;   // no conic (straddles the camera plane / camera inside)
+                    touch = true;   // no conic (straddles the camera plane / camera inside)
                 }
+                if (a.debug_flags & 1) touch = true;
             }
-            if (a.debug_flags & 1) t0 = t1 = pj < cnt;
-            const uint32_t m0 = __ballot_sync(0xffffffffu, t0);
-            const uint32_t m1 = __ballot_sync(0xffffffffu, t1);
-            if (lane == 0) {
-                sm.submask[ps0][wid & 1] = m0;
-                sm.submask[ps0 + 4][wid & 1] = m1;
-            }
-        }
-        __syncthreads();
-        // ---- per warp: candidate pairs -> compaction queue -> 32-wide exact rounds
-        if (!__all_sync(0xffffffffu, ps.done)) {
-            unsigned long long m = (unsigned long long)sm.submask[wid][0] |
-                                   ((unsigned long long)sm.submask[wid][1] << 32);
+            uint32_t m = __ballot_sync(0xffffffffu, touch);
             int qcount = 0;
             auto round = [&](int n) {
                 __syncwarp();
@@ -359,47 +371,40 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 ro.dlx = __shfl_sync(0xffffffffu, ray.dlx, owner);
                 ro.dly = __shfl_sync(0xffffffffu, ray.dly, owner);
                 ro.dlz = __shfl_sync(0xffffffffu, ray.dlz, owner);
-                ro.t_near = cam.t_near;   // uniform: lanes outside the image carry a dummy ray
+                ro.t_near = cam.t_near;
                 ro.t_far = cam.t_far;
-                sm.own[wid][lane] = 0u;
                 bool hit = false;
-                if (valid) {
-                    float th, tl, kap;
-                    const float4 *rec = &sm.rec[slot][j][0];
-                    hit = exact_hit(rec, ro, th, tl, kap);
-                    if (hit) {
-                        const float4 rgb = rec[kRecConicRgb];
-                        sm.r_th[wid][lane] = th;
-                        sm.r_tl[wid][lane] = tl;
-                        sm.r_k[wid][lane] = kap;
-                        sm.r_L[wid][lane] = sm.L[slot][j];
-                        sm.r_r[wid][lane] = rgb.y;
-                        sm.r_g[wid][lane] = rgb.z;
-                        sm.r_b[wid][lane] = rgb.w;
-                        sm.r_id[wid][lane] = sm.id[slot][j];
-                        sm.r_j[wid][lane] = (uint32_t)j;
+                float th = 0.f, tl = 0.f, kap = 0.f;
+                if (valid) hit = exact_hit(&sm.rec[slot][j][0], ro, th, tl, kap);
+                n_hit += hit;
+                // append each hit to its owner's pending list (in queue == record order)
+                const uint32_t peers = __match_any_sync(0xffffffffu, hit ? owner : 64 + lane);
+                const int ot = wid * 32 + owner;
+                int base = 0;
+                if (hit) {
+                    base = sm.p_n[ot];
+                    const int k = base + __popc(peers & lt_mask);
+                    if (k < plimit) {
+                        sm.p_thi[k][ot] = th;
+                        sm.p_tlo[k][ot] = tl;
+                        sm.p_kap[k][ot] = kap;
+                        sm.p_id[k][ot] = sm.id[slot][j];
                     }
                 }
-                const uint32_t peers = __match_any_sync(0xffffffffu, hit ? owner : 64 + lane);
                 __syncwarp();
-                if (hit && lane == __ffs(peers) - 1) sm.own[wid][owner] = peers;
-                __syncwarp();
-                uint32_t mine = sm.own[wid][lane];
-                n_hit += __popc(mine);
-                while (mine) {   // in queue order == record order for this pixel
-                    const int k = __ffs(mine) - 1;
-                    mine &= mine - 1u;
-                    if (ps.done) continue;
-                    insert_hit(sm, ps, sm.r_th[wid][k], sm.r_tl[wid][k], sm.r_id[wid][k], sm.r_k[wid][k],
-                               sm.r_r[wid][k], sm.r_g[wid][k], sm.r_b[wid][k], sm.r_L[wid][k], plimit,
-                               a.t_floor);
-                    if (ps.done && tested_end == end) tested_end = e0 + sm.r_j[wid][k] + 1;
+                if (hit && lane == __ffs(peers) - 1) {
+                    int nn = base + __popc(peers);
+                    if (nn > plimit) {
+                        sm.p_ovf[ot] = 1;
+                        nn = plimit;
+                    }
+                    sm.p_n[ot] = nn;
                 }
                 __syncwarp();
             };
             while (m) {
-                const int j = __ffsll(m) - 1;
-                m &= m - 1ull;
+                const int j = __ffs(m) - 1;
+                m &= m - 1u;
                 const float4 c0 = sm.rec[slot][j][kRecConic];
                 const float cc = sm.rec[slot][j][kRecConicRgb].x;
                 const float dx = pxf - c0.x, dy = pyf - c0.y;
@@ -433,24 +438,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 }
             }
             if (qcount > 0) round(qcount);
+            // batch end: everything left in later batches has t_in >= L of the next key
+            if (!ps.done) {
+                if (sm.p_ovf[tid]) {
+                    ps.overflow = true;
+                    ps.done = true;
+                } else {
+                    emit(sm, ps, sm.L[slot][cnt], a.t_floor, recs);
+                }
+                if (ps.done && tested_end == end) tested_end = e0 + cnt;
+            }
+            if (__all_sync(0xffffffffu, ps.done)) {
+                warp_done = true;
+                if (lane == 0) atomicAdd(&sm.warps_done, 1);
+            }
         }
-        if (!ps.done) {
-            emit(sm, ps, sm.L[slot][cnt], a.t_floor);
-            if (ps.done && tested_end == end) tested_end = e0 + cnt;
-        }
-        const int all_done = __syncthreads_and(ps.done);
-        if (all_done) {
-            ++b;
-            break;
-        }
-        if (issued < nb) {
-            if (tid < 64) issue(issued);
-            ++issued;
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[slot]);
     }
-    // drain: bulk copies still in flight must land before the CTA exits
-    for (int bb = b; bb < issued; ++bb) mbar_wait(&sm.bar[bb % kStages], (uint32_t)((bb / kStages) & 1));
-    if (!ps.done) emit(sm, ps, INFINITY, a.t_floor);
+    if (!ps.done) emit(sm, ps, INFINITY, a.t_floor, recs);
+    __syncthreads();   // no CTA exit while bulk copies of issued batches are in flight (all were waited on)
 
     if (inside) {
         if (ps.overflow) {
@@ -465,7 +472,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             reinterpret_cast<float4 *>(a.out)[((size_t)view * cam.H + y) * cam.W + x] = o;
         }
     }
-    // counters: one atomic per warp per counter
     const unsigned long long tested = inside ? (unsigned long long)(tested_end - beg) : 0ull;
     const unsigned long long v[5] = {tested, n_cand, n_hit, ps.composited, (unsigned long long)ps.overflow};
 #pragma unroll
@@ -487,20 +493,39 @@ __device__ __forceinline__ bool fb_hit(const float4 *rec, const Ray &ray, float 
     return exact_hit(rec, ray, th, tl, kap);
 }
 
-// K6: exact per-pixel fallback (one warp per overflowed pixel).  Phase A stores
-// every hit of the tile list once (t_in hi/lo, kappa, id) in a per-warp scratch;
-// phase B blends them by repeated selection of the next smallest (t_in, id).
-// If a pixel has more than kFbCap hits, phase B recomputes hits instead of
-// reading the scratch (same result, slower).
-__global__ void __launch_bounds__(256) k_fallback(RenderArgs a, CamBatch cb) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    float4 *scratch = a.fb_scratch + gw * kFbCap;
+// K6: exact per-pixel fallback, one CTA per overflowed pixel.  Phase A: the
+// 256 threads split the tile list and store every hit (t_in hi/lo, kappa, id) in
+// shared memory.  Phase B: bitonic sort by (t_in, id) (R11).  Phase C:
+// T before each hit = prefix product of (1 - kappa) (block scan); a hit blends
+// iff T before it is >= floor (Eq. 4 with the stop rule, R13); colours are
+// fetched in parallel and reduced.  Pixels with more than kFbHits hits use a
+// block-wide repeated selection instead (same result, slower).
+constexpr int kFbThreads = 256;
+constexpr int kFbHits = 2048;
+constexpr int kFbPer = kFbHits / kFbThreads;   // 8 sorted entries per thread in phase C
+
+struct FbSmem {
+    float t[kFbHits], l[kFbHits], k[kFbHits];
+    uint32_t id[kFbHits];
+    uint16_t idx[kFbHits];
+    float wsum[kFbThreads / 32][4];
+    float wprod[kFbThreads / 32];
+    int count;
+    int last;
+};
+
+__device__ __forceinline__ bool fb_less(const FbSmem &s, int a, int b, int n) {
+    if (b >= n) return a < n;          // padding sorts last
+    if (a >= n) return false;
+    return before(s.t[a], s.l[a], s.id[a], s.t[b], s.l[b], s.id[b]);
+}
+
+__global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb) {
+    __shared__ FbSmem sm;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int64_t nq = (int64_t)a.counters[kCntFallbackQueue];
     if (nq > a.fallback_capacity) nq = a.fallback_capacity;
-    for (int64_t qi = gw; qi < nq; qi += nw) {
+    for (int64_t qi = blockIdx.x; qi < nq; qi += gridDim.x) {
         const int64_t view = a.fallback[2 * qi];
         if (view < cb.view0 || view >= cb.view0 + cb.nv) continue;
         const DevCam &cam = cb.cams[view - cb.view0];
@@ -512,88 +537,158 @@ __global__ void __launch_bounds__(256) k_fallback(RenderArgs a, CamBatch cb) {
         const float4 *recs = a.records + (size_t)view * (size_t)a.n * 16;
         const Ray ray = make_ray(cam, x, y);
         const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
-        // phase A
-        int count = 0;
-        for (uint32_t e0 = beg; e0 < end; e0 += 32) {
-            const uint32_t e = e0 + lane;
-            float th = 0.f, tl = 0.f, kap = 0.f;
-            uint32_t id = 0;
-            bool hit = false;
-            if (e < end) {
-                id = a.vals[e];
-                hit = fb_hit(recs + (size_t)id * 16, ray, pxf, pyf, th, tl, kap);
-            }
-            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-            const int pos = count + __popc(hm & lt_mask);
-            if (hit && pos < kFbCap) scratch[pos] = make_float4(th, tl, kap, __uint_as_float(id));
-            count += __popc(hm);
-        }
-        __syncwarp();
-        const bool stored = count <= kFbCap;
-        // phase B
-        float T = 1.f, cr = 0.f, cg = 0.f, cbl = 0.f;
-        float lh = -INFINITY, ll = 0.f;
-        uint32_t lid = 0;
-        bool first = true;
-        unsigned long long ncomp = 0;
-        while (true) {
-            float bh = INFINITY, bl = 0.f, bk = 0.f;
-            uint32_t bid = 0xffffffffu;
-            bool found = false;
-            if (stored) {
-                for (int k = lane; k < count; k += 32) {
-                    const float4 h = scratch[k];
-                    const uint32_t id = __float_as_uint(h.w);
-                    if (!first && !before(lh, ll, lid, h.x, h.y, id)) continue;
-                    if (!found || before(h.x, h.y, id, bh, bl, bid)) {
-                        bh = h.x; bl = h.y; bid = id; bk = h.z; found = true;
-                    }
+        if (tid == 0) sm.count = 0;
+        __syncthreads();
+        // ---- phase A: every hit of the tile list, once
+        for (uint32_t e = beg + tid; e < end; e += kFbThreads) {
+            const uint32_t id = a.vals[e];
+            float th, tl, kap;
+            if (fb_hit(recs + (size_t)id * 16, ray, pxf, pyf, th, tl, kap)) {
+                const int pos = atomicAdd(&sm.count, 1);
+                if (pos < kFbHits) {
+                    sm.t[pos] = th; sm.l[pos] = tl; sm.k[pos] = kap; sm.id[pos] = id;
                 }
-            } else {
-                for (uint32_t e = beg + lane; e < end; e += 32) {
+            }
+        }
+        __syncthreads();
+        const int n = sm.count;
+        float T = 1.f, cr = 0.f, cg = 0.f, cbl = 0.f;
+        unsigned long long ncomp = 0;
+        if (n <= kFbHits) {
+            // ---- phase B: bitonic sort of indices
+            int n2 = 1;
+            while (n2 < n) n2 <<= 1;
+            for (int i = tid; i < n2; i += kFbThreads) sm.idx[i] = (uint16_t)i;
+            __syncthreads();
+            for (int kk = 2; kk <= n2; kk <<= 1) {
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                    for (int i = tid; i < n2; i += kFbThreads) {
+                        const int ixj = i ^ jj;
+                        if (ixj > i) {
+                            const int p = sm.idx[i], q = sm.idx[ixj];
+                            const bool asc = (i & kk) == 0;
+                            if (asc ? fb_less(sm, q, p, n) : fb_less(sm, p, q, n)) {
+                                sm.idx[i] = (uint16_t)q;
+                                sm.idx[ixj] = (uint16_t)p;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            // ---- phase C: transmittance before each sorted hit by a block product scan
+            float om[kFbPer];
+            float prod = 1.f;
+#pragma unroll
+            for (int r = 0; r < kFbPer; ++r) {
+                const int i = tid * kFbPer + r;
+                om[r] = i < n ? 1.f - sm.k[sm.idx[i]] : 1.f;
+                prod *= om[r];
+            }
+            float inc = prod;   // inclusive product over threads 0..tid
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc *= v;
+            }
+            if (lane == 31) sm.wprod[wid] = inc;
+            if (tid == 0) sm.last = -1;
+            __syncthreads();
+            float Tb = __shfl_up_sync(0xffffffffu, inc, 1);   // exclusive product within the warp
+            if (lane == 0) Tb = 1.f;
+            for (int w = 0; w < wid; ++w) Tb *= sm.wprod[w];
+            float wr = 0.f, wg = 0.f, wb = 0.f;
+            int last = -1;
+            float t_end = 1.f;
+#pragma unroll
+            for (int r = 0; r < kFbPer; ++r) {
+                const int i = tid * kFbPer + r;
+                if (i < n && Tb >= a.t_floor) {
+                    const int h = sm.idx[i];
+                    const float kap = sm.k[h];
+                    const float4 rgb = __ldg(recs + (size_t)sm.id[h] * 16 + kRecConicRgb);
+                    const float w = Tb * kap;
+                    wr = fmaf(w, rgb.y, wr);
+                    wg = fmaf(w, rgb.z, wg);
+                    wb = fmaf(w, rgb.w, wb);
+                    last = i;
+                    t_end = Tb * om[r];
+                }
+                Tb *= om[r];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                wr += __shfl_xor_sync(0xffffffffu, wr, o);
+                wg += __shfl_xor_sync(0xffffffffu, wg, o);
+                wb += __shfl_xor_sync(0xffffffffu, wb, o);
+            }
+            if (lane == 0) {
+                sm.wsum[wid][0] = wr; sm.wsum[wid][1] = wg; sm.wsum[wid][2] = wb;
+            }
+            if (last >= 0) atomicMax(&sm.last, last);
+            __syncthreads();
+            const int lst = sm.last;
+            if (last >= 0 && last == lst) sm.wsum[0][3] = t_end;   // unique owner of the last blended hit
+            __syncthreads();
+            for (int w = 0; w < kFbThreads / 32; ++w) {
+                cr += sm.wsum[w][0]; cg += sm.wsum[w][1]; cbl += sm.wsum[w][2];
+            }
+            T = lst >= 0 ? sm.wsum[0][3] : 1.f;
+            ncomp = (unsigned long long)(lst + 1);
+        } else {
+            // ---- too many hits for shared memory: block-wide repeated selection
+            float lh = -INFINITY, ll = 0.f;
+            uint32_t lid = 0;
+            bool first = true;
+            while (true) {
+                float bh = INFINITY, bl = 0.f, bk = 0.f;
+                uint32_t bid = 0xffffffffu;
+                for (uint32_t e = beg + tid; e < end; e += kFbThreads) {
                     const uint32_t id = a.vals[e];
                     float th, tl, kap;
                     if (!fb_hit(recs + (size_t)id * 16, ray, pxf, pyf, th, tl, kap)) continue;
                     if (!first && !before(lh, ll, lid, th, tl, id)) continue;
-                    if (!found || before(th, tl, id, bh, bl, bid)) {
-                        bh = th; bl = tl; bid = id; bk = kap; found = true;
-                    }
+                    if (before(th, tl, id, bh, bl, bid)) { bh = th; bl = tl; bid = id; bk = kap; }
                 }
-            }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float oh = __shfl_xor_sync(0xffffffffu, bh, o);
-                const float ol = __shfl_xor_sync(0xffffffffu, bl, o);
-                const uint32_t oid = __shfl_xor_sync(0xffffffffu, bid, o);
-                const float ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                const bool of = __shfl_xor_sync(0xffffffffu, found, o);
-                if (of && (!found || before(oh, ol, oid, bh, bl, bid))) {
-                    bh = oh; bl = ol; bid = oid; bk = ok; found = true;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float oh = __shfl_xor_sync(0xffffffffu, bh, o);
+                    const float ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                    const uint32_t oid = __shfl_xor_sync(0xffffffffu, bid, o);
+                    const float ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                    if (before(oh, ol, oid, bh, bl, bid)) { bh = oh; bl = ol; bid = oid; bk = ok; }
                 }
+                __syncthreads();
+                if (lane == 0) { sm.t[wid] = bh; sm.l[wid] = bl; sm.id[wid] = bid; sm.k[wid] = bk; }
+                __syncthreads();
+                for (int w = 0; w < kFbThreads / 32; ++w)
+                    if (before(sm.t[w], sm.l[w], sm.id[w], bh, bl, bid)) {
+                        bh = sm.t[w]; bl = sm.l[w]; bid = sm.id[w]; bk = sm.k[w];
+                    }
+                if (bid == 0xffffffffu) break;
+                const float4 rgb = __ldg(recs + (size_t)bid * 16 + kRecConicRgb);
+                const float w = T * bk;
+                cr = fmaf(w, rgb.y, cr);
+                cg = fmaf(w, rgb.z, cg);
+                cbl = fmaf(w, rgb.w, cbl);
+                T *= (1.f - bk);
+                ++ncomp;
+                lh = bh; ll = bl; lid = bid; first = false;
+                if (T < a.t_floor) break;
             }
-            if (!found) break;
-            const float4 rgb = recs[(size_t)bid * 16 + kRecConicRgb];
-            const float w = T * bk;
-            cr = fmaf(w, rgb.y, cr);
-            cg = fmaf(w, rgb.z, cg);
-            cbl = fmaf(w, rgb.w, cbl);
-            T *= (1.f - bk);
-            ++ncomp;
-            lh = bh; ll = bl; lid = bid; first = false;
-            if (T < a.t_floor) break;
         }
-        if (lane == 0) {
+        if (tid == 0) {
             reinterpret_cast<float4 *>(a.out)[((size_t)view * cam.H + y) * cam.W + x] =
                 make_float4(fmaf(T, a.bg[0], cr), fmaf(T, a.bg[1], cg), fmaf(T, a.bg[2], cbl), 1.f - T);
             atomicAdd(a.counters + kCntComposited, ncomp);
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
 }  // namespace
 
-int64_t fallback_scratch_float4() { return (int64_t)kFbGrid * 256 / 32 * kFbCap; }
+int64_t fallback_scratch_float4() { return 1; }   // K6 keeps its hits in shared memory
 
 cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_t st) {
     static bool attr_set = false;
@@ -610,7 +705,7 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_
 }
 
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
-    for (int i = 0; i < n_batches; ++i) k_fallback<<<kFbGrid, 256, 0, st>>>(a, cams[i]);
+    for (int i = 0; i < n_batches; ++i) k_fallback<<<kFbGrid, kFbThreads, 0, st>>>(a, cams[i]);
     return cudaGetLastError();
 }
 

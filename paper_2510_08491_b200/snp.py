@@ -23,7 +23,7 @@ STATUS = {0: "SNP_OK", 1: "SNP_ERR_INVALID_ARGUMENT", 2: "SNP_ERR_OUT_OF_MEMORY"
 SNP_MEM_HOST = 0
 SNP_MEM_DEVICE = 1
 
-EXPORTS = ("snp_version", "snp_create_scene", "snp_project", "snp_bin_sort", "snp_render",
+EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
            "snp_set_pending_limit")
 
@@ -75,6 +75,7 @@ def lib():
             L.snp_version.restype = C.c_char_p
             L.snp_last_error.restype = C.c_char_p
             L.snp_create_scene.argtypes = [C.POINTER(SceneDesc), C.c_int, vp, C.POINTER(vp)]
+            L.snp_update_scene.argtypes = [vp, C.POINTER(SceneDesc), vp]
             L.snp_project.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp]
             L.snp_bin_sort.argtypes = [vp, C.POINTER(RenderOpts), vp]
             L.snp_render.argtypes = [vp, C.POINTER(RenderOpts), vp, vp]
@@ -119,9 +120,7 @@ def _is_device(x):
 FIELDS = ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh")
 
 
-def create_scene(scene, device=0, stream=None, n_hidden=8, sh_degree=None, omega=None):
-    """``scene`` has float32 C-contiguous arrays ``centers [n,3] ... sh [n,16,3]``
-    (numpy = host memory, torch CUDA tensors = device memory)."""
+def _desc(scene, n_hidden=8, sh_degree=None, omega=None):
     arrs = []
     for f in FIELDS:
         a = getattr(scene, f)
@@ -135,9 +134,23 @@ def create_scene(scene, device=0, stream=None, n_hidden=8, sh_degree=None, omega
     desc = SceneDesc(n, n_hidden, int(getattr(scene, "sh_degree", 3) if sh_degree is None else sh_degree),
                      float(getattr(scene, "omega", 30.0) if omega is None else omega), mem,
                      *[_ptr(a) for a in arrs])
+    return desc, arrs
+
+
+def create_scene(scene, device=0, stream=None, n_hidden=8, sh_degree=None, omega=None):
+    """``scene`` has float32 C-contiguous arrays ``centers [n,3] ... sh [n,16,3]``
+    (numpy = host memory, torch CUDA tensors = device memory)."""
+    desc, keep = _desc(scene, n_hidden, sh_degree, omega)
     h = C.c_void_p()
     _check(lib().snp_create_scene(C.byref(desc), int(device), _stream(stream), C.byref(h)))
+    del keep
     return h.value
+
+
+def update_scene(h, scene, stream=None, n_hidden=8, sh_degree=None, omega=None):
+    desc, keep = _desc(scene, n_hidden, sh_degree, omega)
+    _check(lib().snp_update_scene(h, C.byref(desc), _stream(stream)))
+    del keep
 
 
 def make_cameras(cams):

@@ -165,3 +165,37 @@ def test_determinism_host_paths_and_stripes():
     for y in range(H):
         p = parts[(y // 16) % 3]
         assert np.array_equal(p[0, y], a[0, y])       # each stripe renders exactly its rows
+
+
+def test_validation_errors_and_update_scene():
+    """zero quaternion / non-positive scale / non-finite values are
+    rejected with the primitive's index; snp_update_scene replaces values."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    sc = synth.make_scene(0, 64)
+    for field, idx, val, word in (("rotations", (3,), 0.0, "quaternion"), ("scales", (5, 2), -1.0, "scale"),
+                                  ("w1", (2, 3, 1), np.nan, "non-finite"), ("sh", (7, 4, 0), np.inf, "non-finite")):
+        bad = sc.subset(np.arange(sc.n))
+        getattr(bad, field)[idx] = val
+        for src in (bad, torch_scene(bad)):
+            with pytest.raises(snp.SnpError) as ei:
+                snp.create_scene(src, 0)
+            assert ei.value.status == 1 and word in str(ei.value)
+    cams = synth.orbit_cameras(1, 4.0, 96, 64, 90.0)
+    a = gpu_render(sc, cams)["img"]
+    sc2 = synth.make_scene(9, 64)
+    b = gpu_render(sc2, cams)["img"]
+    h = snp.create_scene(sc, 0)
+    out = torch.empty((1, 64, 96, 4), device="cuda")
+    opts = snp.make_opts()
+    snp.render_views(h, cams, opts, out)
+    assert np.array_equal(out.cpu().numpy(), a)
+    snp.update_scene(h, sc2)
+    with pytest.raises(snp.SnpError):
+        snp.render(h, opts, out)          # stale binning after an update: BAD_STATE
+    snp.render_views(h, cams, opts, out)
+    assert np.array_equal(out.cpu().numpy(), b)
+    with pytest.raises(snp.SnpError):
+        snp.update_scene(h, synth.make_scene(1, 10))   # n differs
+    snp.destroy(h)
