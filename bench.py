@@ -160,7 +160,7 @@ def run_snp(args):
         step()
     torch.cuda.synchronize()
     stats = snp.get_stats(h, st)
-    passes = (32 + int(np.ceil(np.log2(((W + 15) // 16) * ((H + 15) // 16)))) + 7) // 8
+    passes = (19 + int(np.ceil(np.log2(((W + 15) // 16) * ((H + 15) // 16)))) + 7) // 8
     launches_per_step = 8 + passes
 
     clk = ClockSampler(local)

@@ -485,6 +485,10 @@ int orc_render_frame(const orc_scene *sc, const orc_camera *cam, const double bg
  */
 
 #define ORC_TILE 16
+/* depth code in the key: the fp32 bits of L >> 12 (a rounded-down 19-bit float;
+ * bit 31 is 0 since L > 0), i.e. the key keeps 11 mantissa bits of L (R19). */
+#define ORC_DEPTH_DROP 12
+#define ORC_DEPTH_BITS 19
 static const double ORC_EPS_PX = 1.0 / 256.0;
 
 static uint32_t orc_f32_bits_round_down(double L)
@@ -625,8 +629,8 @@ static int cmp_kv(const void *pa, const void *pb)
 /*
  * Key emission + stable sort + tile ranges over n_views views (rects/depth
  * are [n_views][n][...]).  Emission order: view, then primitive index, then
- * tile rows (only rows of the stripe), then columns; key = view << (tb+32) |
- * tile << 32 | depth, value = primitive index; stable sort by key; ranges[2*(v*T+t)]
+ * tile rows (only rows of the stripe), then columns; key = view << (tb+19) |
+ * tile << 19 | (depth >> 12), value = primitive index; stable sort by key; ranges[2*(v*T+t)]
  * = [begin, end) of (view v, tile t) in the sorted list, (0,0) when empty.
  * Returns N_dup; writes keys/ids/ranges only if N_dup <= capacity.
  */
@@ -657,7 +661,8 @@ int64_t orc_bin_sort(int64_t n, int32_t n_views, const int32_t *rects, const uin
                 if (!orc_row_in_stripe(y, row_begin, row_stride)) continue;
                 for (int32_t x = r[0]; x <= r[2]; ++x) {
                     uint64_t tile = (uint64_t)y * (uint64_t)tiles_x + (uint64_t)x;
-                    kv[e].key = ((uint64_t)v << (tb + 32)) | (tile << 32) | depth[(int64_t)v * n + i];
+                    kv[e].key = ((uint64_t)v << (tb + ORC_DEPTH_BITS)) | (tile << ORC_DEPTH_BITS)
+                               | (uint64_t)(depth[(int64_t)v * n + i] >> ORC_DEPTH_DROP);
                     kv[e].id = (uint32_t)i;
                     kv[e].seq = e;
                     ++e;
@@ -669,10 +674,10 @@ int64_t orc_bin_sort(int64_t n, int32_t n_views, const int32_t *rects, const uin
     for (int64_t k = 0; k < ndup; ++k) {
         keys[k] = kv[k].key;
         ids[k] = kv[k].id;
-        uint64_t vt = kv[k].key >> 32;  /* view << tb | tile */
+        uint64_t vt = kv[k].key >> ORC_DEPTH_BITS;  /* view << tb | tile */
         uint64_t v = vt >> tb, t = vt & (((uint64_t)1 << tb) - 1);
         uint64_t slot = v * (uint64_t)T + t;
-        if (k == 0 || (keys[k - 1] >> 32) != vt) ranges[2 * slot] = (uint32_t)k;
+        if (k == 0 || (keys[k - 1] >> ORC_DEPTH_BITS) != vt) ranges[2 * slot] = (uint32_t)k;
         ranges[2 * slot + 1] = (uint32_t)(k + 1);
     }
     free(kv);

@@ -255,7 +255,7 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
     s->tiles_y = (H + kTile - 1) / kTile;
     s->tile_bits = bits_for((int64_t)s->tiles_x * s->tiles_y);
     s->view_bits = bits_for(n_views);
-    if (32 + s->tile_bits + s->view_bits > 64) return fail(SNP_ERR_UNSUPPORTED, "key exceeds 64 bits");
+    if (kDepthBits + s->tile_bits + s->view_bits > 64) return fail(SNP_ERR_UNSUPPORTED, "key exceeds 64 bits");
     const size_t items = (size_t)n_views * (size_t)s->n;
     SNP_CUDA(s->rects.ensure(items));
     SNP_CUDA(s->depth.ensure(items));
@@ -342,7 +342,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     b.vals = s->vals0.p;
     SNP_CUDA(launch_dup_only(b, st));
     // K3: onesweep over the significant bits only
-    const int bits = 32 + s->tile_bits + s->view_bits;
+    const int bits = kDepthBits + s->tile_bits + s->view_bits;
     const int passes = (bits + 7) / 8;
     const int64_t maxp = (s->key_capacity + sort_partition_size() - 1) / sort_partition_size();
     if (maxp > s->sort_max_partitions || !s->sort_scratch.p) {

@@ -1,6 +1,6 @@
 // binning.cu -- K2 (count, scan, warp-aggregated key duplication) and K4
-// (tile ranges).  Key layout (R19): view << (tile_bits + 32) |
-// tile << 32 | bits(L), L the fp32 depth lower bound from K1; value = primitive
+// (tile ranges).  Key layout (R19): view << (tile_bits + 19) |
+// tile << 19 | bits(L) >> 12, L the fp32 depth lower bound from K1; value = primitive
 // index.  Emission order: view, primitive, stripe rows, columns -- the order the
 // stable sort (K3) then preserves among equal keys.  The paper itself names no
 // tiles; "depth-sorted" is realised per ray in K5 on top of this order.
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
     const int i0 = wid * 32 * kScanItems;
     const uint32_t wbeg = s_off[i0];
     const uint32_t wend = (wid == kScanThreads / 32 - 1) ? s_off[kScanTile] : s_off[i0 + 32 * kScanItems];
-    const uint64_t view_shift = (uint64_t)a.tile_bits + 32;
+    const uint64_t view_shift = (uint64_t)a.tile_bits + kDepthBits;
     for (uint32_t e = wbeg + lane; e < wend; e += 32) {
         // largest item j in [i0, i0+256) with s_off[j] <= e (and count > 0)
         int lo = i0, hi = i0 + 32 * kScanItems - 1;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
         const uint64_t view = (uint64_t)(o / a.n);
         const uint32_t prim = (uint32_t)(o - (int64_t)view * a.n);
         const uint64_t tile = (uint64_t)row * (uint64_t)a.tiles_x + (uint64_t)(it.x0 + c);
-        const uint64_t key = (view << view_shift) | (tile << 32) | (uint64_t)a.depth[o];
+        const uint64_t key = (view << view_shift) | (tile << kDepthBits) | (uint64_t)(a.depth[o] >> kDepthDrop);
         const uint64_t g = gbase + e;
         if (g < (uint64_t)a.capacity) {
             a.keys[g] = key;
@@ -179,10 +179,10 @@ __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *co
     if (n > capacity) n = capacity;
     const uint64_t tmask = (1ull << tile_bits) - 1ull;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t vt = keys[i] >> 32;
+        const uint64_t vt = keys[i] >> kDepthBits;
         const uint64_t slot = (vt >> tile_bits) * (uint64_t)tiles + (vt & tmask);
-        if (i == 0 || (keys[i - 1] >> 32) != vt) ranges[2 * slot] = (uint32_t)i;
-        if (i == n - 1 || (keys[i + 1] >> 32) != vt) ranges[2 * slot + 1] = (uint32_t)(i + 1);
+        if (i == 0 || (keys[i - 1] >> kDepthBits) != vt) ranges[2 * slot] = (uint32_t)i;
+        if (i == n - 1 || (keys[i + 1] >> kDepthBits) != vt) ranges[2 * slot + 1] = (uint32_t)(i + 1);
     }
 }
 

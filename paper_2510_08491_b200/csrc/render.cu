@@ -279,12 +279,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         if ((uint32_t)lane < cnt) {
             const uint32_t id = a.vals[e0 + lane];
             sm.id[slot][lane] = id;
-            sm.L[slot][lane] = __uint_as_float((uint32_t)a.keys[e0 + lane]);
+            sm.L[slot][lane] = key_depth(a.keys[e0 + lane]);
             bulk_g2s(&sm.rec[slot][lane][0], recs + (size_t)id * 16, 256u, &sm.full[slot]);
         }
         if (lane == 0) {
             const uint32_t nx = e0 + cnt;
-            sm.L[slot][cnt] = nx < end ? __uint_as_float((uint32_t)a.keys[nx]) : INFINITY;
+            sm.L[slot][cnt] = nx < end ? key_depth(a.keys[nx]) : INFINITY;
         }
         // the arrive (release) publishes id/L, written by this warp, with the phase
         __syncwarp();

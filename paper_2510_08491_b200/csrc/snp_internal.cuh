@@ -13,6 +13,20 @@ constexpr int kTile = 16;                 // BASELINE north_star: 16x16 tiles (R
 constexpr int kHidden = 8;                // N_sigma = 8
 constexpr int kCamsPerLaunch = 32;        // cameras passed by value per launch
 constexpr int kRecordFloats = 64;         // one render record = 256 B = 16 float4
+// Key = view << (tile_bits + 19) | tile << 19 | (bits(L) >> 12): the depth code is
+// the fp32 lower bound L truncated to 11 mantissa bits (still a lower bound, R19).
+constexpr int kDepthBits = 19;
+constexpr int kDepthDrop = 12;
+__host__ __device__ __forceinline__ float key_depth(uint64_t key) {
+    const uint32_t c = ((uint32_t)key & ((1u << kDepthBits) - 1u)) << kDepthDrop;
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(c);
+#else
+    float f;
+    __builtin_memcpy(&f, &c, 4);
+    return f;
+#endif
+}
 
 // Camera as the kernels see it (by value in the launch parameters).
 struct DevCam {

@@ -122,20 +122,30 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         cnt -= (uint32_t)(kPart - valid);
     }
     // publish aggregate early, then decoupled look-back
-    uint32_t *lb = lookback + ((int64_t)pass * 0) ;  // caller offsets lookback per pass
+    uint32_t *lb = lookback;   // this pass's look-back words [partition][digit]
     if (part == 0) {
         atomicExch(lb + d, kFlagInc | cnt);
         s_excl[d] = 0;
     } else {
         atomicExch(lb + part * 256 + d, kFlagAgg | cnt);
+        // look back over windows of 8 predecessors (8 independent loads per L2 round trip)
         uint32_t sum = 0;
         int64_t q = part - 1;
-        while (true) {
-            uint32_t v = ld_volatile(lb + q * 256 + d);
-            if ((v & ~kValMask) == 0) continue;          // not yet published: spin
-            sum += v & kValMask;
-            if (v & kFlagInc) break;
-            --q;
+        bool found = false;
+        while (!found) {
+            uint32_t v[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) v[w] = (q - w >= 0) ? ld_volatile(lb + (q - w) * 256 + d) : kFlagInc;
+            int w = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (w != k) continue;                    // stopped earlier in this window
+                if ((v[k] & ~kValMask) == 0) break;      // not yet published: re-poll from here
+                sum += v[k] & kValMask;
+                ++w;
+                if (v[k] & kFlagInc) { found = true; break; }
+            }
+            q -= w;
         }
         atomicExch(lb + part * 256 + d, kFlagInc | (sum + cnt));
         s_excl[d] = sum;

@@ -125,14 +125,14 @@ def _python_bin_sort(rects, depth, n, n_views, tx, ty, row_begin=0, row_stride=1
                 if y < row_begin or (y - row_begin) % row_stride:
                     continue
                 for x in range(r[0], r[2] + 1):
-                    keys.append((v << (tb + 32)) | ((y * tx + x) << 32) | int(depth[v * n + i]))
+                    keys.append((v << (tb + 19)) | ((y * tx + x) << 19) | (int(depth[v * n + i]) >> 12))
                     ids.append(i)
     keys = np.array(keys, np.uint64)
     ids = np.array(ids, np.uint32)
     o = np.argsort(keys, kind="stable")
     keys, ids = keys[o], ids[o]
     ranges = np.zeros((n_views * T, 2), np.uint32)
-    slot = (keys >> np.uint64(32 + tb)) * np.uint64(T) + ((keys >> np.uint64(32)) & np.uint64((1 << tb) - 1))
+    slot = (keys >> np.uint64(19 + tb)) * np.uint64(T) + ((keys >> np.uint64(19)) & np.uint64((1 << tb) - 1))
     for s in np.unique(slot):
         w = np.nonzero(slot == s)[0]
         ranges[int(s)] = (w[0], w[-1] + 1)
