@@ -434,6 +434,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                         }
                         __syncwarp();
                         qcount = rem;
+                        // keep pending lists short: every hit this warp has not appended yet
+                        // comes from a record >= the oldest queued one (or > j), so its L bounds them
+                        const int jn = rem > 0 ? (int)__shfl_sync(0xffffffffu, (uint32_t)vj, 0) : j + 1;
+                        if (!ps.done && sm.p_ovf[tid]) {   // a hit was dropped: nothing may be blended
+                            ps.overflow = true;
+                            ps.done = true;
+                        }
+                        if (!ps.done && sm.p_n[tid] > plimit - 4) {
+                            emit(sm, ps, sm.L[slot][jn], a.t_floor, recs);
+                            if (ps.done && tested_end == end) tested_end = e0 + j + 1;
+                        }
                     }
                 }
             }
