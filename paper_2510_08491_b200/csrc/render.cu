@@ -11,44 +11,58 @@
 //              sinc(h_k dt / 2) + b2), g_k = W1'_k.p + omega b1_k, h_k = W1'_k.d
 //              (Eq. 5 normalisation folded into W1' = omega W1 / ||s||_inf, R2);
 //   kernel     kappa = 1 - exp(-max(0, I)) (Eq. 9);
-//   order      hits wait in a per-pixel pending buffer sorted by exact
-//              (t_in, id) and are emitted once t_in < L of the next listed key
-//              (L is a lower bound of t_in for every ray, R19), so blending runs in
-//              exact per-ray entry order (R11);
+//   order      hits wait in a per-pixel pending list and are blended, smallest
+//              (t_in, id) first, once t_in < L of the next unprocessed key (L is a
+//              lower bound of t_in for every ray, R19): exact per-ray entry order
+//              (R11);
 //   blend      C += T kappa c, T *= 1 - kappa, stop at T < floor (Eq. 4, R13).
-// Records are staged per tile batch into shared memory with cp.async.bulk
-// (UBLKCP) + mbarrier transaction counts, 3-stage ring.
+//
+// K5 is persistent and warp-specialised: per CTA one producer warp streams the
+// record batches of successive tiles (tile ids from a global atomic queue) into
+// a 4-stage shared-memory ring with one cp.async.bulk (UBLKCP) per 256-byte
+// record, completing on mbarrier transaction counts; 8 consumer warps (one 8x4
+// pixel block each) release slots through per-slot "empty" mbarriers, so there
+// is no CTA-wide barrier and the next tile's records arrive while the current
+// tile finishes.
 #include <math.h>
+
+#include <algorithm>
 
 #include "snp_internal.cuh"
 
 namespace snp {
 namespace {
 
-constexpr int kThreads = 256;       // one 16x16 tile, one pixel per thread
-constexpr int kWarps = kThreads / 32;
+constexpr int kConsumers = 8;                      // consumer warps = 8x4 pixel blocks of a tile
+constexpr int kThreads = (kConsumers + 1) * 32;    // + 1 producer warp
+constexpr int kWarps = kConsumers;
 constexpr int kBatch = 32;          // records per stage (one per producer lane)
-constexpr int kStages = 4;          // TMA ring depth; warps may run up to kStages batches apart
+constexpr int kStages = 4;          // TMA ring depth
 constexpr int kPend = 16;           // per-pixel pending hits (unsorted)
+constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
 constexpr int kFbGrid = 148 * 2;    // K6 blocks (one overflowed pixel per block at a time)
 
 struct __align__(16) Smem {
     float4 rec[kStages][kBatch][16];          // 32 KB of records, cp.async.bulk-staged
     float L[kStages][kBatch + 1];             // depth lower bounds (+ the next batch's first)
     uint32_t id[kStages][kBatch];
+    // slot metadata written by the producer before its arrive (release)
+    int32_t m_tile[kStages];                  // flattened (view, stripe tile) index, -1 = end of work
+    int32_t m_cnt[kStages];
+    int32_t m_flags[kStages];                 // 1 = first batch of its tile, 2 = last batch
+    int32_t m_seq[kStages];                   // tile sequence number within this CTA
     unsigned long long full[kStages];         // TMA transaction barriers (1 arrival + bytes)
-    unsigned long long empty[kStages];        // slot released by all kWarps consumer warps
+    unsigned long long empty[kStages];        // slot released by all consumer warps
+    int32_t tdone[kTileRing];                 // consumer warps finished with tile seq % kTileRing
+    int32_t next_tile;
     uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs:
     uint8_t ql[kWarps][64];                   //   (record slot j, owner lane)
-    float p_thi[kPend][kThreads];             // pending hits, unsorted, one column per pixel
-    float p_tlo[kPend][kThreads];
-    float p_kap[kPend][kThreads];
-    uint32_t p_id[kPend][kThreads];
-    int32_t p_n[kThreads];                    // pending count (appended to by any lane of the warp)
-    int32_t p_ovf[kThreads];                  // a hit was dropped: pixel goes to K6
-    int32_t warps_done;
-    int32_t stop;
-    int32_t issued_final;
+    float p_thi[kPend][kWarps * 32];          // pending hits, unsorted, one column per pixel
+    float p_tlo[kPend][kWarps * 32];
+    float p_kap[kPend][kWarps * 32];
+    uint32_t p_id[kPend][kWarps * 32];
+    int32_t p_n[kWarps * 32];                 // pending count (appended to by any lane of the warp)
+    int32_t p_ovf[kWarps * 32];               // a hit was dropped: pixel goes to K6
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -242,104 +256,155 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    const int vloc = blockIdx.y;
-    const int64_t view = cb.view0 + vloc;
-    const DevCam &cam = cb.cams[vloc];
-    const int tx = blockIdx.x % a.tiles_x;
-    const int ty = a.row_begin + (blockIdx.x / a.tiles_x) * a.row_stride;
-    const int tile = ty * a.tiles_x + tx;
-    const int bx = tx * kTile + (wid & 1) * 8, by = ty * kTile + (wid >> 1) * 4;   // warp's 8x4 block
-    const int x = bx + (lane & 7);
-    const int y = by + (lane >> 3);
-    const bool inside = x < cam.W && y < cam.H;
-    const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
-    const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
-    const int nb = (int)((end - beg + kBatch - 1) / kBatch);
-    const float4 *recs = a.records + (size_t)view * (size_t)a.n * 16;
+    const int stripe_tiles = a.tiles_x * a.stripe_rows;
+    const int total_tiles = stripe_tiles * cb.nv;
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
-            mbar_init(&sm.empty[s], kWarps);
+            mbar_init(&sm.empty[s], kConsumers);
         }
-        sm.warps_done = 0;
-        sm.stop = 0;
-        sm.issued_final = nb;
+        for (int s = 0; s < kTileRing; ++s) sm.tdone[s] = 0;
     }
-    sm.p_n[tid] = 0;
-    sm.p_ovf[tid] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    // ---- producer (warp 0): one cp.async.bulk per 256-byte record of batch b into slot b % kStages
-    auto issue = [&](int b) {
-        const int slot = b % kStages;
-        const uint32_t e0 = beg + (uint32_t)b * kBatch;
-        const uint32_t cnt = min((uint32_t)kBatch, end - e0);
-        if ((uint32_t)lane < cnt) {
-            const uint32_t id = a.vals[e0 + lane];
-            sm.id[slot][lane] = id;
-            sm.L[slot][lane] = key_depth(a.keys[e0 + lane]);
-            bulk_g2s(&sm.rec[slot][lane][0], recs + (size_t)id * 16, 256u, &sm.full[slot]);
+    if (wid == kConsumers) {
+        // =============================== producer warp
+        uint32_t gb = 0;            // global batch counter (ring slot / phase)
+        int seq = 0;
+        while (true) {
+            int t = 0;
+            if (lane == 0) t = (int)atomicAdd(a.counters + kCntTileQueue, 1ull);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            const int slot0 = (int)(gb % kStages);
+            if (gb >= kStages) {
+                const uint32_t eph = ((gb / kStages) - 1) & 1;
+                while (!mbar_try(&sm.empty[slot0], eph)) {}
+            }
+            if (t >= total_tiles) {           // end marker
+                if (lane == 0) {
+                    sm.m_tile[slot0] = -1;
+                    sm.m_cnt[slot0] = 0;
+                    mbar_arrive_expect_tx(&sm.full[slot0], 0u);
+                }
+                break;
+            }
+            const int vloc = t / stripe_tiles;
+            const int st = t - vloc * stripe_tiles;
+            const int tx = st % a.tiles_x;
+            const int ty = a.row_begin + (st / a.tiles_x) * a.row_stride;
+            const int64_t view = cb.view0 + vloc;
+            const int tile = ty * a.tiles_x + tx;
+            const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
+            const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
+            const int nb = max(1, (int)((end - beg + kBatch - 1) / kBatch));
+            const float4 *recs = a.records + (size_t)view * (size_t)a.n * 16;
+            if (lane == 0) *(volatile int32_t *)&sm.tdone[seq % kTileRing] = 0;
+            for (int bt = 0; bt < nb; ++bt) {
+                const int slot = (int)(gb % kStages);
+                if (bt > 0) {
+                    if (*(volatile int32_t *)&sm.tdone[seq % kTileRing] >= kConsumers) break;   // all done
+                    if (gb >= kStages) {
+                        const uint32_t eph = ((gb / kStages) - 1) & 1;
+                        while (!mbar_try(&sm.empty[slot], eph)) {}
+                    }
+                }
+                const uint32_t e0 = beg + (uint32_t)bt * kBatch;
+                const uint32_t cnt = end > e0 ? min((uint32_t)kBatch, end - e0) : 0u;
+                if ((uint32_t)lane < cnt) {
+                    const uint32_t id = a.vals[e0 + lane];
+                    sm.id[slot][lane] = id;
+                    sm.L[slot][lane] = key_depth(a.keys[e0 + lane]);
+                    bulk_g2s(&sm.rec[slot][lane][0], recs + (size_t)id * 16, 256u, &sm.full[slot]);
+                }
+                if (lane == 0) {
+                    const uint32_t nx = e0 + cnt;
+                    sm.L[slot][cnt] = nx < end ? key_depth(a.keys[nx]) : INFINITY;
+                    sm.m_tile[slot] = t;
+                    sm.m_cnt[slot] = (int)cnt;
+                    sm.m_flags[slot] = (bt == 0 ? 1 : 0) | (bt == nb - 1 ? 2 : 0);
+                    sm.m_seq[slot] = seq;
+                }
+                // the arrive (release) publishes id/L/metadata with the phase
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(&sm.full[slot], cnt * 256u);
+                ++gb;
+            }
+            ++seq;
         }
-        if (lane == 0) {
-            const uint32_t nx = e0 + cnt;
-            sm.L[slot][cnt] = nx < end ? key_depth(a.keys[nx]) : INFINITY;
-        }
-        // the arrive (release) publishes id/L, written by this warp, with the phase
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&sm.full[slot], cnt * 256u);
-    };
-    int next_issue = 0;
-    if (wid == 0) {
-        for (; next_issue < nb && next_issue < kStages; ++next_issue) issue(next_issue);
+        return;
     }
 
-    const Ray ray = inside ? make_ray(cam, x, y) : Ray{0, 0, 1, 0, 0, 0, cam.t_near, cam.t_far};
-    const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
-    const float bx0 = (float)bx + 0.5f, by0 = (float)by + 0.5f;
-    PixelState ps{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
-    uint32_t tested_end = end;
-    uint32_t n_cand = 0, n_hit = 0;
-    bool warp_done = false;
+    // =============================== consumer warps
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
+    uint32_t n_cand = 0, n_hit = 0, n_comp = 0, n_ovf = 0;
+    unsigned long long n_tested = 0;
+    // per-tile state
+    int cur_seq = -1;
+    bool tile_finished = true;    // this warp has written its pixels of the current tile
+    int x = 0, y = 0;
+    bool inside = false;
+    int64_t view = 0;
+    const DevCam *cam = &cb.cams[0];
+    const float4 *recs = a.records;
+    Ray ray{0, 0, 1, 0, 0, 0, 0, 0};
+    float pxf = 0.f, pyf = 0.f, bx0 = 0.f, by0 = 0.f;
+    PixelState ps{1.f, 0.f, 0.f, 0.f, true, false, 0u};
 
-    for (int b = 0; b < nb; ++b) {
-        const int slot = b % kStages;
-        // producer duties: issue what fits; block only for the batch needed now
-        if (wid == 0) {
-            while (next_issue < nb && next_issue < b + kStages) {
-                if (*(volatile int32_t *)&sm.warps_done == kWarps) {
-                    if (lane == 0) {
-                        *(volatile int32_t *)&sm.issued_final = next_issue;
-                        __threadfence_block();
-                        *(volatile int32_t *)&sm.stop = 1;
-                    }
-                    __syncwarp();
-                    break;
+    auto finish_tile = [&]() {   // write this warp's pixels; count the warp as done with the tile
+        if (inside) {
+            if (ps.overflow) {
+                const unsigned long long q = atomicAdd(a.counters + kCntFallbackQueue, 1ull);
+                if ((int64_t)q < a.fallback_capacity) {
+                    a.fallback[2 * q] = (uint32_t)view;
+                    a.fallback[2 * q + 1] = (uint32_t)(y * cam->W + x);
                 }
-                const int ns = next_issue % kStages;
-                const uint32_t eph = (uint32_t)((next_issue / kStages - 1) & 1);
-                if (next_issue == b) {
-                    while (!mbar_try(&sm.empty[ns], eph)) {}
-                } else if (!mbar_test(&sm.empty[ns], eph)) {
-                    break;
-                }
-                issue(next_issue);
-                ++next_issue;
+                ++n_ovf;
+            } else {
+                const float4 o = make_float4(fmaf(ps.T, a.bg[0], ps.cr), fmaf(ps.T, a.bg[1], ps.cg),
+                                             fmaf(ps.T, a.bg[2], ps.cb), 1.0f - ps.T);
+                reinterpret_cast<float4 *>(a.out)[((size_t)view * cam->H + y) * cam->W + x] = o;
             }
         }
-        // wait for the records (or for the stop signal past the last issued batch)
-        {
-            bool ready = false;
-            while (!(ready = mbar_try(&sm.full[slot], (uint32_t)((b / kStages) & 1)))) {
-                if (*(volatile int32_t *)&sm.stop && b >= *(volatile int32_t *)&sm.issued_final) break;
-            }
-            if (!ready) break;
+        n_comp += ps.composited;
+        tile_finished = true;
+        __syncwarp();
+        if (lane == 0) atomicAdd(&sm.tdone[cur_seq % kTileRing], 1);
+    };
+
+    for (uint32_t gb = 0;; ++gb) {
+        const int slot = (int)(gb % kStages);
+        while (!mbar_try(&sm.full[slot], (gb / kStages) & 1)) {}
+        const int t = sm.m_tile[slot];
+        if (t < 0) break;                      // end of work (no release needed)
+        const int cnt = sm.m_cnt[slot];
+        const int flags = sm.m_flags[slot];
+        if (flags & 1) {                       // first batch of a new tile: set up the pixels
+            cur_seq = sm.m_seq[slot];
+            const int vloc = t / stripe_tiles;
+            const int st = t - vloc * stripe_tiles;
+            const int tx = st % a.tiles_x;
+            const int ty = a.row_begin + (st / a.tiles_x) * a.row_stride;
+            view = cb.view0 + vloc;
+            cam = &cb.cams[vloc];
+            recs = a.records + (size_t)view * (size_t)a.n * 16;
+            const int bx = tx * kTile + (wid & 1) * 8, by = ty * kTile + (wid >> 1) * 4;
+            x = bx + (lane & 7);
+            y = by + (lane >> 3);
+            inside = x < cam->W && y < cam->H;
+            ray = inside ? make_ray(*cam, x, y) : Ray{0, 0, 1, 0, 0, 0, cam->t_near, cam->t_far};
+            pxf = (float)x + 0.5f;
+            pyf = (float)y + 0.5f;
+            bx0 = (float)bx + 0.5f;
+            by0 = (float)by + 0.5f;
+            ps = PixelState{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
+            sm.p_n[tid] = 0;
+            sm.p_ovf[tid] = 0;
+            tile_finished = false;
         }
-        const uint32_t e0 = beg + (uint32_t)b * kBatch;
-        const int cnt = (int)min((uint32_t)kBatch, end - e0);
-        if (!warp_done) {
+        if (!tile_finished) {
+            if (!ps.done) n_tested += (unsigned long long)cnt;
             // records whose conic box touches this warp's 8x4 block
             bool touch = false;
             if (lane < cnt) {
@@ -371,8 +436,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 ro.dlx = __shfl_sync(0xffffffffu, ray.dlx, owner);
                 ro.dly = __shfl_sync(0xffffffffu, ray.dly, owner);
                 ro.dlz = __shfl_sync(0xffffffffu, ray.dlz, owner);
-                ro.t_near = cam.t_near;
-                ro.t_far = cam.t_far;
+                ro.t_near = cam->t_near;
+                ro.t_far = cam->t_far;
                 bool hit = false;
                 float th = 0.f, tl = 0.f, kap = 0.f;
                 if (valid) hit = exact_hit(&sm.rec[slot][j][0], ro, th, tl, kap);
@@ -441,50 +506,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                             ps.overflow = true;
                             ps.done = true;
                         }
-                        if (!ps.done && sm.p_n[tid] > plimit - 4) {
-                            emit(sm, ps, sm.L[slot][jn], a.t_floor, recs);
-                            if (ps.done && tested_end == end) tested_end = e0 + j + 1;
-                        }
+                        if (!ps.done && sm.p_n[tid] > plimit - 4) emit(sm, ps, sm.L[slot][jn], a.t_floor, recs);
                     }
                 }
             }
             if (qcount > 0) round(qcount);
-            // batch end: everything left in later batches has t_in >= L of the next key
+            // batch end: everything in later batches has t_in >= L of the next key
             if (!ps.done) {
                 if (sm.p_ovf[tid]) {
                     ps.overflow = true;
                     ps.done = true;
                 } else {
-                    emit(sm, ps, sm.L[slot][cnt], a.t_floor, recs);
+                    emit(sm, ps, (flags & 2) ? INFINITY : sm.L[slot][cnt], a.t_floor, recs);
                 }
-                if (ps.done && tested_end == end) tested_end = e0 + cnt;
             }
-            if (__all_sync(0xffffffffu, ps.done)) {
-                warp_done = true;
-                if (lane == 0) atomicAdd(&sm.warps_done, 1);
-            }
+            if ((flags & 2) || __all_sync(0xffffffffu, ps.done)) finish_tile();
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[slot]);
     }
-    if (!ps.done) emit(sm, ps, INFINITY, a.t_floor, recs);
-    __syncthreads();   // no CTA exit while bulk copies of issued batches are in flight (all were waited on)
-
-    if (inside) {
-        if (ps.overflow) {
-            const unsigned long long slot = atomicAdd(a.counters + kCntFallbackQueue, 1ull);
-            if ((int64_t)slot < a.fallback_capacity) {
-                a.fallback[2 * slot] = (uint32_t)view;
-                a.fallback[2 * slot + 1] = (uint32_t)(y * cam.W + x);
-            }
-        } else {
-            const float4 o = make_float4(fmaf(ps.T, a.bg[0], ps.cr), fmaf(ps.T, a.bg[1], ps.cg),
-                                         fmaf(ps.T, a.bg[2], ps.cb), 1.0f - ps.T);
-            reinterpret_cast<float4 *>(a.out)[((size_t)view * cam.H + y) * cam.W + x] = o;
-        }
-    }
-    const unsigned long long tested = inside ? (unsigned long long)(tested_end - beg) : 0ull;
-    const unsigned long long v[5] = {tested, n_cand, n_hit, ps.composited, (unsigned long long)ps.overflow};
+    const unsigned long long v[5] = {n_tested, n_cand, n_hit, n_comp, n_ovf};
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
         unsigned long long s = v[c];
@@ -709,8 +750,18 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)(a.tiles_x * a.stripe_rows), (unsigned)cams.nv);
-    if (grid.x == 0) return cudaSuccess;
+    const int tiles = a.tiles_x * a.stripe_rows * cams.nv;
+    if (tiles == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.counters + kCntTileQueue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int grid = std::min(tiles, 2 * sms);   // persistent: 2 CTAs per SM
     k_render<<<grid, kThreads, smem, st>>>(a, cams);
     return cudaGetLastError();
 }
