@@ -524,6 +524,19 @@ snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream) {
     return SNP_OK;
 }
 
+snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!out || n < 0 || n > kNumCounters) return fail(SNP_ERR_INVALID_ARGUMENT, "out is NULL or n out of range");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    SNP_CUDA(cudaMemcpyAsync(s->h_counters, s->counters.p, sizeof(unsigned long long) * kNumCounters,
+                             cudaMemcpyDeviceToHost, st));
+    SNP_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < n; ++i) out[i] = s->h_counters[i];
+    return SNP_OK;
+}
+
 snp_status snp_set_pending_limit(snp_scene s, int32_t k) {
     if (!s) return fail(SNP_ERR_INVALID_ARGUMENT, "scene handle is NULL");
     if (k < 0 || k > 16) return fail(SNP_ERR_INVALID_ARGUMENT, "pending limit must be 0..16");

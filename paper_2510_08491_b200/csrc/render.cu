@@ -337,6 +337,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     }
 
     // =============================== consumer warps
+#ifdef SNP_INSTRUMENT
+    long long ins_wait = 0, ins_round = 0, ins_emit = 0, ins_rounds = 0, ins_lanes = 0;
+    const long long ins_start = clock64();
+#endif
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
     uint32_t n_cand = 0, n_hit = 0, n_comp = 0, n_ovf = 0;
     unsigned long long n_tested = 0;
@@ -375,7 +379,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 
     for (uint32_t gb = 0;; ++gb) {
         const int slot = (int)(gb % kStages);
+#ifdef SNP_INSTRUMENT
+        long long _t0 = clock64();
+#endif
         while (!mbar_try(&sm.full[slot], (gb / kStages) & 1)) {}
+#ifdef SNP_INSTRUMENT
+        ins_wait += clock64() - _t0;
+#endif
         const int t = sm.m_tile[slot];
         if (t < 0) break;                      // end of work (no release needed)
         const int cnt = sm.m_cnt[slot];
@@ -425,6 +435,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             uint32_t m = __ballot_sync(0xffffffffu, touch);
             int qcount = 0;
             auto round = [&](int n) {
+#ifdef SNP_INSTRUMENT
+                long long _r0 = clock64();
+                ++ins_rounds;
+                ins_lanes += n;
+#endif
                 __syncwarp();
                 const bool valid = lane < n;
                 const int owner = valid ? sm.ql[wid][lane] : lane;
@@ -466,17 +481,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     sm.p_n[ot] = nn;
                 }
                 __syncwarp();
+#ifdef SNP_INSTRUMENT
+                ins_round += clock64() - _r0;
+#endif
             };
-            while (m) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1u;
-                const float4 c0 = sm.rec[slot][j][kRecConic];
-                const float cc = sm.rec[slot][j][kRecConicRgb].x;
-                const float dx = pxf - c0.x, dy = pyf - c0.y;
-                const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
-                const bool cand = !ps.done && q <= 1.0f;
-                const uint32_t cm = __ballot_sync(0xffffffffu, cand);
-                if (cm) {
+            // Single call site for the exact round and for emission (keeps the hot code
+            // inside the instruction cache).
+            int jlast = -1;
+            while (true) {
+                // fill the queue from the records that touch this warp's block
+                while (m && qcount < 32) {
+                    const int j = __ffs(m) - 1;
+                    m &= m - 1u;
+                    jlast = j;
+                    const float4 c0 = sm.rec[slot][j][kRecConic];
+                    const float cc = sm.rec[slot][j][kRecConicRgb].x;
+                    const float dx = pxf - c0.x, dy = pyf - c0.y;
+                    const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
+                    const bool cand = !ps.done && q <= 1.0f;
+                    const uint32_t cm = __ballot_sync(0xffffffffu, cand);
                     if (cand) {
                         const int pos = qcount + __popc(cm & lt_mask);
                         sm.qj[wid][pos] = (uint8_t)j;
@@ -484,54 +507,67 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                         ++n_cand;
                     }
                     qcount += __popc(cm);
-                    if (qcount >= 32) {
-                        round(32);
-                        const int rem = qcount - 32;
-                        uint8_t vj = 0, vl = 0;
-                        if (lane < rem) {
-                            vj = sm.qj[wid][32 + lane];
-                            vl = sm.ql[wid][32 + lane];
-                        }
-                        __syncwarp();
-                        if (lane < rem) {
-                            sm.qj[wid][lane] = vj;
-                            sm.ql[wid][lane] = vl;
-                        }
-                        __syncwarp();
-                        qcount = rem;
-                        // keep pending lists short: every hit this warp has not appended yet
-                        // comes from a record >= the oldest queued one (or > j), so its L bounds them
-                        const int jn = rem > 0 ? (int)__shfl_sync(0xffffffffu, (uint32_t)vj, 0) : j + 1;
-                        if (!ps.done && sm.p_ovf[tid]) {   // a hit was dropped: nothing may be blended
-                            ps.overflow = true;
-                            ps.done = true;
-                        }
-                        if (!ps.done && sm.p_n[tid] > plimit - 4) emit(sm, ps, sm.L[slot][jn], a.t_floor, recs);
-                    }
                 }
-            }
-            if (qcount > 0) round(qcount);
-            // batch end: everything in later batches has t_in >= L of the next key
-            if (!ps.done) {
-                if (sm.p_ovf[tid]) {
+                int rem = 0, jn = jlast + 1;
+                if (qcount > 0) {
+                    round(qcount < 32 ? qcount : 32);
+                    rem = qcount > 32 ? qcount - 32 : 0;
+                    uint8_t vj = 0, vl = 0;
+                    if (lane < rem) {
+                        vj = sm.qj[wid][32 + lane];
+                        vl = sm.ql[wid][32 + lane];
+                    }
+                    __syncwarp();
+                    if (lane < rem) {
+                        sm.qj[wid][lane] = vj;
+                        sm.ql[wid][lane] = vl;
+                    }
+                    __syncwarp();
+                    // every hit this warp has not appended yet comes from a record >= the
+                    // oldest queued one (or > jlast), so that record's L bounds its t_in
+                    if (rem > 0) jn = (int)__shfl_sync(0xffffffffu, (uint32_t)vj, 0);
+                    qcount = rem;
+                }
+                const bool batch_end = (m == 0u) && rem == 0;
+                if (!ps.done && sm.p_ovf[tid]) {   // a hit was dropped: nothing may be blended
                     ps.overflow = true;
                     ps.done = true;
-                } else {
-                    emit(sm, ps, (flags & 2) ? INFINITY : sm.L[slot][cnt], a.t_floor, recs);
                 }
+                // batch end: everything in later batches has t_in >= L of the next key;
+                // mid-batch: only when the pending list runs full
+                if (!ps.done && (batch_end || sm.p_n[tid] > plimit - 4)) {
+#ifdef SNP_INSTRUMENT
+                    long long _e0 = clock64();
+#endif
+                    emit(sm, ps, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                         a.t_floor, recs);
+#ifdef SNP_INSTRUMENT
+                    ins_emit += clock64() - _e0;
+#endif
+                }
+                if (batch_end) break;
             }
             if ((flags & 2) || __all_sync(0xffffffffu, ps.done)) finish_tile();
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[slot]);
     }
-    const unsigned long long v[5] = {n_tested, n_cand, n_hit, n_comp, n_ovf};
+#ifdef SNP_INSTRUMENT
+    if (lane == 0) {
+        atomicAdd(a.counters + 16, (unsigned long long)ins_wait);
+        atomicAdd(a.counters + 17, (unsigned long long)ins_round);
+        atomicAdd(a.counters + 18, (unsigned long long)ins_emit);
+        atomicAdd(a.counters + 19, (unsigned long long)ins_rounds);
+        atomicAdd(a.counters + 20, (unsigned long long)ins_lanes);
+        atomicAdd(a.counters + 21, (unsigned long long)(clock64() - ins_start));
+    }
+#endif
+    __syncwarp();
+    const uint32_t v[5] = {(uint32_t)n_tested, n_cand, n_hit, n_comp, n_ovf};
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-        unsigned long long s = v[c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-        if (lane == 0 && s) atomicAdd(a.counters + kCntTested + c, s);
+        const uint32_t s = __reduce_add_sync(0xffffffffu, v[c]);   // per-warp totals fit 32 bits
+        if (lane == 0 && s) atomicAdd(a.counters + kCntTested + c, (unsigned long long)s);
     }
 }
 

@@ -58,7 +58,7 @@ enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecW
 // Device-side counters (one 64-bit slot each), see snp_stats.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntTested = 2, kCntCandidate = 3, kCntHit = 4,
                kCntComposited = 5, kCntOverflow = 6, kCntCapOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
-               kNumCounters = 16 };
+               kNumCounters = 32 };   // 16..31: SNP_INSTRUMENT builds only
 
 struct ProjectArgs {
     int64_t n;

@@ -128,17 +128,18 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         s_excl[d] = 0;
     } else {
         atomicExch(lb + part * 256 + d, kFlagAgg | cnt);
-        // look back over windows of 8 predecessors (8 independent loads per L2 round trip)
+        // look back over windows of kWin predecessors (kWin independent loads per L2 round trip)
+        constexpr int kWin = 24;
         uint32_t sum = 0;
         int64_t q = part - 1;
         bool found = false;
         while (!found) {
-            uint32_t v[8];
+            uint32_t v[kWin];
 #pragma unroll
-            for (int w = 0; w < 8; ++w) v[w] = (q - w >= 0) ? ld_volatile(lb + (q - w) * 256 + d) : kFlagInc;
+            for (int w = 0; w < kWin; ++w) v[w] = (q - w >= 0) ? ld_volatile(lb + (q - w) * 256 + d) : kFlagInc;
             int w = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < kWin; ++k) {
                 if (w != k) continue;                    // stopped earlier in this window
                 if ((v[k] & ~kValMask) == 0) break;      // not yet published: re-poll from here
                 sum += v[k] & kValMask;

@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsnp.so")
+LIB_PATH = os.environ.get("SNP_LIB_PATH") or os.path.join(_HERE, "libsnp.so")   # override: A/B experiments only
 
 SNP_OK = 0
 STATUS = {0: "SNP_OK", 1: "SNP_ERR_INVALID_ARGUMENT", 2: "SNP_ERR_OUT_OF_MEMORY", 3: "SNP_ERR_CUDA",
@@ -25,7 +25,7 @@ SNP_MEM_DEVICE = 1
 
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
-           "snp_set_pending_limit")
+           "snp_set_pending_limit", "snp_get_debug_counters")
 
 
 class SnpError(RuntimeError):
@@ -84,6 +84,7 @@ def lib():
             L.snp_get_binning.argtypes = [vp, vp, vp, vp, vp, C.c_int64, C.POINTER(C.c_int64), vp, vp]
             L.snp_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
+            L.snp_get_debug_counters.argtypes = [vp, vp, C.c_int32, vp]
             for f in EXPORTS:
                 if f not in ("snp_version", "snp_last_error"):
                     getattr(L, f).restype = C.c_int
@@ -194,6 +195,12 @@ def destroy(h):
 
 def set_pending_limit(h, k):
     _check(lib().snp_set_pending_limit(h, int(k)))
+
+
+def get_debug_counters(h, n=32, stream=None):
+    out = np.zeros(n, np.uint64)
+    _check(lib().snp_get_debug_counters(h, out.ctypes.data, int(n), _stream(stream)))
+    return out
 
 
 def get_stats(h, stream=None):
