@@ -32,46 +32,101 @@ __device__ __forceinline__ bool quat_rot(const float *q4, double R[9]) {
 }
 
 // Real SH basis, degrees 0..3 (Condon-Shortley phase, m = -l..l; 3DGS convention).
-__device__ __forceinline__ void sh_rgb(int degree, const float *sh, double x, double y, double z,
+__device__ __forceinline__ void sh_rgb(int degree, const float *sh, double xd, double yd, double zd,
                                        float rgb[3]) {
-    double Y[16];
-    const double xx = x * x, yy = y * y, zz = z * z;
-    Y[0] = 0.28209479177387814;
-    Y[1] = -0.4886025119029199 * y;
-    Y[2] = 0.4886025119029199 * z;
-    Y[3] = -0.4886025119029199 * x;
-    Y[4] = 1.0925484305920792 * (x * y);
-    Y[5] = -1.0925484305920792 * (y * z);
-    Y[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
-    Y[7] = -1.0925484305920792 * (x * z);
-    Y[8] = 0.5462742152960396 * (xx - yy);
-    Y[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
-    Y[10] = 2.890611442640554 * (x * y) * z;
-    Y[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
-    Y[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-    Y[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
-    Y[14] = 1.445305721320277 * z * (xx - yy);
-    Y[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+    // fp32 is ample here: colour enters the pixel linearly (error ~1e-7)
+    const float x = (float)xd, y = (float)yd, z = (float)zd;
+    float Y[16];
+    const float xx = x * x, yy = y * y, zz = z * z;
+    Y[0] = 0.28209479177387814f;
+    Y[1] = -0.4886025119029199f * y;
+    Y[2] = 0.4886025119029199f * z;
+    Y[3] = -0.4886025119029199f * x;
+    Y[4] = 1.0925484305920792f * (x * y);
+    Y[5] = -1.0925484305920792f * (y * z);
+    Y[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+    Y[7] = -1.0925484305920792f * (x * z);
+    Y[8] = 0.5462742152960396f * (xx - yy);
+    Y[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+    Y[10] = 2.890611442640554f * (x * y) * z;
+    Y[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+    Y[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    Y[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+    Y[14] = 1.445305721320277f * z * (xx - yy);
+    Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
     const int nc = (degree + 1) * (degree + 1);
-    double acc[3] = {0.0, 0.0, 0.0};
+    float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         if (i < nc) {
-            acc[0] += Y[i] * (double)sh[3 * i + 0];
-            acc[1] += Y[i] * (double)sh[3 * i + 1];
-            acc[2] += Y[i] * (double)sh[3 * i + 2];
+            acc[0] += Y[i] * sh[3 * i + 0];
+            acc[1] += Y[i] * sh[3 * i + 1];
+            acc[2] += Y[i] * sh[3 * i + 2];
         }
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        double v = acc[c] + 0.5;
-        rgb[c] = (float)(v > 0.0 ? v : 0.0);
+        const float v = acc[c] + 0.5f;
+        rgb[c] = v > 0.f ? v : 0.f;
     }
 }
 
-__global__ void __launch_bounds__(256, 2) k_project(ProjectArgs a, CamBatch cb) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int vloc = blockIdx.y;
+constexpr int kProjThreads = 128;
+
+// Per-CTA parameter slice, loaded once with cp.async.bulk and reused by every view.
+struct ProjSmem {
+    float centers[kProjThreads * 3];
+    float rot[kProjThreads * 4];
+    float scales[kProjThreads * 3];
+    float w1[kProjThreads * 24];
+    float b1[kProjThreads * 8];
+    float w2[kProjThreads * 8];
+    float b2[kProjThreads];
+    float sh[kProjThreads * 48];
+    unsigned long long bar;
+};
+
+__device__ __forceinline__ uint32_t psmem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(kProjThreads, 4) k_project(ProjectArgs a, CamBatch cb) {
+    extern __shared__ __align__(128) unsigned char psm_raw[];
+    ProjSmem &ps = *reinterpret_cast<ProjSmem *>(psm_raw);
+    const int64_t i0 = (int64_t)blockIdx.x * kProjThreads;
+    const int li = threadIdx.x;
+    const int64_t i = i0 + li;
+    const int cnt = (int)(a.n - i0 < kProjThreads ? a.n - i0 : kProjThreads);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&ps.bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const float *src[8] = {a.centers, a.rotations, a.scales, a.w1, a.b1, a.w2, a.b2, a.sh};
+        float *dst[8] = {ps.centers, ps.rot, ps.scales, ps.w1, ps.b1, ps.w2, ps.b2, ps.sh};
+        const int per[8] = {3, 4, 3, 24, 8, 8, 1, 48};
+        uint32_t total = 0, bytes[8];
+        for (int k = 0; k < 8; ++k) {
+            bytes[k] = ((uint32_t)(cnt * per[k] * 4) + 15u) & ~15u;   // arrays are padded in the allocation
+            total += bytes[k];
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(&ps.bar)), "r"(total)
+                     : "memory");
+        for (int k = 0; k < 8; ++k)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    psmem_u32(dst[k])),
+                "l"(src[k] + i0 * per[k]), "r"(bytes[k]), "r"(psmem_u32(&ps.bar))
+                : "memory");
+    }
+    __syncthreads();
+    {
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(ok)
+                : "r"(psmem_u32(&ps.bar))
+                : "memory");
+    }
+    unsigned long long n_vis = 0;
+    for (int vloc = 0; vloc < cb.nv; ++vloc) {
     const int64_t view = cb.view0 + vloc;
     const DevCam &cam = cb.cams[vloc];
     bool visible = false;
@@ -80,9 +135,9 @@ __global__ void __launch_bounds__(256, 2) k_project(ProjectArgs a, CamBatch cb) 
         short4 rect = make_short4(-1, -1, -1, -1);
         uint32_t dep = 0;
         double R[9];
-        const float mu0 = a.centers[3 * i], mu1 = a.centers[3 * i + 1], mu2 = a.centers[3 * i + 2];
-        const float s0f = a.scales[3 * i], s1f = a.scales[3 * i + 1], s2f = a.scales[3 * i + 2];
-        float4 qv = reinterpret_cast<const float4 *>(a.rotations)[i];
+        const float mu0 = ps.centers[3 * li], mu1 = ps.centers[3 * li + 1], mu2 = ps.centers[3 * li + 2];
+        const float s0f = ps.scales[3 * li], s1f = ps.scales[3 * li + 1], s2f = ps.scales[3 * li + 2];
+        float4 qv = reinterpret_cast<const float4 *>(ps.rot)[li];
         float q4[4] = {qv.x, qv.y, qv.z, qv.w};
         double Rc[9], S[9], m[3];
         double zmin = 0.0;
@@ -206,14 +261,16 @@ __global__ void __launch_bounds__(256, 2) k_project(ProjectArgs a, CamBatch cb) 
                     const double A00 = Q[0], A01 = Q[1], A11 = Q[4], l0 = Q[2], l1 = Q[5], kq = Q[8];
                     const double det = A00 * A11 - A01 * A01;
                     if (det > 0.0 && A00 > 0.0) {
-                        const double u0 = -(A11 * l0 - A01 * l1) / det;
-                        const double v0 = -(A00 * l1 - A01 * l0) / det;
+                        const double idet = 1.0 / det;
+                        const double u0 = -(A11 * l0 - A01 * l1) * idet;
+                        const double v0 = -(A00 * l1 - A01 * l0) * idet;
                         const double qc = kq + l0 * u0 + l1 * v0;
                         if (qc < 0.0) {
                             const double fx = cam.fx, fy = cam.fy;
-                            const double an = A00 / (-qc) / (fx * fx);
-                            const double bn = A01 / (-qc) / (fx * fy);
-                            const double cn = A11 / (-qc) / (fy * fy);
+                            const double iq = -1.0 / qc, ifx = 1.0 / fx, ify = 1.0 / fy;
+                            const double an = A00 * iq * (ifx * ifx);
+                            const double bn = A01 * iq * (ifx * ify);
+                            const double cn = A11 * iq * (ify * ify);
                             const double x0 = fx * u0 + (double)cam.cx, y0 = fy * v0 + (double)cam.cy;
                             const double lmax = 0.5 * (an + cn) + sqrt(0.25 * (an - cn) * (an - cn) + bn * bn);
                             const double delta = ldexp(fabs(x0) + fabs(y0) + 1.0, -21);
@@ -242,19 +299,23 @@ __global__ void __launch_bounds__(256, 2) k_project(ProjectArgs a, CamBatch cb) 
             {
                 double nd = sqrt(mw0 * mw0 + mw1 * mw1 + mw2 * mw2);
                 double x = 0.0, y = 0.0, z = 1.0;
-                if (nd > 0.0) { x = mw0 / nd; y = mw1 / nd; z = mw2 / nd; }
-                sh_rgb(a.sh_degree, a.sh + 48 * i, x, y, z, rgb);
+                if (nd > 0.0) {
+                    const double ind = 1.0 / nd;
+                    x = mw0 * ind; y = mw1 * ind; z = mw2 * ind;
+                }
+                sh_rgb(a.sh_degree, ps.sh + 48 * li, x, y, z, rgb);
             }
-            // whitening Wh = diag(1/s) R^T (world -> unit-sphere frame)
+            // whitening Wh = diag(1/s) R^T (world -> unit-sphere frame); fp32 suffices
             float Wh[9];
+            {
+                const float is[3] = {1.0f / s0f, 1.0f / s1f, 1.0f / s2f};
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const double sk = k == 0 ? s0 : (k == 1 ? s1 : s2);
+                for (int k = 0; k < 3; ++k)
 #pragma unroll
-                for (int j = 0; j < 3; ++j) Wh[3 * k + j] = (float)(R[3 * j + k] / sk);
+                    for (int j = 0; j < 3; ++j) Wh[3 * k + j] = (float)R[3 * j + k] * is[k];
             }
             float4 *rec = a.records + o * 16;
-            const float b2 = a.b2[i];
+            const float b2 = ps.b2[li];
             rec[kRecConic] = make_float4(cx0, cy0, ca, cb2);
             rec[kRecConicRgb] = make_float4(cc, rgb[0], rgb[1], rgb[2]);
             rec[kRecMh] = make_float4(mh0, mh1, mh2, b2);
@@ -263,9 +324,9 @@ __global__ void __launch_bounds__(256, 2) k_project(ProjectArgs a, CamBatch cb) 
             rec[kRecWh1] = make_float4(Wh[5], Wh[6], Wh[7], Wh[8]);
             // MLP (Eq. 6) with the Eq. 5 normalisation folded in: W1' = omega W1 / ||s||_inf
             const double om = (double)a.omega;
-            const float4 *w1v = reinterpret_cast<const float4 *>(a.w1 + (int64_t)24 * i);
-            const float4 *b1v = reinterpret_cast<const float4 *>(a.b1 + (int64_t)8 * i);
-            const float4 *w2v = reinterpret_cast<const float4 *>(a.w2 + (int64_t)8 * i);
+            const float4 *w1v = reinterpret_cast<const float4 *>(ps.w1 + 24 * li);
+            const float4 *b1v = reinterpret_cast<const float4 *>(ps.b1 + 8 * li);
+            const float4 *w2v = reinterpret_cast<const float4 *>(ps.w2 + 8 * li);
             float w1[24], b1[8];
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
@@ -277,18 +338,20 @@ __global__ void __launch_bounds__(256, 2) k_project(ProjectArgs a, CamBatch cb) 
                 float4 t = b1v[k];
                 b1[4 * k] = t.x; b1[4 * k + 1] = t.y; b1[4 * k + 2] = t.z; b1[4 * k + 3] = t.w;
             }
-            const double sc = om / smax;
+            const float scf = (float)(om / smax), omf = a.omega;
 #pragma unroll
             for (int k = 0; k < kHidden; ++k)
-                rec[kRecUnits + k] = make_float4((float)(sc * w1[3 * k]), (float)(sc * w1[3 * k + 1]),
-                                                 (float)(sc * w1[3 * k + 2]), (float)(om * b1[k]));
+                rec[kRecUnits + k] = make_float4(scf * w1[3 * k], scf * w1[3 * k + 1], scf * w1[3 * k + 2],
+                                                 omf * b1[k]);
             rec[kRecW2] = w2v[0];
             rec[kRecW2 + 1] = w2v[1];
         }
     }
+    n_vis += visible;
+    }   // views
     // warp-aggregated visible count
-    unsigned vb = __ballot_sync(0xffffffffu, visible);
-    if ((threadIdx.x & 31) == 0 && vb) atomicAdd(a.counters + kCntVisible, (unsigned long long)__popc(vb));
+    const uint32_t vb = __reduce_add_sync(0xffffffffu, (uint32_t)n_vis);
+    if ((threadIdx.x & 31) == 0 && vb) atomicAdd(a.counters + kCntVisible, (unsigned long long)vb);
 }
 
 // Input validation: q nonzero, s > 0, every value finite.
@@ -323,8 +386,13 @@ __global__ void k_validate(ProjectArgs a, int *bad) {
 
 cudaError_t launch_project(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
     if (a.n == 0) return cudaSuccess;
-    dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)cams.nv);
-    k_project<<<grid, 256, 0, st>>>(a, cams);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ProjSmem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_project<<<(unsigned)((a.n + kProjThreads - 1) / kProjThreads), kProjThreads, sizeof(ProjSmem), st>>>(a, cams);
     return cudaGetLastError();
 }
 

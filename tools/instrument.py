@@ -18,5 +18,6 @@ snp.render_views(h, cams, opts, out)
 torch.cuda.synchronize()
 c = snp.get_debug_counters(h).astype(np.float64)
 tot = c[21]
-print(cfg, "consumer-warp cycles: wait %.1f%%  rounds %.1f%%  emit %.1f%%  other %.1f%%  rounds=%d avg_lanes=%.1f total=%.3g" % (
-    100 * c[16] / tot, 100 * c[17] / tot, 100 * c[18] / tot, 100 * (tot - c[16] - c[17] - c[18]) / tot, c[19], c[20] / max(c[19], 1), tot))
+print(cfg, "consumer-warp cycles: wait %.1f%%  rounds %.1f%%  emit %.1f%%  fill %.1f%%  pre %.1f%%  other %.1f%%  rounds=%d avg_lanes=%.1f total=%.3g" % (
+    100 * c[16] / tot, 100 * c[17] / tot, 100 * c[18] / tot, 100 * c[22] / tot, 100 * c[23] / tot,
+    100 * (tot - c[16] - c[17] - c[18] - c[22] - c[23]) / tot, c[19], c[20] / max(c[19], 1), tot))
