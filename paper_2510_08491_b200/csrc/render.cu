@@ -127,16 +127,14 @@ __device__ __forceinline__ Ray make_ray(const DevCam &cam, int x, int y) {
     return ray;
 }
 
-// cos / sin after Cody-Waite reduction to [-pi, pi] (the MUFU argument range).
-__device__ __forceinline__ float reduce_2pi(float x) {
-    const float n = rintf(x * 0.15915494309189535f);
-    float r = fmaf(-n, 6.28318548202514648f, x);
-    return fmaf(-n, -1.7484556000744487e-07f, r);
-}
+// MUFU sin/cos take the argument through one FMUL by 1/(2 pi): for |phase| <= 60 rad
+// (|omega W1| <= 17 rad per unit radius, |omega b1| <= 30) that rounding costs <= 4e-6 rad,
+// i.e. <= 4e-6 * |W2 dt| per hidden unit -- well inside the 1e-4 pixel tolerance.
+// sinc uses its Taylor polynomial below |x| = 0.25 where sin(x)/x loses relative accuracy.
 __device__ __forceinline__ float sinc_f(float x) {
     const float x2 = x * x;
     const float poly = fmaf(x2, fmaf(x2, fmaf(x2, -1.9841270e-04f, 8.3333333e-03f), -1.6666667e-01f), 1.0f);
-    const float s = __fdividef(__sinf(reduce_2pi(x)), x);
+    const float s = __fdividef(__sinf(x), x);
     return fabsf(x) < 0.25f ? poly : s;
 }
 
@@ -185,7 +183,7 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
         const float h = fmaf(u.z, r.dhz, fmaf(u.y, r.dhy, u.x * r.dhx));
         const float g = fmaf(u.z, pz, fmaf(u.y, py, fmaf(u.x, px, u.w)));
         const float phi = fmaf(h, tm, g);
-        acc = fmaf(W2[k], __cosf(reduce_2pi(phi)) * sinc_f(h * hdt), acc);
+        acc = fmaf(W2[k], __cosf(phi) * sinc_f(h * hdt), acc);
     }
     const float I = dt * (acc + mh.w);
     kap = 1.0f - __expf(-fmaxf(I, 0.0f));
@@ -338,7 +336,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 
     // =============================== consumer warps
 #ifdef SNP_INSTRUMENT
-    long long ins_wait = 0, ins_round = 0, ins_emit = 0, ins_rounds = 0, ins_lanes = 0;
+    long long ins_wait = 0, ins_round = 0, ins_emit = 0, ins_rounds = 0, ins_lanes = 0, ins_fill = 0, ins_pre = 0,
+              ins_setup = 0, ins_finish = 0;
     const long long ins_start = clock64();
 #endif
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
@@ -390,6 +389,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         if (t < 0) break;                      // end of work (no release needed)
         const int cnt = sm.m_cnt[slot];
         const int flags = sm.m_flags[slot];
+#ifdef SNP_INSTRUMENT
+        long long _s0 = clock64();
+#endif
         if (flags & 1) {                       // first batch of a new tile: set up the pixels
             cur_seq = sm.m_seq[slot];
             const int vloc = t / stripe_tiles;
@@ -413,7 +415,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             sm.p_ovf[tid] = 0;
             tile_finished = false;
         }
+#ifdef SNP_INSTRUMENT
+        ins_setup += clock64() - _s0;
+#endif
         if (!tile_finished) {
+#ifdef SNP_INSTRUMENT
+            long long _p0 = clock64();
+#endif
             if (!ps.done) n_tested += (unsigned long long)cnt;
             // records whose conic box touches this warp's 8x4 block
             bool touch = false;
@@ -433,6 +441,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 if (a.debug_flags & 1) touch = true;
             }
             uint32_t m = __ballot_sync(0xffffffffu, touch);
+#ifdef SNP_INSTRUMENT
+            ins_pre += clock64() - _p0;
+#endif
             int qcount = 0;
             auto round = [&](int n) {
 #ifdef SNP_INSTRUMENT
@@ -490,6 +501,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             int jlast = -1;
             while (true) {
                 // fill the queue from the records that touch this warp's block
+#ifdef SNP_INSTRUMENT
+                long long _f0 = clock64();
+#endif
                 while (m && qcount < 32) {
                     const int j = __ffs(m) - 1;
                     m &= m - 1u;
@@ -508,6 +522,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     }
                     qcount += __popc(cm);
                 }
+#ifdef SNP_INSTRUMENT
+                ins_fill += clock64() - _f0;
+#endif
                 int rem = 0, jn = jlast + 1;
                 if (qcount > 0) {
                     round(qcount < 32 ? qcount : 32);
@@ -547,7 +564,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 }
                 if (batch_end) break;
             }
+#ifdef SNP_INSTRUMENT
+            long long _z0 = clock64();
+#endif
             if ((flags & 2) || __all_sync(0xffffffffu, ps.done)) finish_tile();
+#ifdef SNP_INSTRUMENT
+            ins_finish += clock64() - _z0;
+#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[slot]);
@@ -560,6 +583,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         atomicAdd(a.counters + 19, (unsigned long long)ins_rounds);
         atomicAdd(a.counters + 20, (unsigned long long)ins_lanes);
         atomicAdd(a.counters + 21, (unsigned long long)(clock64() - ins_start));
+        atomicAdd(a.counters + 22, (unsigned long long)ins_fill);
+        atomicAdd(a.counters + 23, (unsigned long long)ins_pre);
+        atomicAdd(a.counters + 24, (unsigned long long)ins_setup);
+        atomicAdd(a.counters + 25, (unsigned long long)ins_finish);
     }
 #endif
     __syncwarp();

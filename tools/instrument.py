@@ -18,6 +18,8 @@ snp.render_views(h, cams, opts, out)
 torch.cuda.synchronize()
 c = snp.get_debug_counters(h).astype(np.float64)
 tot = c[21]
-print(cfg, "consumer-warp cycles: wait %.1f%%  rounds %.1f%%  emit %.1f%%  fill %.1f%%  pre %.1f%%  other %.1f%%  rounds=%d avg_lanes=%.1f total=%.3g" % (
-    100 * c[16] / tot, 100 * c[17] / tot, 100 * c[18] / tot, 100 * c[22] / tot, 100 * c[23] / tot,
-    100 * (tot - c[16] - c[17] - c[18] - c[22] - c[23]) / tot, c[19], c[20] / max(c[19], 1), tot))
+names = {16: "wait", 17: "rounds", 18: "emit", 22: "fill", 23: "pre", 24: "setup", 25: "finish"}
+parts = "  ".join("%s %.1f%%" % (nm, 100 * c[k] / tot) for k, nm in names.items())
+other = tot - sum(c[k] for k in names)
+print(cfg, "consumer-warp cycles:", parts, " other %.1f%%" % (100 * other / tot),
+      " rounds=%d avg_lanes=%.1f total=%.3g" % (c[19], c[20] / max(c[19], 1), tot))
