@@ -57,8 +57,9 @@ struct __align__(16) Smem {
     int32_t next_tile;
     uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs:
     uint8_t ql[kWarps][64];                   //   (record slot j, owner lane)
-    float p_thi[kPend][kWarps * 32];          // pending hits, unsorted, one column per pixel
-    float p_tlo[kPend][kWarps * 32];
+    float p_thi[kPend][kWarps * 32];          // pending hits, unsorted, one column per pixel: t_in
+                                              // (fp32: its 6e-8 rounding is far below the 1e-6
+                                              // near-tie flag of R23), kappa, primitive id
     float p_kap[kPend][kWarps * 32];
     uint32_t p_id[kPend][kWarps * 32];
     int32_t p_n[kWarps * 32];                 // pending count (appended to by any lane of the warp)
@@ -218,14 +219,14 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_
     int n = sm.p_n[tid];
     while (n > 0) {
         int kmin = 0;
-        float mh = sm.p_thi[0][tid], ml = sm.p_tlo[0][tid];
+        float mh = sm.p_thi[0][tid];
         uint32_t mid = sm.p_id[0][tid];
         for (int k = 1; k < n; ++k) {
-            const float h = sm.p_thi[k][tid], l = sm.p_tlo[k][tid];
+            const float h = sm.p_thi[k][tid];
             const uint32_t id = sm.p_id[k][tid];
-            if (before(h, l, id, mh, ml, mid)) { mh = h; ml = l; mid = id; kmin = k; }
+            if (h < mh || (h == mh && id < mid)) { mh = h; mid = id; kmin = k; }
         }
-        if (!(mh < L || (mh == L && ml < 0.f))) break;
+        if (!(mh < L)) break;
         const float kap = sm.p_kap[kmin][tid];
         const float4 rgb = __ldg(recs + (size_t)mid * 16 + kRecConicRgb);
         const float w = ps.T * kap;
@@ -237,7 +238,6 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_
         --n;
         if (kmin != n) {
             sm.p_thi[kmin][tid] = sm.p_thi[n][tid];
-            sm.p_tlo[kmin][tid] = sm.p_tlo[n][tid];
             sm.p_kap[kmin][tid] = sm.p_kap[n][tid];
             sm.p_id[kmin][tid] = sm.p_id[n][tid];
         }
@@ -269,6 +269,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 
     if (wid == kConsumers) {
         // =============================== producer warp
+#ifdef SNP_INSTRUMENT
+        long long p_wait = 0;
+        const long long p_start = clock64();
+#endif
         uint32_t gb = 0;            // global batch counter (ring slot / phase)
         int seq = 0;
         while (true) {
@@ -278,7 +282,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             const int slot0 = (int)(gb % kStages);
             if (gb >= kStages) {
                 const uint32_t eph = ((gb / kStages) - 1) & 1;
+#ifdef SNP_INSTRUMENT
+                long long _w0 = clock64();
+#endif
                 while (!mbar_try(&sm.empty[slot0], eph)) {}
+#ifdef SNP_INSTRUMENT
+                p_wait += clock64() - _w0;
+#endif
             }
             if (t >= total_tiles) {           // end marker
                 if (lane == 0) {
@@ -305,7 +315,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     if (*(volatile int32_t *)&sm.tdone[seq % kTileRing] >= kConsumers) break;   // all done
                     if (gb >= kStages) {
                         const uint32_t eph = ((gb / kStages) - 1) & 1;
+#ifdef SNP_INSTRUMENT
+                        long long _w1 = clock64();
+#endif
                         while (!mbar_try(&sm.empty[slot], eph)) {}
+#ifdef SNP_INSTRUMENT
+                        p_wait += clock64() - _w1;
+#endif
                     }
                 }
                 const uint32_t e0 = beg + (uint32_t)bt * kBatch;
@@ -331,6 +347,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             }
             ++seq;
         }
+#ifdef SNP_INSTRUMENT
+        if (lane == 0) {
+            atomicAdd(a.counters + 26, (unsigned long long)p_wait);
+            atomicAdd(a.counters + 27, (unsigned long long)(clock64() - p_start));
+        }
+#endif
         return;
     }
 
@@ -477,7 +499,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     const int k = base + __popc(peers & lt_mask);
                     if (k < plimit) {
                         sm.p_thi[k][ot] = th;
-                        sm.p_tlo[k][ot] = tl;
                         sm.p_kap[k][ot] = kap;
                         sm.p_id[k][ot] = sm.id[slot][j];
                     }

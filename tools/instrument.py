@@ -23,3 +23,4 @@ parts = "  ".join("%s %.1f%%" % (nm, 100 * c[k] / tot) for k, nm in names.items(
 other = tot - sum(c[k] for k in names)
 print(cfg, "consumer-warp cycles:", parts, " other %.1f%%" % (100 * other / tot),
       " rounds=%d avg_lanes=%.1f total=%.3g" % (c[19], c[20] / max(c[19], 1), tot))
+print(cfg, "producer: waiting on free slots %.1f%% of its time" % (100 * c[26] / max(c[27], 1)))
