@@ -37,7 +37,7 @@ constexpr int kConsumers = 8;                      // consumer warps = 8x4 pixel
 constexpr int kThreads = (kConsumers + 1) * 32;    // + 1 producer warp
 constexpr int kWarps = kConsumers;
 constexpr int kBatch = 32;          // records per stage (one per producer lane)
-constexpr int kStages = 4;          // TMA ring depth
+constexpr int kStages = 5;          // TMA ring depth
 constexpr int kPend = 16;           // per-pixel pending hits (unsorted)
 constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
 constexpr int kFbGrid = 148 * 2;    // K6 blocks (one overflowed pixel per block at a time)
