@@ -111,15 +111,16 @@ struct Ray {
 };
 
 __device__ __forceinline__ Ray make_ray(const DevCam &cam, int x, int y) {
-    const double u = ((double)x + 0.5 - (double)cam.cx) / (double)cam.fx;
-    const double v = ((double)y + 0.5 - (double)cam.cy) / (double)cam.fy;
+    // d = normalize(R_wc ((x+.5-cx)/fx, (y+.5-cy)/fy, 1)) in FP64 (R6), split into hi + lo
+    const double u = ((double)x + 0.5 - (double)cam.cx) * (1.0 / (double)cam.fx);
+    const double v = ((double)y + 0.5 - (double)cam.cy) * (1.0 / (double)cam.fy);
     double r[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
         r[i] = (double)cam.R[3 * i] * u + (double)cam.R[3 * i + 1] * v + (double)cam.R[3 * i + 2];
-    const double nd = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    const double inv = rsqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
     Ray ray;
-    const double d0 = r[0] / nd, d1 = r[1] / nd, d2 = r[2] / nd;
+    const double d0 = r[0] * inv, d1 = r[1] * inv, d2 = r[2] * inv;
     ray.dhx = (float)d0; ray.dlx = (float)(d0 - (double)ray.dhx);
     ray.dhy = (float)d1; ray.dly = (float)(d1 - (double)ray.dhy);
     ray.dhz = (float)d2; ray.dlz = (float)(d2 - (double)ray.dhz);
