@@ -103,19 +103,12 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def _scene_tensors(scene, torch, dev):
-    import types
-    ns = types.SimpleNamespace(omega=scene.omega, sh_degree=scene.sh_degree)
-    for f in ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh"):
-        setattr(ns, f, torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).to(dev))
-    return ns
-
-
 def run_snp(args):
     import torch
     import torch.distributed as dist
 
     import synth
+    from paper_2510_08491_b200 import multigpu as mg
     from paper_2510_08491_b200 import snp
 
     ws, rank, local = _dist()
@@ -133,11 +126,12 @@ def run_snp(args):
     W, H = cam.width, cam.height
     st = torch.cuda.Stream(device=dev)
 
-    # X1: parameters broadcast once from rank 0 (flat [n, 99] fp32)
-    recs = torch.from_numpy(scene.records()).to(dev)
-    if ws > 1:
-        dist.broadcast(recs, src=0)
-    dscene = _scene_tensors(scene, torch, dev)
+    # X1: parameters broadcast once from rank 0 (flat [n, 99] fp32); every rank builds its
+    # scene from the broadcast copy
+    flat = mg.pack_params(scene, dev) if rank == 0 else torch.empty(0, device=dev)
+    flat = mg.broadcast_params(flat, scene.n, src=0)
+    dscene = mg.unpack_params(flat)
+    dscene.omega, dscene.sh_degree = scene.omega, scene.sh_degree
 
     h = snp.create_scene(dscene, local, st)
     out = torch.empty((1, H, W, 4), device=dev)
@@ -182,11 +176,7 @@ def run_snp(args):
     if ws > 1:
         dist.barrier()
     times = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(sum(times))
-    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = mg.max_over_ranks(float(sum(times)), dev)
     ms_per_step = total_ms / args.steps
     fps = ws * args.steps / (total_ms / 1e3)     # views (frames) per second, all GPUs
 
@@ -250,15 +240,10 @@ def run_snp(args):
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     snp.destroy(he)
-    te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-    if ws > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_fps = ws * e2e_steps / float(te.item())
+    e2e_fps = ws * e2e_steps / mg.max_over_ranks(e2e_s, dev)
 
     # X2: gather the last frames to rank 0 once (outside the timed region)
-    if ws > 1:
-        gl = [torch.empty_like(out) for _ in range(ws)] if rank == 0 else None
-        dist.gather(out, gl, dst=0)
+    mg.gather_frames(out, dst=0)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
