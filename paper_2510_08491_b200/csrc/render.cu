@@ -839,14 +839,15 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_
     if (tiles == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(a.counters + kCntTileQueue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
+    static int resident = 0;   // persistent grid: every CTA that fits, all SMs
+    if (!resident) {
+        int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render, kThreads, smem);
+        resident = std::max(1, sms) * std::max(1, per_sm);
     }
-    const int grid = std::min(tiles, 2 * sms);   // persistent: 2 CTAs per SM
+    const int grid = std::min(tiles, resident);
     k_render<<<grid, kThreads, smem, st>>>(a, cams);
     return cudaGetLastError();
 }
