@@ -338,10 +338,8 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
         }
         b.capacity = s->key_capacity;
     }
-    b.keys = s->keys0.p;
-    b.vals = s->vals0.p;
-    SNP_CUDA(launch_dup_only(b, st));
-    // K3: onesweep over the significant bits only
+    // K3 scratch: onesweep over the significant bits only; the digit histograms are
+    // accumulated by the duplication kernel itself
     const int bits = kDepthBits + s->tile_bits + s->view_bits;
     const int passes = (bits + 7) / 8;
     const int64_t maxp = (s->key_capacity + sort_partition_size() - 1) / sort_partition_size();
@@ -352,11 +350,17 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     SortScratch sc{};
     sc.hist = s->sort_scratch.p;
     sc.lookback = s->sort_scratch.p + 8 * 256;
-    sc.tickets = s->sort_scratch.p + 8 * 256 + (size_t)8 * maxp * 256;
+    sc.tickets = s->sort_scratch.p + 8 * 256 + (size_t)8 * s->sort_max_partitions * 256;
     sc.max_partitions = s->sort_max_partitions;
+    SNP_CUDA(cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 256 * passes, st));
+    b.keys = s->keys0.p;
+    b.vals = s->vals0.p;
+    b.hist = sc.hist;
+    b.passes = passes;
+    SNP_CUDA(launch_dup_only(b, st));
     int final_idx = 0;
     SNP_CUDA(launch_onesweep(s->keys0.p, s->vals0.p, s->keys1.p, s->vals1.p, s->key_capacity, s->counters.p,
-                             passes, sc, st, &final_idx));
+                             passes, sc, true, st, &final_idx));
     s->sorted_idx = final_idx;
     const uint64_t *sk = final_idx ? s->keys1.p : s->keys0.p;
     // K4

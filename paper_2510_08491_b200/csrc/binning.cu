@@ -10,8 +10,8 @@ namespace snp {
 namespace {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;                       // items per thread (blocked)
-constexpr int kScanTile = kScanThreads * kScanItems;  // 2048 items per block
+constexpr int kScanItems = 2;                       // items per thread (blocked)
+constexpr int kScanTile = kScanThreads * kScanItems;  // 512 items per block
 
 struct ItemInfo {
     uint32_t count;
@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(1024) k_scan_partials(BinArgs a, int64_t nbloc
 __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
     __shared__ uint32_t sw[32];
     __shared__ uint32_t s_off[kScanTile + 8];   // per item exclusive offset (block-relative)
+    __shared__ uint32_t s_hist[8][256];         // digit histograms of the keys this block emits
+    __shared__ int32_t s_x0[kScanTile], s_w[kScanTile], s_rf[kScanTile];   // item geometry, read once
+    __shared__ uint32_t s_dep[kScanTile];
+    for (int i = threadIdx.x; i < a.passes * 256; i += kScanThreads) (&s_hist[0][0])[i] = 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t total_items = a.n * a.n_views;
     const int64_t blk0 = (int64_t)blockIdx.x * kScanTile;
@@ -130,7 +134,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
     uint32_t s = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        cnt[k] = (base + k < total_items) ? item_info(a, base + k).count : 0u;
+        ItemInfo it{0, 0, 1, 0};
+        if (base + k < total_items) it = item_info(a, base + k);
+        cnt[k] = it.count;
+        const int li = threadIdx.x * kScanItems + k;
+        s_x0[li] = it.x0;
+        s_w[li] = it.w > 0 ? it.w : 1;
+        s_rf[li] = it.r_first;
+        s_dep[li] = (it.count && base + k < total_items) ? (a.depth[base + k] >> kDepthDrop) : 0u;
         s += cnt[k];
     }
     uint32_t tot;
@@ -156,20 +167,26 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
             if (s_off[mid] <= e) lo = mid; else hi = mid - 1;
         }
         const int64_t o = blk0 + lo;
-        const ItemInfo it = item_info(a, o);
+        const uint32_t w = (uint32_t)s_w[lo];
         const uint32_t k = e - s_off[lo];
-        const int32_t ri = (int32_t)(k / (uint32_t)it.w);
-        const int32_t c = (int32_t)(k - (uint32_t)ri * (uint32_t)it.w);
-        const int32_t row = it.r_first + ri * a.row_stride;
+        const int32_t ri = (int32_t)(k / w);
+        const int32_t c = (int32_t)(k - (uint32_t)ri * w);
+        const int32_t row = s_rf[lo] + ri * a.row_stride;
         const uint64_t view = (uint64_t)(o / a.n);
         const uint32_t prim = (uint32_t)(o - (int64_t)view * a.n);
-        const uint64_t tile = (uint64_t)row * (uint64_t)a.tiles_x + (uint64_t)(it.x0 + c);
-        const uint64_t key = (view << view_shift) | (tile << kDepthBits) | (uint64_t)(a.depth[o] >> kDepthDrop);
+        const uint64_t tile = (uint64_t)row * (uint64_t)a.tiles_x + (uint64_t)(s_x0[lo] + c);
+        const uint64_t key = (view << view_shift) | (tile << kDepthBits) | (uint64_t)s_dep[lo];
         const uint64_t g = gbase + e;
         if (g < (uint64_t)a.capacity) {
             a.keys[g] = key;
             a.vals[g] = prim;
+            for (int p = 0; p < a.passes; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
         }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.passes * 256; i += kScanThreads) {
+        const uint32_t v = (&s_hist[0][0])[i];
+        if (v) atomicAdd(a.hist + i, v);
     }
 }
 

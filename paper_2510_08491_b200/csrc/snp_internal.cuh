@@ -88,6 +88,8 @@ struct BinArgs {
     int64_t capacity;
     uint32_t *partials;     // scan scratch [num_blocks + 1]
     unsigned long long *counters;
+    uint32_t *hist;         // [passes][256] digit histograms accumulated during duplication (zeroed)
+    int32_t passes;
 };
 int64_t bin_scan_blocks(int64_t items);
 cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st);   // counts + scan -> counters[kCntDup]
@@ -107,8 +109,10 @@ size_t sort_scratch_words(int passes, int64_t max_partitions);
 // Sorts keys/vals (n read from counters[kCntDup], clamped to capacity) by bits
 // [0, 8*passes).  Ping-pongs between (k0,v0) and (k1,v1); returns in *final_idx
 // which buffer (0 or 1) holds the result.
+// hist_ready: the digit histograms were already accumulated (by the key
+// duplication kernel, zeroed before it); otherwise a histogram pass runs first.
 cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
-                            const unsigned long long *counters, int passes, SortScratch scratch,
+                            const unsigned long long *counters, int passes, SortScratch scratch, bool hist_ready,
                             cudaStream_t st, int *final_idx);
 
 struct RenderArgs {

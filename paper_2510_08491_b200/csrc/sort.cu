@@ -62,17 +62,16 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
     __shared__ uint32_t s_bstart[256];         // block-local start of digit
     __shared__ uint32_t s_excl[256];           // keys of this digit in earlier partitions
     __shared__ uint32_t s_scan[kWarps];
-    __shared__ int s_part;
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int shift = 8 * pass;
-    if (threadIdx.x == 0) s_part = (int)atomicAdd(tickets + pass, 1u);
-    for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&s_wh[0][0])[i] = 0;
-    __syncthreads();
     const int64_t n = sort_n(counters, capacity);
-    const int64_t part = s_part;
     const int64_t nparts = (n + kPart - 1) / kPart;
-    if (part >= nparts) return;
+    // Persistent: CTA c takes partitions c, c + G, ... in increasing order; the grid
+    // never exceeds the co-resident CTA count, so every partition a look-back waits
+    // on is owned by a running CTA that never waits on a later one (no deadlock).
+    for (int64_t part = blockIdx.x; part < nparts; part += gridDim.x) {
+    for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&s_wh[0][0])[i] = 0;
     const int64_t pbase = part * kPart;
 
     // ---- load (warp-striped: item k of lane l is key pbase + wid*384 + k*32 + l)
@@ -90,12 +89,18 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
             val[k] = 0;
         }
     }
-    // ---- stable warp ranking with match-any
+    __syncthreads();   // s_wh zeroed (and the previous partition's smem reads are done)
+    // ---- stable warp ranking: peers with the same digit from 8 ballots (no MATCH)
     const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
     for (int k = 0; k < kIpt; ++k) {
         const uint32_t d = (uint32_t)(key[k] >> shift) & 255u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t peers = 0xffffffffu;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? bal : ~bal;
+        }
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
         if (lane == leader) {
@@ -201,6 +206,8 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         kout[dest] = kk;
         vout[dest] = s_vals[i];
     }
+    __syncthreads();   // smem reuse by the next partition of this CTA
+    }
 }
 
 }  // namespace
@@ -212,26 +219,38 @@ size_t sort_scratch_words(int passes, int64_t max_partitions) {
 }
 
 cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
-                            const unsigned long long *counters, int passes, SortScratch sc,
+                            const unsigned long long *counters, int passes, SortScratch sc, bool hist_ready,
                             cudaStream_t st, int *final_idx) {
     *final_idx = 0;
     if (capacity == 0 || passes == 0) return cudaSuccess;
     const int64_t maxp = (capacity + kPart - 1) / kPart;
     if (maxp > sc.max_partitions) return cudaErrorInvalidValue;
-    cudaError_t e = cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 256 * passes, st);
-    if (e != cudaSuccess) return e;
+    static int resident = 0;
+    if (!resident) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass, kThreads, 0);
+        resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
+    }
+    cudaError_t e;
+    if (!hist_ready) {
+        e = cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 256 * passes, st);
+        if (e != cudaSuccess) return e;
+    }
     e = cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * 256 * (size_t)maxp * passes, st);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(sc.tickets, 0, sizeof(uint32_t) * passes, st);
-    if (e != cudaSuccess) return e;
-    int64_t hb = (capacity + kThreads * 16 - 1) / (kThreads * 16);
-    if (hb > 148 * 4) hb = 148 * 4;
-    k_hist<<<(unsigned)hb, kThreads, 0, st>>>(k0, capacity, counters, passes, sc.hist);
+    if (!hist_ready) {
+        int64_t hb = (capacity + kThreads * 16 - 1) / (kThreads * 16);
+        if (hb > 148 * 4) hb = 148 * 4;
+        k_hist<<<(unsigned)hb, kThreads, 0, st>>>(k0, capacity, counters, passes, sc.hist);
+    }
+    const unsigned grid = (unsigned)(maxp < resident ? maxp : resident);
     uint64_t *kin = k0, *kout = k1;
     uint32_t *vin = v0, *vout = v1;
     for (int p = 0; p < passes; ++p) {
-        k_pass<<<(unsigned)maxp, kThreads, 0, st>>>(kin, vin, kout, vout, capacity, counters, p, sc.hist,
-                                                    sc.lookback + (size_t)p * (size_t)maxp * 256, sc.tickets);
+        k_pass<<<grid, kThreads, 0, st>>>(kin, vin, kout, vout, capacity, counters, p, sc.hist,
+                                          sc.lookback + (size_t)p * (size_t)maxp * 256, sc.tickets);
         uint64_t *tk = kin; kin = kout; kout = tk;
         uint32_t *tv = vin; vin = vout; vout = tv;
     }
