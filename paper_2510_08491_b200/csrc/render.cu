@@ -133,10 +133,17 @@ __device__ __forceinline__ Ray make_ray(const DevCam &cam, int x, int y) {
 // (|omega W1| <= 17 rad per unit radius, |omega b1| <= 30) that rounding costs <= 4e-6 rad,
 // i.e. <= 4e-6 * |W2 dt| per hidden unit -- well inside the 1e-4 pixel tolerance.
 // sinc uses its Taylor polynomial below |x| = 0.25 where sin(x)/x loses relative accuracy.
+// MUFU reciprocal (rcp.approx: ~1 ulp), no special-case handling: callers divide by
+// values bounded away from 0 and infinity.
+__device__ __forceinline__ float rcp_fast(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float sinc_f(float x) {
     const float x2 = x * x;
     const float poly = fmaf(x2, fmaf(x2, fmaf(x2, -1.9841270e-04f, 8.3333333e-03f), -1.6666667e-01f), 1.0f);
-    const float s = __fdividef(__sinf(x), x);
+    const float s = __sinf(x) * rcp_fast(x);
     return fabsf(x) < 0.25f ? poly : s;
 }
 
@@ -166,7 +173,7 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
     if (!(disc > 0.0f)) return false;
     const float sq = disc * rsqrtf(disc);
     const float qq = -(B + copysignf(sq, B));
-    float t0 = __fdividef(qq, A), t1 = __fdividef(Cq, qq);
+    float t0 = qq * rcp_fast(A), t1 = Cq * rcp_fast(qq);
     if (t0 > t1) { const float t = t0; t0 = t1; t1 = t; }
     const float lo_lim = r.t_near - tc, hi_lim = r.t_far - tc;
     const bool clipped = !(t0 > lo_lim);
