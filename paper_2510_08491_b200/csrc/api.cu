@@ -426,7 +426,8 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
         for (const CamBatch &cb : s->cams) SNP_CUDA(launch_render(a, cb, st));
-        if (s->n > 0) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
+        // (SNP_DEBUG bit 2 skips K6: timing experiments only, overflowed pixels stay unwritten)
+        if (s->n > 0 && !(a.debug_flags & 2)) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
     }
     if (opts->out_memory == SNP_MEM_HOST) {
         SNP_CUDA(cudaMemcpyAsync(out_rgba, dout, out_floats * sizeof(float), cudaMemcpyDeviceToHost, st));

@@ -40,7 +40,6 @@ constexpr int kBatch = 32;          // records per stage (one per producer lane)
 constexpr int kStages = 5;          // TMA ring depth
 constexpr int kPend = 16;           // per-pixel pending hits (unsorted)
 constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
-constexpr int kFbGrid = 148 * 2;    // K6 blocks (one overflowed pixel per block at a time)
 
 struct __align__(16) Smem {
     float4 rec[kStages][kBatch][16];          // 32 KB of records, cp.async.bulk-staged
@@ -79,12 +78,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, u
 __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// suspend-time hint: the waiting warp sleeps until the phase completes (or the hint
+// expires) instead of spinning on issue slots the working warps need
+constexpr uint32_t kSuspendNs = 0x989680;
 __device__ __forceinline__ bool mbar_try(unsigned long long *bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs)
         : "memory");
     return ok != 0;
 }
@@ -637,6 +639,8 @@ __device__ __forceinline__ bool fb_hit(const float4 *rec, const Ray &ray, float 
 // block-wide repeated selection instead (same result, slower).
 constexpr int kFbThreads = 256;
 constexpr int kFbHits = 2048;
+constexpr int kFbIlp = 4;
+constexpr int kFbRank = 512;
 constexpr int kFbPer = kFbHits / kFbThreads;   // 8 sorted entries per thread in phase C
 
 struct FbSmem {
@@ -674,23 +678,74 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
         const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
         if (tid == 0) sm.count = 0;
         __syncthreads();
+#ifdef SNP_INSTRUMENT
+        const long long _fa = clock64();
+#endif
         // ---- phase A: every hit of the tile list, once
-        for (uint32_t e = beg + tid; e < end; e += kFbThreads) {
-            const uint32_t id = a.vals[e];
-            float th, tl, kap;
-            if (fb_hit(recs + (size_t)id * 16, ray, pxf, pyf, th, tl, kap)) {
-                const int pos = atomicAdd(&sm.count, 1);
-                if (pos < kFbHits) {
-                    sm.t[pos] = th; sm.l[pos] = tl; sm.k[pos] = kap; sm.id[pos] = id;
+        // kFbIlp independent records per thread per step: the id and conic loads of a
+        // step are all in flight together (the loop is latency-bound otherwise)
+        for (uint32_t e0 = beg + tid; e0 < end; e0 += kFbThreads * kFbIlp) {
+            uint32_t ids[kFbIlp];
+            bool cand[kFbIlp];
+#pragma unroll
+            for (int u = 0; u < kFbIlp; ++u) {
+                const uint32_t e = e0 + (uint32_t)(u * kFbThreads);
+                ids[u] = e < end ? a.vals[e] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < kFbIlp; ++u) {
+                cand[u] = false;
+                if (ids[u] != 0xffffffffu) {
+                    const float4 *rec = recs + (size_t)ids[u] * 16;
+                    const float4 c0 = rec[kRecConic];
+                    const float cc = rec[kRecConicRgb].x;
+                    const float dx = pxf - c0.x, dy = pyf - c0.y;
+                    cand[u] = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx)) <= 1.0f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kFbIlp; ++u) {
+                float th, tl, kap;
+                if (cand[u] && exact_hit(recs + (size_t)ids[u] * 16, ray, th, tl, kap)) {
+                    const int pos = atomicAdd(&sm.count, 1);
+                    if (pos < kFbHits) {
+                        sm.t[pos] = th; sm.l[pos] = tl; sm.k[pos] = kap; sm.id[pos] = ids[u];
+                    }
                 }
             }
         }
         __syncthreads();
         const int n = sm.count;
+#ifdef SNP_INSTRUMENT
+        const long long _fb = clock64();
+        if (tid == 0) {
+            atomicAdd(a.counters + 28, (unsigned long long)(_fb - _fa));
+            atomicAdd(a.counters + 31, (unsigned long long)n + ((unsigned long long)(end - beg) << 32));
+        }
+#endif
         float T = 1.f, cr = 0.f, cg = 0.f, cbl = 0.f;
         unsigned long long ncomp = 0;
         if (n <= kFbHits) {
-            // ---- phase B: bitonic sort of indices
+            // ---- phase B: sort of indices.  Up to kFbRank hits: rank sort (the rank of
+            // hit i is the number of hits before it in the strict total order (t_in, id);
+            // one pass, no block barriers).  Above: bitonic network.
+            if (n <= kFbRank) {
+                // g = 256 / n rounded down to a power of two (<= 32) lanes share one hit's count
+                int g = 1;
+                while (g < 32 && g * 2 * n <= kFbThreads) g <<= 1;
+                const int part = tid & (g - 1);
+                for (int i0 = tid / g; i0 < (n + kFbThreads / g - 1) / (kFbThreads / g) * (kFbThreads / g);
+                     i0 += kFbThreads / g) {
+                    const int i = i0 < n ? i0 : n - 1;
+                    const float ti = sm.t[i], li = sm.l[i];
+                    const uint32_t di = sm.id[i];
+                    int r = 0;
+                    for (int j = part; j < n; j += g) r += before(sm.t[j], sm.l[j], sm.id[j], ti, li, di);
+                    for (int o = 1; o < g; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+                    if (part == 0 && i0 < n) sm.idx[r] = (uint16_t)i;
+                }
+                __syncthreads();
+            } else {
             int n2 = 1;
             while (n2 < n) n2 <<= 1;
             for (int i = tid; i < n2; i += kFbThreads) sm.idx[i] = (uint16_t)i;
@@ -711,6 +766,10 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
                     __syncthreads();
                 }
             }
+            }
+#ifdef SNP_INSTRUMENT
+            if (tid == 0) atomicAdd(a.counters + 29, (unsigned long long)(clock64() - _fb));
+#endif
             // ---- phase C: transmittance before each sorted hit by a block product scan
             float om[kFbPer];
             float prod = 1.f;
@@ -771,6 +830,9 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
             T = lst >= 0 ? sm.wsum[0][3] : 1.f;
             ncomp = (unsigned long long)(lst + 1);
         } else {
+#ifdef SNP_INSTRUMENT
+            if (tid == 0) atomicAdd(a.counters + 30, 1ull);
+#endif
             // ---- too many hits for shared memory: block-wide repeated selection
             float lh = -INFINITY, ll = 0.f;
             uint32_t lid = 0;
@@ -851,7 +913,15 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_
 }
 
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
-    for (int i = 0; i < n_batches; ++i) k_fallback<<<kFbGrid, kFbThreads, 0, st>>>(a, cams[i]);
+    static int resident = 0;   // every CTA that fits, all SMs (the queue loop strides by the grid)
+    if (!resident) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback, kFbThreads, 0);
+        resident = std::max(1, sms) * std::max(1, per_sm);
+    }
+    for (int i = 0; i < n_batches; ++i) k_fallback<<<resident, kFbThreads, 0, st>>>(a, cams[i]);
     return cudaGetLastError();
 }
 
