@@ -76,6 +76,7 @@ struct snp_scene_s {
     DevBuf<uint64_t> keys0, keys1;
     DevBuf<uint32_t> vals0, vals1;
     int64_t key_capacity = 0;
+    int64_t known_ndup = 0;    // key count seen by the last sync_check (sizes the sort grid only)
     DevBuf<uint32_t> partials;
     DevBuf<uint32_t> sort_scratch;
     int64_t sort_max_partitions = 0;
@@ -92,7 +93,24 @@ struct snp_scene_s {
     unsigned long long *h_counters = nullptr;  // pinned
     DevBuf<int> flag;
     int *h_flag = nullptr;                     // pinned
+    // K1b (render records) runs on a side stream forked from the caller's stream
+    // after K1a and joined at the end of snp_bin_sort (also under stream capture)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool join_pending = false;
 };
+
+namespace snp {
+int greatest_priority() {
+    static int prio = 1;   // 1 = not queried yet (priorities are <= 0)
+    if (prio == 1) {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) hi = 0;
+        prio = hi;
+    }
+    return prio;
+}
+}  // namespace snp
 
 namespace {
 
@@ -197,6 +215,11 @@ snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stre
     if (ce == cudaSuccess) ce = cudaMallocHost((void **)&s->h_counters, sizeof(unsigned long long) * kNumCounters);
     if (ce == cudaSuccess) ce = cudaMallocHost((void **)&s->h_flag, 2 * sizeof(int));
     if (ce == cudaSuccess) ce = cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kNumCounters, st);
+    // K1b's side stream keeps the default (lowest) priority: the K2-K4 chain it overlaps
+    // is launched with the greatest priority and takes SM slots first (launch_hi)
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
     if (ce != cudaSuccess) {
         snp_destroy(s);
         return fail(ce == cudaErrorMemoryAllocation ? SNP_ERR_OUT_OF_MEMORY : SNP_ERR_CUDA,
@@ -224,6 +247,10 @@ snp_status snp_update_scene(snp_scene s, const snp_scene_desc *d, void *cuda_str
     if (d->n != s->n) return fail(SNP_ERR_INVALID_ARGUMENT, "snp_update_scene: n differs from the scene's");
     s->sh_degree = d->sh_degree;
     s->omega = d->omega;
+    if (s->join_pending) {   // K1b may still read the parameters being replaced
+        SNP_CUDA(cudaStreamWaitEvent((cudaStream_t)cuda_stream, s->ev_join, 0));
+        s->join_pending = false;
+    }
     r = upload_and_validate(s, d, (cudaStream_t)cuda_stream);
     if (r != SNP_OK) return r;
     s->state = kCreated;   // parameters changed: project again
@@ -276,10 +303,20 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
         }
         s->cams.push_back(cb);
     }
+    if (s->join_pending) {   // a previous K1b (project without bin_sort) must finish first
+        SNP_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+        s->join_pending = false;
+    }
     SNP_CUDA(cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kNumCounters, st));
     ProjectArgs a{};
     fill_args(s, a);
-    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_project(a, cb, st));
+    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_bin_geom(a, cb, st));
+    // fork: K1b on the side stream, overlapping K2-K4 (which need only K1a's output)
+    SNP_CUDA(cudaEventRecord(s->ev_fork, st));
+    SNP_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_records(a, cb, std::getenv("SNP_SERIAL_K1B") ? st : s->side));
+    SNP_CUDA(cudaEventRecord(s->ev_join, s->side));
+    s->join_pending = true;
     s->state = kProjected;
     return SNP_OK;
 }
@@ -330,6 +367,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
                                  cudaMemcpyDeviceToHost, st));
         SNP_CUDA(cudaStreamSynchronize(st));
         const int64_t ndup = (int64_t)s->h_counters[kCntDup];
+        s->known_ndup = ndup;
         if (ndup > s->key_capacity) {
             s->key_capacity = ndup + ndup / 4 + 1024;
             SNP_CUDA(alloc_keys(s->key_capacity));
@@ -360,7 +398,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     SNP_CUDA(launch_dup_only(b, st));
     int final_idx = 0;
     SNP_CUDA(launch_onesweep(s->keys0.p, s->vals0.p, s->keys1.p, s->vals1.p, s->key_capacity, s->counters.p,
-                             passes, sc, true, st, &final_idx));
+                             passes, sc, true, s->known_ndup + s->known_ndup / 8, st, &final_idx));
     s->sorted_idx = final_idx;
     const uint64_t *sk = final_idx ? s->keys1.p : s->keys0.p;
     // K4
@@ -368,6 +406,11 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     SNP_CUDA(s->ranges.ensure((size_t)slots * 2));
     SNP_CUDA(launch_tile_ranges(sk, s->counters.p, s->key_capacity, s->tile_bits, s->tiles_x * s->tiles_y,
                                 s->ranges.p, slots, st));
+    // join K1b: everything after bin_sort on the caller's stream sees the records
+    if (s->join_pending) {
+        SNP_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+        s->join_pending = false;
+    }
     s->state = kBinned;
     return SNP_OK;
 }
@@ -449,6 +492,9 @@ snp_status snp_destroy(snp_scene s) {
     if (!s) return SNP_OK;
     cudaSetDevice(s->device);
     cudaDeviceSynchronize();
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->side) cudaStreamDestroy(s->side);
     s->params.release();
     s->rects.release();
     s->depth.release();

@@ -215,15 +215,18 @@ cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         return cudaMemsetAsync(a.counters + kCntCapOverflow, 0, sizeof(unsigned long long), st);
     }
-    k_count_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(a);
-    k_scan_partials<<<1, 1024, 0, st>>>(a, nb);
+    cudaError_t e0 = launch_hi(k_count_reduce, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a);
+    if (e0 != cudaSuccess) return e0;
+    e0 = launch_hi(k_scan_partials, dim3(1), dim3(1024), 0, st, a, (int64_t)nb);
+    if (e0 != cudaSuccess) return e0;
     return cudaGetLastError();
 }
 
 cudaError_t launch_dup_only(const BinArgs &a, cudaStream_t st) {
     const int64_t nb = bin_scan_blocks(a.n * a.n_views);
     if (nb == 0) return cudaSuccess;
-    k_scan_dup<<<(unsigned)nb, kScanThreads, 0, st>>>(a);
+    cudaError_t e0 = launch_hi(k_scan_dup, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a);
+    if (e0 != cudaSuccess) return e0;
     return cudaGetLastError();
 }
 
@@ -235,7 +238,8 @@ cudaError_t launch_tile_ranges(const uint64_t *keys, const unsigned long long *c
     if (capacity == 0) return cudaSuccess;
     int64_t blocks = (capacity + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_tile_ranges<<<(unsigned)blocks, 256, 0, st>>>(keys, counters, capacity, tile_bits, tiles, ranges);
+    e = launch_hi(k_tile_ranges, dim3((unsigned)blocks), dim3(256), 0, st, keys, counters, capacity, tile_bits, tiles, ranges);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

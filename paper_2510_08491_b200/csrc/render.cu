@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     // =============================== consumer warps
 #ifdef SNP_INSTRUMENT
     long long ins_wait = 0, ins_round = 0, ins_emit = 0, ins_rounds = 0, ins_lanes = 0, ins_fill = 0, ins_pre = 0,
-              ins_setup = 0, ins_finish = 0;
+              ins_setup = 0, ins_finish = 0, ins_touch = 0, ins_empty = 0, ins_ecalls = 0, ins_enone = 0;
     const long long ins_start = clock64();
 #endif
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
@@ -543,6 +543,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                         ++n_cand;
                     }
                     qcount += __popc(cm);
+#ifdef SNP_INSTRUMENT
+                    ++ins_touch;
+                    ins_empty += (cm == 0u);
+#endif
                 }
 #ifdef SNP_INSTRUMENT
                 ins_fill += clock64() - _f0;
@@ -577,6 +581,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 if (!ps.done && (batch_end || sm.p_n[tid] > plimit - 4)) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
+                    ++ins_ecalls;
+                    ins_enone += (sm.p_n[tid] == 0);
 #endif
                     emit(sm, ps, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
                          a.t_floor, recs);
@@ -609,6 +615,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         atomicAdd(a.counters + 23, (unsigned long long)ins_pre);
         atomicAdd(a.counters + 24, (unsigned long long)ins_setup);
         atomicAdd(a.counters + 25, (unsigned long long)ins_finish);
+        atomicAdd(a.counters + 12, (unsigned long long)ins_touch);
+        atomicAdd(a.counters + 13, (unsigned long long)ins_empty);
+    }
+    {
+        const unsigned long long ec = __reduce_add_sync(0xffffffffu, (uint32_t)ins_ecalls);
+        const unsigned long long en = __reduce_add_sync(0xffffffffu, (uint32_t)ins_enone);
+        if (lane == 0) {
+            atomicAdd(a.counters + 14, ec);
+            atomicAdd(a.counters + 15, en);
+        }
     }
 #endif
     __syncwarp();

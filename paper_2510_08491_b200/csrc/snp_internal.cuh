@@ -9,6 +9,26 @@
 
 namespace snp {
 
+// Launch with the device's greatest scheduling priority.  Used for the K2-K4 chain
+// (latency-bound, on the frame's critical path) so that its CTAs take SM slots
+// ahead of the concurrently running K1b (side stream, default priority).
+int greatest_priority();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_hi(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = greatest_priority();
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr int kTile = 16;                 // BASELINE north_star: 16x16 tiles (R18)
 constexpr int kHidden = 8;                // N_sigma = 8
 constexpr int kCamsPerLaunch = 32;        // cameras passed by value per launch
@@ -74,7 +94,10 @@ struct ProjectArgs {
 
 // ---- host-side launchers (each .cu owns its kernels) ----
 cudaError_t launch_validate(const ProjectArgs &a, int *d_bad, cudaStream_t st);
-cudaError_t launch_project(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st);
+// K1a: cull + tile rect + depth key (critical path).  K1b: render records of the
+// visible pairs (reads K1a's rects; may run concurrently with K2-K4).
+cudaError_t launch_bin_geom(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st);
+cudaError_t launch_records(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st);
 
 struct BinArgs {
     int64_t n;              // primitives per view
@@ -108,12 +131,13 @@ int64_t sort_partition_size();
 size_t sort_scratch_words(int passes, int64_t max_partitions);
 // Sorts keys/vals (n read from counters[kCntDup], clamped to capacity) by bits
 // [0, 8*passes).  Ping-pongs between (k0,v0) and (k1,v1); returns in *final_idx
-// which buffer (0 or 1) holds the result.
+// which buffer (0 or 1) holds the result.  expected_n (the last host-known key
+// count, or 0) only sizes the persistent grid.
 // hist_ready: the digit histograms were already accumulated (by the key
 // duplication kernel, zeroed before it); otherwise a histogram pass runs first.
 cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
                             const unsigned long long *counters, int passes, SortScratch scratch, bool hist_ready,
-                            cudaStream_t st, int *final_idx);
+                            int64_t expected_n, cudaStream_t st, int *final_idx);
 
 struct RenderArgs {
     int32_t tiles_x, tiles_y, tiles_per_view;

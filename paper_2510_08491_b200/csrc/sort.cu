@@ -47,6 +47,14 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t *keys, int64_t
     }
 }
 
+#ifdef SNP_SORT_INSTRUMENT
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
     return *reinterpret_cast<const volatile uint32_t *>(p);
 }
@@ -70,6 +78,10 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
     // Persistent: CTA c takes partitions c, c + G, ... in increasing order; the grid
     // never exceeds the co-resident CTA count, so every partition a look-back waits
     // on is owned by a running CTA that never waits on a later one (no deadlock).
+#ifdef SNP_SORT_INSTRUMENT
+    unsigned long long _t0 = gtimer(), _t1 = 0, _t2 = 0, _t3 = 0;
+    if (threadIdx.x == 0) atomicMax(const_cast<unsigned long long *>(counters) + 16 + 3 * pass, ~_t0);
+#endif
     for (int64_t part = blockIdx.x; part < nparts; part += gridDim.x) {
     for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&s_wh[0][0])[i] = 0;
     const int64_t pbase = part * kPart;
@@ -90,6 +102,9 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         }
     }
     __syncthreads();   // s_wh zeroed (and the previous partition's smem reads are done)
+#ifdef SNP_SORT_INSTRUMENT
+    _t1 = gtimer();
+#endif
     // ---- stable warp ranking: peers with the same digit from 8 ballots (no MATCH)
     const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
@@ -112,6 +127,9 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         __syncwarp();
     }
     __syncthreads();
+#ifdef SNP_SORT_INSTRUMENT
+    _t2 = gtimer();
+#endif
     // ---- per digit: exclusive over warps, block count, block-local digit start
     const int d = threadIdx.x;  // kThreads == 256 == radix
     uint32_t cnt = 0;
@@ -156,6 +174,10 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         atomicExch(lb + part * 256 + d, kFlagInc | (sum + cnt));
         s_excl[d] = sum;
     }
+#ifdef SNP_SORT_INSTRUMENT
+    __syncthreads();
+    _t3 = gtimer();
+#endif
     // block-wide exclusive scan of cnt over digits (d = threadIdx.x); the tail
     // correction above only shrinks digit 255, the last, so starts are unaffected
     {
@@ -207,6 +229,19 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         vout[dest] = s_vals[i];
     }
     __syncthreads();   // smem reuse by the next partition of this CTA
+#ifdef SNP_SORT_INSTRUMENT
+    if (threadIdx.x == 0) {
+        unsigned long long *c = const_cast<unsigned long long *>(counters);
+        const unsigned long long t4 = gtimer();
+        atomicAdd(c + 28, _t1 - _t0);
+        atomicAdd(c + 29, _t2 - _t1);
+        atomicAdd(c + 30, _t3 - _t2);
+        atomicAdd(c + 31, t4 - _t3);
+        atomicMax(c + 17 + 3 * pass, t4);
+        atomicMax(c + 18 + 3 * pass, 1ull);
+        _t0 = t4;
+    }
+#endif
     }
 }
 
@@ -220,7 +255,7 @@ size_t sort_scratch_words(int passes, int64_t max_partitions) {
 
 cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
                             const unsigned long long *counters, int passes, SortScratch sc, bool hist_ready,
-                            cudaStream_t st, int *final_idx) {
+                            int64_t expected_n, cudaStream_t st, int *final_idx) {
     *final_idx = 0;
     if (capacity == 0 || passes == 0) return cudaSuccess;
     const int64_t maxp = (capacity + kPart - 1) / kPart;
@@ -245,12 +280,17 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
         if (hb > 148 * 4) hb = 148 * 4;
         k_hist<<<(unsigned)hb, kThreads, 0, st>>>(k0, capacity, counters, passes, sc.hist);
     }
-    const unsigned grid = (unsigned)(maxp < resident ? maxp : resident);
+    // persistent partitions: any grid size is correct; size it for the expected key
+    // count so that idle CTAs do not hold SM slots that concurrent work (K1b) could use
+    int64_t want = expected_n > 0 ? (expected_n + kPart - 1) / kPart : maxp;
+    if (want > maxp) want = maxp;
+    const unsigned grid = (unsigned)(want < resident ? want : resident);
     uint64_t *kin = k0, *kout = k1;
     uint32_t *vin = v0, *vout = v1;
     for (int p = 0; p < passes; ++p) {
-        k_pass<<<grid, kThreads, 0, st>>>(kin, vin, kout, vout, capacity, counters, p, sc.hist,
-                                          sc.lookback + (size_t)p * (size_t)maxp * 256, sc.tickets);
+        e = launch_hi(k_pass, dim3(grid), dim3(kThreads), 0, st, kin, vin, kout, vout, capacity, counters, p, sc.hist,
+                      sc.lookback + (size_t)p * (size_t)maxp * 256, sc.tickets);
+        if (e != cudaSuccess) return e;
         uint64_t *tk = kin; kin = kout; kout = tk;
         uint32_t *tv = vin; vin = vout; vout = tv;
     }

@@ -24,3 +24,5 @@ other = tot - sum(c[k] for k in names)
 print(cfg, "consumer-warp cycles:", parts, " other %.1f%%" % (100 * other / tot),
       " rounds=%d avg_lanes=%.1f total=%.3g" % (c[19], c[20] / max(c[19], 1), tot))
 print(cfg, "producer: waiting on free slots %.1f%% of its time" % (100 * c[26] / max(c[27], 1)))
+print(cfg, "touching (warp, record) pairs %.3g, with no candidate lane %.1f%%; emit calls (lane) %.3g, with empty list %.1f%%" % (
+    c[12], 100 * c[13] / max(c[12], 1), c[14], 100 * c[15] / max(c[14], 1)))
