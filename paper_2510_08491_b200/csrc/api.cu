@@ -361,6 +361,26 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     };
     SNP_CUDA(alloc_keys(s->key_capacity));
     b.capacity = s->key_capacity;
+    // K3 scratch: onesweep over the significant bits only; the digit histograms are
+    // accumulated by the duplication kernel itself (cleared by k_scan_partials); the
+    // look-back regions are cleared by the passes themselves (region 0 is clean on entry)
+    const int bits = kDepthBits + s->tile_bits + s->view_bits;
+    const int passes = (bits + 7) / 8;
+    auto ensure_sort_scratch = [&]() -> cudaError_t {
+        const int64_t maxp = (s->key_capacity + sort_partition_size() - 1) / sort_partition_size();
+        if (maxp <= s->sort_max_partitions && s->sort_scratch.p) return cudaSuccess;
+        cudaError_t e = s->sort_scratch.ensure(sort_scratch_words(8, maxp));
+        if (e != cudaSuccess) return e;
+        s->sort_max_partitions = maxp;
+        return cudaMemsetAsync(s->sort_scratch.p, 0, sizeof(uint32_t) * sort_scratch_words(8, maxp), st);
+    };
+    SNP_CUDA(ensure_sort_scratch());
+    const int64_t slots = (int64_t)s->n_views * s->tiles_x * s->tiles_y;
+    SNP_CUDA(s->ranges.ensure((size_t)slots * 2));
+    b.hist = s->sort_scratch.p;
+    b.passes = passes;
+    b.ranges = s->ranges.p;
+    b.n_slots = slots;
     SNP_CUDA(launch_count_scan(b, st));
     if (opts->sync_check) {
         SNP_CUDA(cudaMemcpyAsync(s->h_counters + kCntDup, s->counters.p + kCntDup, sizeof(unsigned long long),
@@ -373,28 +393,18 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
             SNP_CUDA(alloc_keys(s->key_capacity));
             // counters[kCntCapOverflow] was computed against the old capacity
             SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntCapOverflow, 0, sizeof(unsigned long long), st));
+            SNP_CUDA(ensure_sort_scratch());   // (a new scratch is cleared, histograms included)
         }
         b.capacity = s->key_capacity;
-    }
-    // K3 scratch: onesweep over the significant bits only; the digit histograms are
-    // accumulated by the duplication kernel itself
-    const int bits = kDepthBits + s->tile_bits + s->view_bits;
-    const int passes = (bits + 7) / 8;
-    const int64_t maxp = (s->key_capacity + sort_partition_size() - 1) / sort_partition_size();
-    if (maxp > s->sort_max_partitions || !s->sort_scratch.p) {
-        SNP_CUDA(s->sort_scratch.ensure(sort_scratch_words(8, maxp)));
-        s->sort_max_partitions = maxp;
     }
     SortScratch sc{};
     sc.hist = s->sort_scratch.p;
     sc.lookback = s->sort_scratch.p + 8 * 256;
     sc.tickets = s->sort_scratch.p + 8 * 256 + (size_t)8 * s->sort_max_partitions * 256;
     sc.max_partitions = s->sort_max_partitions;
-    SNP_CUDA(cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 256 * passes, st));
     b.keys = s->keys0.p;
     b.vals = s->vals0.p;
     b.hist = sc.hist;
-    b.passes = passes;
     SNP_CUDA(launch_dup_only(b, st));
     int final_idx = 0;
     SNP_CUDA(launch_onesweep(s->keys0.p, s->vals0.p, s->keys1.p, s->vals1.p, s->key_capacity, s->counters.p,
@@ -402,8 +412,6 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     s->sorted_idx = final_idx;
     const uint64_t *sk = final_idx ? s->keys1.p : s->keys0.p;
     // K4
-    const int64_t slots = (int64_t)s->n_views * s->tiles_x * s->tiles_y;
-    SNP_CUDA(s->ranges.ensure((size_t)slots * 2));
     SNP_CUDA(launch_tile_ranges(sk, s->counters.p, s->key_capacity, s->tile_bits, s->tiles_x * s->tiles_y,
                                 s->ranges.p, slots, st));
     // join K1b: everything after bin_sort on the caller's stream sees the records
@@ -439,8 +447,9 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
         s->fallback_capacity = fb_cap;
     }
     SNP_CUDA(s->fb_scratch.ensure((size_t)fallback_scratch_float4()));
-    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0, sizeof(unsigned long long) * 5, st));
-    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntFallbackQueue, 0, sizeof(unsigned long long), st));
+    // stats, fallback queue and tile queue: one memset (contiguous counters)
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
+                             sizeof(unsigned long long) * (kCntTileQueue - kCntTested + 1), st));
     RenderArgs a{};
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
@@ -468,7 +477,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     a.counters = s->counters.p;
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
-        for (const CamBatch &cb : s->cams) SNP_CUDA(launch_render(a, cb, st));
+        for (size_t k = 0; k < s->cams.size(); ++k) SNP_CUDA(launch_render(a, s->cams[k], k > 0, st));
         // (SNP_DEBUG bit 2 skips K6: timing experiments only, overflowed pixels stay unwritten)
         if (s->n > 0 && !(a.debug_flags & 2)) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
     }

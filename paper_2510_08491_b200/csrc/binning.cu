@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(kScanThreads) k_count_reduce(BinArgs a) {
     uint32_t tot;
     block_exclusive_scan(s, sw, tot);
     if (threadIdx.x == 0) a.partials[blockIdx.x] = tot;
+    // K4 writes only the non-empty tiles' ranges: clear all of them here
+    for (int64_t j = (int64_t)blockIdx.x * kScanThreads + threadIdx.x; j < 2 * a.n_slots;
+         j += (int64_t)gridDim.x * kScanThreads)
+        a.ranges[j] = 0u;
 }
 
 // Single block: exclusive scan of the block partials; total -> counters[kCntDup].
@@ -79,6 +83,8 @@ __global__ void __launch_bounds__(1024) k_scan_partials(BinArgs a, int64_t nbloc
     __shared__ unsigned long long carry;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) carry = 0;
+    // the duplication kernel accumulates the digit histograms: clear them here
+    for (int i = threadIdx.x; i < a.passes * 256; i += 1024) a.hist[i] = 0u;
     __syncthreads();
     for (int64_t b0 = 0; b0 < nblocks; b0 += 1024) {
         int64_t b = b0 + threadIdx.x;
@@ -213,7 +219,10 @@ cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st) {
     if (nb == 0) {
         cudaError_t e = cudaMemsetAsync(a.counters + kCntDup, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
-        return cudaMemsetAsync(a.counters + kCntCapOverflow, 0, sizeof(unsigned long long), st);
+        e = cudaMemsetAsync(a.counters + kCntCapOverflow, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        if (a.n_slots > 0) e = cudaMemsetAsync(a.ranges, 0, sizeof(uint32_t) * 2 * (size_t)a.n_slots, st);
+        return e;
     }
     cudaError_t e0 = launch_hi(k_count_reduce, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a);
     if (e0 != cudaSuccess) return e0;
@@ -233,8 +242,8 @@ cudaError_t launch_dup_only(const BinArgs &a, cudaStream_t st) {
 cudaError_t launch_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
                                int32_t tile_bits, int32_t tiles, uint32_t *ranges, int64_t n_slots,
                                cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(ranges, 0, sizeof(uint32_t) * 2 * (size_t)n_slots, st);
-    if (e != cudaSuccess) return e;
+    (void)n_slots;   // cleared by k_count_reduce
+    cudaError_t e = cudaSuccess;
     if (capacity == 0) return cudaSuccess;
     int64_t blocks = (capacity + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
 
 int64_t fallback_scratch_float4() { return 1; }   // K6 keeps its hits in shared memory
 
-cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_t st) {
+cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st) {
     static bool attr_set = false;
     const int smem = (int)sizeof(Smem);
     if (!attr_set) {
@@ -913,8 +913,10 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_
     }
     const int tiles = a.tiles_x * a.stripe_rows * cams.nv;
     if (tiles == 0) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(a.counters + kCntTileQueue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
+    if (reset_queue) {
+        cudaError_t e = cudaMemsetAsync(a.counters + kCntTileQueue, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+    }
     static int resident = 0;   // persistent grid: every CTA that fits, all SMs
     if (!resident) {
         int dev = 0, sms = 0, per_sm = 0;

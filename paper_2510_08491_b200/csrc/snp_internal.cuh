@@ -76,8 +76,9 @@ enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecW
                   kRecWh1 = 5, kRecUnits = 6, kRecW2 = 14 };
 
 // Device-side counters (one 64-bit slot each), see snp_stats.
-enum Counter { kCntVisible = 0, kCntDup = 1, kCntTested = 2, kCntCandidate = 3, kCntHit = 4,
-               kCntComposited = 5, kCntOverflow = 6, kCntCapOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
+// The render counters kCntTested..kCntTileQueue are contiguous: one memset per render.
+enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
+               kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
                kNumCounters = 32 };   // 16..31: SNP_INSTRUMENT builds only
 
 struct ProjectArgs {
@@ -111,8 +112,11 @@ struct BinArgs {
     int64_t capacity;
     uint32_t *partials;     // scan scratch [num_blocks + 1]
     unsigned long long *counters;
-    uint32_t *hist;         // [passes][256] digit histograms accumulated during duplication (zeroed)
+    uint32_t *hist;         // [passes][256] digit histograms accumulated during duplication
+                            // (zeroed by k_scan_partials)
     int32_t passes;
+    uint32_t *ranges;       // [n_slots][2] tile ranges, zeroed by k_count_reduce (filled by K4)
+    int64_t n_slots;
 };
 int64_t bin_scan_blocks(int64_t items);
 cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st);   // counts + scan -> counters[kCntDup]
@@ -123,7 +127,8 @@ cudaError_t launch_tile_ranges(const uint64_t *keys, const unsigned long long *c
 
 struct SortScratch {
     uint32_t *hist;         // [passes][256]
-    uint32_t *lookback;     // [passes][max_partitions][256]
+    uint32_t *lookback;     // [8][max_partitions][256]; region 0 is zero on entry, pass p
+                            // zeroes region (p+1) % passes (region 0 again after the last pass)
     uint32_t *tickets;      // [passes]
     int64_t max_partitions;
 };
@@ -159,7 +164,9 @@ struct RenderArgs {
     unsigned long long *counters;
 };
 int64_t fallback_scratch_float4();
-cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, cudaStream_t st);
+// reset_queue: zero the tile queue first (needed for every camera batch after the
+// first; the caller zeroes all render counters once per snp_render)
+cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st);
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
 
 }  // namespace snp

@@ -62,7 +62,8 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
 __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                    uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
                                                    int64_t capacity, const unsigned long long *counters, int pass,
-                                                   const uint32_t *hist, uint32_t *lookback, uint32_t *tickets) {
+                                                   const uint32_t *hist, uint32_t *lookback, uint32_t *zero_next,
+                                                   int64_t zero_words) {
     __shared__ uint64_t s_keys[kPart];
     __shared__ uint32_t s_vals[kPart];
     __shared__ uint32_t s_wh[kWarps][256];     // per-warp digit counts -> per-warp exclusive offsets
@@ -73,6 +74,9 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int shift = 8 * pass;
+    // clear the look-back region of the next pass (no memset node between passes)
+    for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < zero_words; j += (int64_t)gridDim.x * kThreads)
+        zero_next[j] = 0u;
     const int64_t n = sort_n(counters, capacity);
     const int64_t nparts = (n + kPart - 1) / kPart;
     // Persistent: CTA c takes partitions c, c + G, ... in increasing order; the grid
@@ -273,8 +277,6 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
         e = cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 256 * passes, st);
         if (e != cudaSuccess) return e;
     }
-    e = cudaMemsetAsync(sc.lookback, 0, sizeof(uint32_t) * 256 * (size_t)maxp * passes, st);
-    if (e != cudaSuccess) return e;
     if (!hist_ready) {
         int64_t hb = (capacity + kThreads * 16 - 1) / (kThreads * 16);
         if (hb > 148 * 4) hb = 148 * 4;
@@ -285,11 +287,13 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
     int64_t want = expected_n > 0 ? (expected_n + kPart - 1) / kPart : maxp;
     if (want > maxp) want = maxp;
     const unsigned grid = (unsigned)(want < resident ? want : resident);
+    const size_t region = (size_t)sc.max_partitions * 256;   // look-back words per pass (fixed layout)
     uint64_t *kin = k0, *kout = k1;
     uint32_t *vin = v0, *vout = v1;
     for (int p = 0; p < passes; ++p) {
         e = launch_hi(k_pass, dim3(grid), dim3(kThreads), 0, st, kin, vin, kout, vout, capacity, counters, p, sc.hist,
-                      sc.lookback + (size_t)p * (size_t)maxp * 256, sc.tickets);
+                      sc.lookback + (size_t)p * region, sc.lookback + (size_t)((p + 1) % passes) * region,
+                      (int64_t)region);
         if (e != cudaSuccess) return e;
         uint64_t *tk = kin; kin = kout; kout = tk;
         uint32_t *tv = vin; vin = vout; vout = tv;
