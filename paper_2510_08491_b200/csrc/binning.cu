@@ -61,6 +61,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_count_reduce(BinArgs a) {
+    pdl_prologue();
     __shared__ uint32_t sw[32];
     const int64_t total_items = a.n * a.n_views;
     const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(kScanThreads) k_count_reduce(BinArgs a) {
 
 // Single block: exclusive scan of the block partials; total -> counters[kCntDup].
 __global__ void __launch_bounds__(1024) k_scan_partials(BinArgs a, int64_t nblocks) {
+    pdl_prologue();
     __shared__ uint32_t sw[32];
     __shared__ unsigned long long carry;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(1024) k_scan_partials(BinArgs a, int64_t nbloc
 // at a time (coalesced 8-byte key + 4-byte value stores), each lane finding its
 // key's item by binary search over the warp's item offsets in shared memory.
 __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
+    pdl_prologue();
     __shared__ uint32_t sw[32];
     __shared__ uint32_t s_off[kScanTile + 8];   // per item exclusive offset (block-relative)
     __shared__ uint32_t s_hist[8][256];         // digit histograms of the keys this block emits
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
 
 __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
                               int32_t tile_bits, int32_t tiles, uint32_t *ranges) {
+    pdl_prologue();
     int64_t n = (int64_t)counters[kCntDup];
     if (n > capacity) n = capacity;
     const uint64_t tmask = (1ull << tile_bits) - 1ull;

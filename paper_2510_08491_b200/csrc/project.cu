@@ -35,8 +35,16 @@ __device__ __forceinline__ bool quat_rot(const float *q4, double R[9]) {
 }
 
 // Real SH basis, degrees 0..3 (Condon-Shortley phase, m = -l..l; 3DGS convention).
-__device__ __forceinline__ void sh_rgb(int degree, const float *sh, double xd, double yd, double zd,
+__device__ __forceinline__ void sh_rgb(int degree, const float4 *sh4, double xd, double yd, double zd,
                                        float rgb[3]) {
+    // float4 reads: a 192-byte row stride gives 4-way shared-memory bank conflicts
+    // instead of the 16-way of scalar reads
+    float sh[48];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const float4 t = sh4[k];
+        sh[4 * k] = t.x; sh[4 * k + 1] = t.y; sh[4 * k + 2] = t.z; sh[4 * k + 3] = t.w;
+    }
     // fp32 is ample here: colour enters the pixel linearly (error ~1e-7)
     const float x = (float)xd, y = (float)yd, z = (float)zd;
     float Y[16];
@@ -348,7 +356,7 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
                 const double ind = 1.0 / nd;
                 x = mw0 * ind; y = mw1 * ind; z = mw2 * ind;
             }
-            sh_rgb(a.sh_degree, ps.sh + 48 * li, x, y, z, rgb);
+            sh_rgb(a.sh_degree, reinterpret_cast<const float4 *>(ps.sh + 48 * li), x, y, z, rgb);
         }
         // whitening Wh = diag(1/s) R^T (world -> unit-sphere frame); fp32 suffices
         float Wh[9];

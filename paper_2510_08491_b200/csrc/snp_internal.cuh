@@ -12,7 +12,16 @@ namespace snp {
 // Launch with the device's greatest scheduling priority.  Used for the K2-K4 chain
 // (latency-bound, on the frame's critical path) so that its CTAs take SM slots
 // ahead of the concurrently running K1b (side stream, default priority).
+// The launch is also a programmatic dependent launch: the kernel may be scheduled
+// while its predecessor in the stream still runs, so every kernel launched this way
+// starts with pdl_prologue() before touching global memory.
 int greatest_priority();
+__device__ __forceinline__ void pdl_prologue() {
+    // wait for the predecessor grid (complete, memory visible), then let the next
+    // grid in the stream be scheduled (it waits in its own prologue)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_hi(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                       Args &&...args) {
@@ -21,11 +30,13 @@ cudaError_t launch_hi(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributePriority;
     at[0].val.priority = greatest_priority();
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
                                                    int64_t capacity, const unsigned long long *counters, int pass,
                                                    const uint32_t *hist, uint32_t *lookback, uint32_t *zero_next,
                                                    int64_t zero_words) {
+    pdl_prologue();
     __shared__ uint64_t s_keys[kPart];
     __shared__ uint32_t s_vals[kPart];
     __shared__ uint32_t s_wh[kWarps][256];     // per-warp digit counts -> per-warp exclusive offsets
