@@ -38,7 +38,8 @@ constexpr int kThreads = (kConsumers + 1) * 32;    // + 1 producer warp
 constexpr int kWarps = kConsumers;
 constexpr int kBatch = 32;          // records per stage (one per producer lane)
 constexpr int kStages = 5;          // TMA ring depth
-constexpr int kPend = 16;           // per-pixel pending hits (unsorted)
+constexpr int kPend = 16;           // per-pixel pending hits (sorted ring)
+static_assert((kPend & (kPend - 1)) == 0, "the pending ring needs a power of two");
 constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
 
 struct __align__(16) Smem {
@@ -56,12 +57,14 @@ struct __align__(16) Smem {
     int32_t next_tile;
     uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs:
     uint8_t ql[kWarps][64];                   //   (record slot j, owner lane)
-    float p_thi[kPend][kWarps * 32];          // pending hits, unsorted, one column per pixel: t_in
+    float p_thi[kPend][kWarps * 32];          // pending hits, one column per pixel, kept sorted by
+                                              // (t_in, id) in a ring starting at p_head: t_in
                                               // (fp32: its 6e-8 rounding is far below the 1e-6
                                               // near-tie flag of R23), kappa, primitive id
     float p_kap[kPend][kWarps * 32];
     uint32_t p_id[kPend][kWarps * 32];
-    int32_t p_n[kWarps * 32];                 // pending count (appended to by any lane of the warp)
+    int32_t p_n[kWarps * 32];                 // pending count (inserted into by any lane of the warp)
+    int32_t p_head[kWarps * 32];              // ring slot of the smallest pending hit
     int32_t p_ovf[kWarps * 32];               // a hit was dropped: pixel goes to K6
 };
 
@@ -213,23 +216,18 @@ struct PixelState {
 };
 
 // Blend, front to back, every pending hit of this thread's pixel with t_in < L
-// (strictly): every hit not yet appended has t_in >= L (R19), so these are
-// exactly the next hits of the ray in (t_in, id) order (Eq. 4).
+// (strictly): every hit not yet inserted has t_in >= L (R19), so these are
+// exactly the next hits of the ray in (t_in, id) order (Eq. 4).  The
+// list is sorted, so they are popped from its head.
 __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_floor, const float4 *recs) {
     const int tid = threadIdx.x;
     int n = sm.p_n[tid];
+    int h = sm.p_head[tid];
     while (n > 0) {
-        int kmin = 0;
-        float mh = sm.p_thi[0][tid];
-        uint32_t mid = sm.p_id[0][tid];
-        for (int k = 1; k < n; ++k) {
-            const float h = sm.p_thi[k][tid];
-            const uint32_t id = sm.p_id[k][tid];
-            if (h < mh || (h == mh && id < mid)) { mh = h; mid = id; kmin = k; }
-        }
-        if (!(mh < L)) break;
-        const float kap = sm.p_kap[kmin][tid];
-        const float4 rgb = __ldg(recs + (size_t)mid * 16 + kRecConicRgb);
+        const float t = sm.p_thi[h][tid];
+        if (!(t < L)) break;
+        const float kap = sm.p_kap[h][tid];
+        const float4 rgb = __ldg(recs + (size_t)sm.p_id[h][tid] * 16 + kRecConicRgb);
         const float w = ps.T * kap;
         ps.cr = fmaf(w, rgb.y, ps.cr);
         ps.cg = fmaf(w, rgb.z, ps.cg);
@@ -237,17 +235,14 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_
         ps.T *= (1.0f - kap);
         ++ps.composited;
         --n;
-        if (kmin != n) {
-            sm.p_thi[kmin][tid] = sm.p_thi[n][tid];
-            sm.p_kap[kmin][tid] = sm.p_kap[n][tid];
-            sm.p_id[kmin][tid] = sm.p_id[n][tid];
-        }
+        h = (h + 1) & (kPend - 1);
         if (ps.T < t_floor) {
             ps.done = true;
             break;
         }
     }
     sm.p_n[tid] = n;
+    sm.p_head[tid] = h;
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
@@ -435,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             by0 = (float)by + 0.5f;
             ps = PixelState{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
             sm.p_n[tid] = 0;
+            sm.p_head[tid] = 0;
             sm.p_ovf[tid] = 0;
             tile_finished = false;
         }
@@ -491,29 +487,42 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 float th = 0.f, tl = 0.f, kap = 0.f;
                 if (valid) hit = exact_hit(&sm.rec[slot][j][0], ro, th, tl, kap);
                 n_hit += hit;
-                // append each hit to its owner's pending list (in queue == record order)
+                // insert each hit into its owner's sorted pending ring; the hits of one
+                // owner in this round go in one at a time (peer rank order).  Records
+                // stream in L order, so a new hit usually lands at the tail (one compare).
                 const uint32_t peers = __match_any_sync(0xffffffffu, hit ? owner : 64 + lane);
                 const int ot = wid * 32 + owner;
-                int base = 0;
-                if (hit) {
-                    base = sm.p_n[ot];
-                    const int k = base + __popc(peers & lt_mask);
-                    if (k < plimit) {
-                        sm.p_thi[k][ot] = th;
-                        sm.p_kap[k][ot] = kap;
-                        sm.p_id[k][ot] = sm.id[slot][j];
+                const int rank = __popc(peers & lt_mask);
+                const int steps = __reduce_max_sync(0xffffffffu, hit ? (uint32_t)rank + 1u : 0u);
+                const uint32_t idn = hit ? sm.id[slot][j] : 0u;
+                for (int r = 0; r < steps; ++r) {
+                    if (hit && rank == r) {
+                        const int n = sm.p_n[ot];
+                        if (n >= plimit) {
+                            sm.p_ovf[ot] = 1;   // dropped: the pixel goes to K6
+                        } else {
+                            const int hd = sm.p_head[ot];
+                            int k = n;
+                            while (k > 0) {
+                                const int sp = (hd + k - 1) & (kPend - 1);
+                                const float tp = sm.p_thi[sp][ot];
+                                const uint32_t ip = sm.p_id[sp][ot];
+                                if (!(th < tp || (th == tp && idn < ip))) break;
+                                const int sd = (hd + k) & (kPend - 1);
+                                sm.p_thi[sd][ot] = tp;
+                                sm.p_kap[sd][ot] = sm.p_kap[sp][ot];
+                                sm.p_id[sd][ot] = ip;
+                                --k;
+                            }
+                            const int sd = (hd + k) & (kPend - 1);
+                            sm.p_thi[sd][ot] = th;
+                            sm.p_kap[sd][ot] = kap;
+                            sm.p_id[sd][ot] = idn;
+                            sm.p_n[ot] = n + 1;
+                        }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
-                if (hit && lane == __ffs(peers) - 1) {
-                    int nn = base + __popc(peers);
-                    if (nn > plimit) {
-                        sm.p_ovf[ot] = 1;
-                        nn = plimit;
-                    }
-                    sm.p_n[ot] = nn;
-                }
-                __syncwarp();
 #ifdef SNP_INSTRUMENT
                 ins_round += clock64() - _r0;
 #endif

@@ -9,12 +9,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--views", type=int, default=0)
+ap.add_argument("--plimit", type=int, default=0)
 args = ap.parse_args()
 scene, cams, bg = synth.make_config(args.config, views=args.views or None)
 ns = types.SimpleNamespace(omega=scene.omega, sh_degree=scene.sh_degree)
 for f in snp.FIELDS:
     setattr(ns, f, torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).cuda())
 h = snp.create_scene(ns, 0)
+if args.plimit:
+    snp.set_pending_limit(h, args.plimit)
 out = torch.empty((len(cams), cams[0].height, cams[0].width, 4), device="cuda")
 snp.render_views(h, cams, snp.make_opts(bg, sync_check=1), out)
 opts = snp.make_opts(bg, sync_check=0)
