@@ -58,13 +58,13 @@ struct __align__(16) Smem {
     uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs:
     uint8_t ql[kWarps][64];                   //   (record slot j, owner lane)
     float p_thi[kPend][kWarps * 32];          // pending hits, one column per pixel, kept sorted by
-                                              // (t_in, id) in a ring starting at p_head: t_in
+                                              // (t_in, id) in a ring starting at the head: t_in
                                               // (fp32: its 6e-8 rounding is far below the 1e-6
                                               // near-tie flag of R23), kappa, primitive id
     float p_kap[kPend][kWarps * 32];
     uint32_t p_id[kPend][kWarps * 32];
-    int32_t p_n[kWarps * 32];                 // pending count (inserted into by any lane of the warp)
-    int32_t p_head[kWarps * 32];              // ring slot of the smallest pending hit
+    int32_t p_nh[kWarps * 32];                // pending count | ring slot of the smallest pending
+                                              // hit << 16 (one load for the inserting lanes)
     int32_t p_ovf[kWarps * 32];               // a hit was dropped: pixel goes to K6
 };
 
@@ -221,8 +221,9 @@ struct PixelState {
 // list is sorted, so they are popped from its head.
 __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_floor, const float4 *recs) {
     const int tid = threadIdx.x;
-    int n = sm.p_n[tid];
-    int h = sm.p_head[tid];
+    const int nh = sm.p_nh[tid];
+    int n = nh & 0xffff;
+    int h = nh >> 16;
     while (n > 0) {
         const float t = sm.p_thi[h][tid];
         if (!(t < L)) break;
@@ -241,8 +242,7 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_
             break;
         }
     }
-    sm.p_n[tid] = n;
-    sm.p_head[tid] = h;
+    sm.p_nh[tid] = n | (h << 16);
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
@@ -429,8 +429,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             bx0 = (float)bx + 0.5f;
             by0 = (float)by + 0.5f;
             ps = PixelState{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
-            sm.p_n[tid] = 0;
-            sm.p_head[tid] = 0;
+            sm.p_nh[tid] = 0;
             sm.p_ovf[tid] = 0;
             tile_finished = false;
         }
@@ -497,11 +496,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 const uint32_t idn = hit ? sm.id[slot][j] : 0u;
                 for (int r = 0; r < steps; ++r) {
                     if (hit && rank == r) {
-                        const int n = sm.p_n[ot];
+                        const int nh = sm.p_nh[ot];
+                        const int n = nh & 0xffff;
                         if (n >= plimit) {
                             sm.p_ovf[ot] = 1;   // dropped: the pixel goes to K6
                         } else {
-                            const int hd = sm.p_head[ot];
+                            const int hd = nh >> 16;
                             int k = n;
                             while (k > 0) {
                                 const int sp = (hd + k - 1) & (kPend - 1);
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                             sm.p_thi[sd][ot] = th;
                             sm.p_kap[sd][ot] = kap;
                             sm.p_id[sd][ot] = idn;
-                            sm.p_n[ot] = n + 1;
+                            sm.p_nh[ot] = nh + 1;
                         }
                     }
                     __syncwarp();
@@ -587,11 +587,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 }
                 // batch end: everything in later batches has t_in >= L of the next key;
                 // mid-batch: only when the pending list runs full
-                if (!ps.done && (batch_end || sm.p_n[tid] > plimit - 4)) {
+                if (!ps.done && (batch_end || (sm.p_nh[tid] & 0xffff) > plimit - 4)) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
                     ++ins_ecalls;
-                    ins_enone += (sm.p_n[tid] == 0);
+                    ins_enone += ((sm.p_nh[tid] & 0xffff) == 0);
 #endif
                     emit(sm, ps, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
                          a.t_floor, recs);
