@@ -270,11 +270,18 @@ __device__ __forceinline__ void issue_slice(const ProjectArgs &a, Slice &dst, un
 }
 
 
-__device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch &cb, const Slice &ps, int li,
+// One primitive's parameters, wherever they live (shared-memory slice or global).
+struct PrimParams {
+    const float *center, *scale;
+    const float4 *rot, *sh, *w1, *b1, *w2;
+    float b2;
+};
+
+__device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch &cb, const PrimParams &pp,
                                            int64_t i, uint32_t vis_mask) {
-    const float mu0 = ps.centers[3 * li], mu1 = ps.centers[3 * li + 1], mu2 = ps.centers[3 * li + 2];
-    const float s0f = ps.scales[3 * li], s1f = ps.scales[3 * li + 1], s2f = ps.scales[3 * li + 2];
-    const float4 qv = reinterpret_cast<const float4 *>(ps.rot)[li];
+    const float mu0 = pp.center[0], mu1 = pp.center[1], mu2 = pp.center[2];
+    const float s0f = pp.scale[0], s1f = pp.scale[1], s2f = pp.scale[2];
+    const float4 qv = pp.rot[0];
     const float q4[4] = {qv.x, qv.y, qv.z, qv.w};
     for (int vloc = 0; vloc < cb.nv; ++vloc) {
         if (!((vis_mask >> vloc) & 1u)) continue;
@@ -356,7 +363,7 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
                 const double ind = 1.0 / nd;
                 x = mw0 * ind; y = mw1 * ind; z = mw2 * ind;
             }
-            sh_rgb(a.sh_degree, reinterpret_cast<const float4 *>(ps.sh + 48 * li), x, y, z, rgb);
+            sh_rgb(a.sh_degree, pp.sh, x, y, z, rgb);
         }
         // whitening Wh = diag(1/s) R^T (world -> unit-sphere frame); fp32 suffices
         float Wh[9];
@@ -368,7 +375,7 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
                 for (int j = 0; j < 3; ++j) Wh[3 * k + j] = (float)R[3 * j + k] * is[k];
         }
         float4 *rec = a.records + o * 16;
-        const float b2 = ps.b2[li];
+        const float b2 = pp.b2;
         rec[kRecConic] = make_float4(cx0, cy0, ca, cb2);
         rec[kRecConicRgb] = make_float4(cc, rgb[0], rgb[1], rgb[2]);
         rec[kRecMh] = make_float4(mh0, mh1, mh2, b2);
@@ -377,9 +384,9 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
         rec[kRecWh1] = make_float4(Wh[5], Wh[6], Wh[7], Wh[8]);
         // MLP (Eq. 6) with the Eq. 5 normalisation folded in: W1' = omega W1 / ||s||_inf
         const double om = (double)a.omega;
-        const float4 *w1v = reinterpret_cast<const float4 *>(ps.w1 + 24 * li);
-        const float4 *b1v = reinterpret_cast<const float4 *>(ps.b1 + 8 * li);
-        const float4 *w2v = reinterpret_cast<const float4 *>(ps.w2 + 8 * li);
+        const float4 *w1v = pp.w1;
+        const float4 *b1v = pp.b1;
+        const float4 *w2v = pp.w2;
         float w1[24], b1[8];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
@@ -421,8 +428,22 @@ __global__ void __launch_bounds__(kProjThreads, 4) k_records(ProjectArgs a, CamB
             : "=r"(ok)
             : "r"(psmem_u32(&ps.bar))
             : "memory");
-    if (vis) record_one(a, cb, ps.buf, threadIdx.x, i0 + threadIdx.x, vis);
+    if (vis) {
+        const int li = threadIdx.x;
+        const Slice &sl = ps.buf;
+        PrimParams pp;
+        pp.center = sl.centers + 3 * li;
+        pp.scale = sl.scales + 3 * li;
+        pp.rot = reinterpret_cast<const float4 *>(sl.rot) + li;
+        pp.sh = reinterpret_cast<const float4 *>(sl.sh + 48 * li);
+        pp.w1 = reinterpret_cast<const float4 *>(sl.w1 + 24 * li);
+        pp.b1 = reinterpret_cast<const float4 *>(sl.b1 + 8 * li);
+        pp.w2 = reinterpret_cast<const float4 *>(sl.w2 + 8 * li);
+        pp.b2 = sl.b2[li];
+        record_one(a, cb, pp, i0 + li, vis);
+    }
 }
+
 
 // Input validation: q nonzero, s > 0, every value finite.
 // bad[0] |= 1 non-finite, 2 zero quaternion, 4 scale <= 0; bad[1] = min bad index.
