@@ -38,12 +38,17 @@ constexpr int kThreads = (kConsumers + 1) * 32;    // + 1 producer warp
 constexpr int kWarps = kConsumers;
 constexpr int kBatch = 32;          // records per stage (one per producer lane)
 constexpr int kStages = 5;          // TMA ring depth
+constexpr int kRecStride = 17;      // float4 per staged record (16 + 1 pad)
 constexpr int kPend = 16;           // per-pixel pending hits (sorted ring)
 static_assert((kPend & (kPend - 1)) == 0, "the pending ring needs a power of two");
+constexpr int kCountMask = 0xff;    // p_nh: pending count (bits 0-7), overflow flag (bit 8), head (16+)
+constexpr int kOvf = 0x100;
 constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
 
 struct __align__(16) Smem {
-    float4 rec[kStages][kBatch][16];          // 32 KB of records, cp.async.bulk-staged
+    float4 rec[kStages][kBatch][kRecStride];  // records, cp.async.bulk-staged, padded to 17 float4 so
+                                              // that 8 distinct records read by one warp hit 8
+                                              // distinct 16-byte bank groups
     float L[kStages][kBatch + 1];             // depth lower bounds (+ the next batch's first)
     uint32_t id[kStages][kBatch];
     // slot metadata written by the producer before its arrive (release)
@@ -63,9 +68,8 @@ struct __align__(16) Smem {
                                               // near-tie flag of R23), kappa, primitive id
     float p_kap[kPend][kWarps * 32];
     uint32_t p_id[kPend][kWarps * 32];
-    int32_t p_nh[kWarps * 32];                // pending count | ring slot of the smallest pending
+    int32_t p_nh[kWarps * 32];                // pending count | kOvf | ring slot of the smallest pending
                                               // hit << 16 (one load for the inserting lanes)
-    int32_t p_ovf[kWarps * 32];               // a hit was dropped: pixel goes to K6
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -222,7 +226,7 @@ struct PixelState {
 __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_floor, const float4 *recs) {
     const int tid = threadIdx.x;
     const int nh = sm.p_nh[tid];
-    int n = nh & 0xffff;
+    int n = nh & kCountMask;
     int h = nh >> 16;
     while (n > 0) {
         const float t = sm.p_thi[h][tid];
@@ -242,7 +246,7 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_
             break;
         }
     }
-    sm.p_nh[tid] = n | (h << 16);
+    sm.p_nh[tid] = n | (nh & kOvf) | (h << 16);
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     // =============================== consumer warps
 #ifdef SNP_INSTRUMENT
     long long ins_wait = 0, ins_round = 0, ins_emit = 0, ins_rounds = 0, ins_lanes = 0, ins_fill = 0, ins_pre = 0,
-              ins_setup = 0, ins_finish = 0, ins_touch = 0, ins_empty = 0, ins_ecalls = 0, ins_enone = 0;
+              ins_setup = 0, ins_finish = 0, ins_touch = 0, ins_empty = 0, ins_ecalls = 0, ins_enone = 0, ins_steps = 0;
     const long long ins_start = clock64();
 #endif
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
@@ -430,7 +434,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             by0 = (float)by + 0.5f;
             ps = PixelState{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
             sm.p_nh[tid] = 0;
-            sm.p_ovf[tid] = 0;
             tile_finished = false;
         }
 #ifdef SNP_INSTRUMENT
@@ -494,12 +497,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 const int rank = __popc(peers & lt_mask);
                 const int steps = __reduce_max_sync(0xffffffffu, hit ? (uint32_t)rank + 1u : 0u);
                 const uint32_t idn = hit ? sm.id[slot][j] : 0u;
+#ifdef SNP_INSTRUMENT
+                ins_steps += steps;
+#endif
                 for (int r = 0; r < steps; ++r) {
                     if (hit && rank == r) {
                         const int nh = sm.p_nh[ot];
-                        const int n = nh & 0xffff;
+                        const int n = nh & kCountMask;
                         if (n >= plimit) {
-                            sm.p_ovf[ot] = 1;   // dropped: the pixel goes to K6
+                            sm.p_nh[ot] = nh | kOvf;   // dropped: the pixel goes to K6
                         } else {
                             const int hd = nh >> 16;
                             int k = n;
@@ -581,17 +587,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     qcount = rem;
                 }
                 const bool batch_end = (m == 0u) && rem == 0;
-                if (!ps.done && sm.p_ovf[tid]) {   // a hit was dropped: nothing may be blended
+                if (!ps.done && (sm.p_nh[tid] & kOvf)) {   // a hit was dropped: nothing may be blended
                     ps.overflow = true;
                     ps.done = true;
                 }
                 // batch end: everything in later batches has t_in >= L of the next key;
                 // mid-batch: only when the pending list runs full
-                if (!ps.done && (batch_end || (sm.p_nh[tid] & 0xffff) > plimit - 4)) {
+                if (!ps.done && (batch_end || (sm.p_nh[tid] & kCountMask) > plimit - 4)) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
                     ++ins_ecalls;
-                    ins_enone += ((sm.p_nh[tid] & 0xffff) == 0);
+                    ins_enone += ((sm.p_nh[tid] & kCountMask) == 0);
 #endif
                     emit(sm, ps, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
                          a.t_floor, recs);
@@ -626,6 +632,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         atomicAdd(a.counters + 25, (unsigned long long)ins_finish);
         atomicAdd(a.counters + 12, (unsigned long long)ins_touch);
         atomicAdd(a.counters + 13, (unsigned long long)ins_empty);
+        atomicAdd(a.counters + 10, (unsigned long long)ins_steps);
     }
     {
         const unsigned long long ec = __reduce_add_sync(0xffffffffu, (uint32_t)ins_ecalls);

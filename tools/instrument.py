@@ -26,3 +26,4 @@ print(cfg, "consumer-warp cycles:", parts, " other %.1f%%" % (100 * other / tot)
 print(cfg, "producer: waiting on free slots %.1f%% of its time" % (100 * c[26] / max(c[27], 1)))
 print(cfg, "touching (warp, record) pairs %.3g, with no candidate lane %.1f%%; emit calls (lane) %.3g, with empty list %.1f%%" % (
     c[12], 100 * c[13] / max(c[12], 1), c[14], 100 * c[15] / max(c[14], 1)))
+print(cfg, "insertion steps per round %.2f" % (c[10] / max(c[19], 1)))
