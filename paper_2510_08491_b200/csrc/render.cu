@@ -37,7 +37,7 @@ constexpr int kConsumers = 8;                      // consumer warps = 8x4 pixel
 constexpr int kThreads = (kConsumers + 1) * 32;    // + 1 producer warp
 constexpr int kWarps = kConsumers;
 constexpr int kBatch = 32;          // records per stage (one per producer lane)
-constexpr int kStages = 5;          // TMA ring depth
+constexpr int kStages = 7;          // TMA ring depth (2 CTAs x ~113 KB per SM)
 constexpr int kRecStride = 17;      // float4 per staged record (16 + 1 pad)
 constexpr int kPend = 16;           // per-pixel pending hits (sorted ring)
 static_assert((kPend & (kPend - 1)) == 0, "the pending ring needs a power of two");
