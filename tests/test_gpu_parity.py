@@ -199,3 +199,57 @@ def test_validation_errors_and_update_scene():
     with pytest.raises(snp.SnpError):
         snp.update_scene(h, synth.make_scene(1, 10))   # n differs
     snp.destroy(h)
+
+
+@pytest.mark.gpu
+def test_stream_ordering_and_graph_capture():
+    """K1b runs on the scene's side stream (forked after K1a, joined at the end of
+    snp_bin_sort): project twice before binning, render twice after one binning,
+    update the scene right after projecting, and replay the whole frame as a CUDA
+    graph captured on a user stream -- every result bit-identical to a plain frame."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene, cams, bg = synth.make_config("C2", n=3000)
+    V, H, W = len(cams), cams[0].height, cams[0].width
+    ref = gpu_render(scene, cams, bg)["img"]
+    cc = snp.make_cameras(cams)
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        first = snp.make_opts(bg, sync_check=1)
+        opts = snp.make_opts(bg, sync_check=0)
+        out = torch.full((V, H, W, 4), float("nan"), device="cuda")
+        other = synth.orbit_cameras(1, 3.0, W, H, 60.0)
+        snp.project(h, snp.make_cameras(other))     # pending K1b, never binned
+        snp.project(h, cc)                          # must wait for it
+        snp.bin_sort(h, first)
+        snp.render(h, opts, out)
+        snp.render(h, opts, out)                    # second render of the same binning
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref)
+        # update right after a projection (K1b still reading the old parameters)
+        scene2, _, _ = synth.make_config("C2", n=3000)
+        scene2.b2[:] = scene2.b2 * 0.5
+        ref2 = gpu_render(scene2, cams, bg)["img"]
+        snp.project(h, cc)
+        snp.update_scene(h, torch_scene(scene2))
+        snp.render_views(h, cams, first, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref2)
+        # whole frame captured on a user stream, replayed
+        st = torch.cuda.Stream()
+        out.fill_(float("nan"))
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            snp.project(h, cc, st)
+            snp.bin_sort(h, opts, st)
+            snp.render(h, opts, out, st)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref2)
+        s = snp.get_stats(h)
+        assert s["composited"] > 0 and s["capacity_overflow"] == 0
+    finally:
+        snp.destroy(h)
