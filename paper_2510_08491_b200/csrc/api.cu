@@ -77,7 +77,7 @@ struct snp_scene_s {
     DevBuf<uint32_t> vals0, vals1;
     int64_t key_capacity = 0;
     int64_t known_ndup = 0;    // key count seen by the last sync_check (sizes the sort grid only)
-    DevBuf<uint32_t> partials;
+    DevBuf<unsigned long long> dup_status;   // K2 block look-back states + ticket (zero between frames)
     DevBuf<uint32_t> sort_scratch;
     int64_t sort_max_partitions = 0;
     int sorted_idx = 0;
@@ -334,7 +334,11 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     s->row_stride = opts->tile_row_stride;
     s->stripe_rows = s->row_begin < s->tiles_y ? (s->tiles_y - 1 - s->row_begin) / s->row_stride + 1 : 0;
     const int64_t items = (int64_t)s->n_views * s->n;
-    SNP_CUDA(s->partials.ensure((size_t)bin_scan_blocks(items) + 1));
+    const int64_t nblk = bin_scan_blocks(items);
+    if (!s->dup_status.p || s->dup_status.cap < (size_t)nblk + 1) {
+        SNP_CUDA(s->dup_status.ensure((size_t)nblk + 1));
+        SNP_CUDA(cudaMemsetAsync(s->dup_status.p, 0, sizeof(unsigned long long) * s->dup_status.cap, st));
+    }
     if (s->key_capacity == 0) {
         // first guess: 4 keys per (view, primitive); sync_check resizes exactly
         s->key_capacity = std::max<int64_t>(4 * items, 1024);
@@ -349,7 +353,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     b.row_stride = s->row_stride;
     b.rects = s->rects.p;
     b.depth = s->depth.p;
-    b.partials = s->partials.p;
+    b.dup_status = s->dup_status.p;
     b.counters = s->counters.p;
     auto alloc_keys = [&](int64_t cap) -> cudaError_t {
         cudaError_t e;
@@ -362,8 +366,8 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     SNP_CUDA(alloc_keys(s->key_capacity));
     b.capacity = s->key_capacity;
     // K3 scratch: onesweep over the significant bits only; the digit histograms are
-    // accumulated by the duplication kernel itself (cleared by k_scan_partials); the
-    // look-back regions are cleared by the passes themselves (region 0 is clean on entry)
+    // accumulated by the duplication kernel itself (zero on entry, cleared again by K4);
+    // the look-back regions are cleared by the passes themselves (region 0 is clean on entry)
     const int bits = kDepthBits + s->tile_bits + s->view_bits;
     const int passes = (bits + 7) / 8;
     auto ensure_sort_scratch = [&]() -> cudaError_t {
@@ -381,7 +385,9 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     b.passes = passes;
     b.ranges = s->ranges.p;
     b.n_slots = slots;
-    SNP_CUDA(launch_count_scan(b, st));
+    b.keys = s->keys0.p;
+    b.vals = s->vals0.p;
+    SNP_CUDA(launch_dup(b, st));
     if (opts->sync_check) {
         SNP_CUDA(cudaMemcpyAsync(s->h_counters + kCntDup, s->counters.p + kCntDup, sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, st));
@@ -389,23 +395,25 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
         const int64_t ndup = (int64_t)s->h_counters[kCntDup];
         s->known_ndup = ndup;
         if (ndup > s->key_capacity) {
+            // grow exactly once, then duplicate again (the first pass's keys were cut at
+            // the old capacity; its histograms and block states are cleared)
             s->key_capacity = ndup + ndup / 4 + 1024;
             SNP_CUDA(alloc_keys(s->key_capacity));
-            // counters[kCntCapOverflow] was computed against the old capacity
-            SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntCapOverflow, 0, sizeof(unsigned long long), st));
-            SNP_CUDA(ensure_sort_scratch());   // (a new scratch is cleared, histograms included)
+            SNP_CUDA(ensure_sort_scratch());
+            SNP_CUDA(cudaMemsetAsync(s->sort_scratch.p, 0, sizeof(uint32_t) * 8 * 256, st));
+            SNP_CUDA(cudaMemsetAsync(s->dup_status.p, 0, sizeof(unsigned long long) * s->dup_status.cap, st));
+            b.capacity = s->key_capacity;
+            b.hist = s->sort_scratch.p;
+            b.keys = s->keys0.p;
+            b.vals = s->vals0.p;
+            SNP_CUDA(launch_dup(b, st));
         }
-        b.capacity = s->key_capacity;
     }
     SortScratch sc{};
     sc.hist = s->sort_scratch.p;
     sc.lookback = s->sort_scratch.p + 8 * 256;
     sc.tickets = s->sort_scratch.p + 8 * 256 + (size_t)8 * s->sort_max_partitions * 256;
     sc.max_partitions = s->sort_max_partitions;
-    b.keys = s->keys0.p;
-    b.vals = s->vals0.p;
-    b.hist = sc.hist;
-    SNP_CUDA(launch_dup_only(b, st));
     int final_idx = 0;
     SNP_CUDA(launch_onesweep(s->keys0.p, s->vals0.p, s->keys1.p, s->vals1.p, s->key_capacity, s->counters.p,
                              passes, sc, true, s->known_ndup + s->known_ndup / 8, st, &final_idx));
@@ -413,7 +421,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     const uint64_t *sk = final_idx ? s->keys1.p : s->keys0.p;
     // K4
     SNP_CUDA(launch_tile_ranges(sk, s->counters.p, s->key_capacity, s->tile_bits, s->tiles_x * s->tiles_y,
-                                s->ranges.p, slots, st));
+                                s->ranges.p, b, st));
     // join K1b: everything after bin_sort on the caller's stream sees the records
     if (s->join_pending) {
         SNP_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
@@ -512,7 +520,7 @@ snp_status snp_destroy(snp_scene s) {
     s->keys1.release();
     s->vals0.release();
     s->vals1.release();
-    s->partials.release();
+    s->dup_status.release();
     s->sort_scratch.release();
     s->ranges.release();
     s->fallback.release();

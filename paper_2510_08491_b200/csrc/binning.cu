@@ -60,84 +60,68 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s
     return before + x - v;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_count_reduce(BinArgs a) {
-    pdl_prologue();
-    __shared__ uint32_t sw[32];
-    const int64_t total_items = a.n * a.n_views;
-    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-    uint32_t s = 0;
+constexpr unsigned long long kStAgg = 1ull << 62;   // block status: aggregate published
+constexpr unsigned long long kStInc = 2ull << 62;   //               inclusive prefix published
+constexpr unsigned long long kStVal = (1ull << 62) - 1ull;
+
+// Decoupled look-back over the duplication blocks (one warp): returns the number of
+// keys of all blocks before `blk`.  Lane l polls block blk-1-l; the nearest block
+// with an inclusive prefix ends the walk.
+__device__ __forceinline__ unsigned long long dup_lookback(const unsigned long long *status, int64_t blk) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long sum = 0;
+    int64_t q = blk - 1;
+    while (q >= 0) {
+        const int64_t me = q - lane;
+        unsigned long long v = kStInc;   // (before block 0: an inclusive prefix of 0)
+        if (me >= 0) {
+            do {
+                v = *reinterpret_cast<const volatile unsigned long long *>(status + me);
+            } while ((v & ~kStVal) == 0);
+        }
+        const uint32_t inc = __ballot_sync(0xffffffffu, (v & kStInc) != 0);
+        const int stop = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive within the window
+        unsigned long long x = lane <= stop ? (v & kStVal) : 0ull;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k)
-        if (base + k < total_items) s += item_info(a, base + k).count;
-    uint32_t tot;
-    block_exclusive_scan(s, sw, tot);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = tot;
-    // K4 writes only the non-empty tiles' ranges: clear all of them here
-    for (int64_t j = (int64_t)blockIdx.x * kScanThreads + threadIdx.x; j < 2 * a.n_slots;
-         j += (int64_t)gridDim.x * kScanThreads)
-        a.ranges[j] = 0u;
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        sum += x;
+        if (inc) break;
+        q -= 32;
+    }
+    return sum;
 }
 
-// Single block: exclusive scan of the block partials; total -> counters[kCntDup].
-__global__ void __launch_bounds__(1024) k_scan_partials(BinArgs a, int64_t nblocks) {
-    pdl_prologue();
-    __shared__ uint32_t sw[32];
-    __shared__ unsigned long long carry;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry = 0;
-    // the duplication kernel accumulates the digit histograms: clear them here
-    for (int i = threadIdx.x; i < a.passes * 256; i += 1024) a.hist[i] = 0u;
-    __syncthreads();
-    for (int64_t b0 = 0; b0 < nblocks; b0 += 1024) {
-        int64_t b = b0 + threadIdx.x;
-        uint32_t v = b < nblocks ? a.partials[b] : 0;
-        uint32_t x = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y;
-        }
-        if (lane == 31) sw[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t w = sw[lane];
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
-                if (lane >= d) w += y;
-            }
-            sw[lane] = w;
-        }
-        __syncthreads();
-        uint32_t before = wid ? sw[wid - 1] : 0;
-        unsigned long long c = carry;
-        if (b < nblocks) a.partials[b] = (uint32_t)(c + before + x - v);
-        __syncthreads();
-        if (threadIdx.x == 0) carry = c + sw[31];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        unsigned long long tot = carry;
-        a.counters[kCntDup] = tot;
-        a.counters[kCntCapOverflow] = tot > (unsigned long long)a.capacity ? 1ull : 0ull;
-    }
-}
-
-// Recomputes counts, forms per-item offsets, and emits keys warp-aggregated:
-// the 256 items of a warp own a contiguous output range; lanes walk it 32 keys
-// at a time (coalesced 8-byte key + 4-byte value stores), each lane finding its
-// key's item by binary search over the warp's item offsets in shared memory.
+// Single pass: counts the keys of a block of 512 items, gets the block's output
+// offset by a decoupled look-back over the earlier blocks (block order from an
+// atomic ticket, so every earlier block is resident or done), forms per-item
+// offsets and emits keys warp-aggregated: the 256 items of a warp own a contiguous
+// output range; lanes walk it 32 keys at a time (coalesced 8-byte key + 4-byte
+// value stores), each lane finding its key's item by binary search over the warp's
+// item offsets in shared memory.  The last block writes the key count.
 __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
     pdl_prologue();
     __shared__ uint32_t sw[32];
+    __shared__ int64_t s_blk;
+    __shared__ unsigned long long s_gbase;
     __shared__ uint32_t s_off[kScanTile + 8];   // per item exclusive offset (block-relative)
     __shared__ uint32_t s_hist[8][256];         // digit histograms of the keys this block emits
     __shared__ int32_t s_x0[kScanTile], s_w[kScanTile], s_rf[kScanTile];   // item geometry, read once
     __shared__ uint32_t s_dep[kScanTile];
     for (int i = threadIdx.x; i < a.passes * 256; i += kScanThreads) (&s_hist[0][0])[i] = 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        const int64_t t = (int64_t)atomicAdd(a.dup_status + gridDim.x, 1ull);
+        s_blk = t;
+        if (t == (int64_t)gridDim.x - 1) a.dup_status[gridDim.x] = 0ull;   // last ticket: reset
+    }
+    // K4 writes only the non-empty tiles' ranges: clear all of them here
+    for (int64_t j = (int64_t)blockIdx.x * kScanThreads + threadIdx.x; j < 2 * a.n_slots;
+         j += (int64_t)gridDim.x * kScanThreads)
+        a.ranges[j] = 0u;
+    __syncthreads();
+    const int64_t blk = s_blk;
     const int64_t total_items = a.n * a.n_views;
-    const int64_t blk0 = (int64_t)blockIdx.x * kScanTile;
+    const int64_t blk0 = blk * kScanTile;
     const int64_t base = blk0 + (int64_t)threadIdx.x * kScanItems;
     uint32_t cnt[kScanItems];
     uint32_t s = 0;
@@ -161,8 +145,23 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
         ex += cnt[k];
     }
     if (threadIdx.x == kScanThreads - 1) s_off[kScanTile] = ex;   // block total
+    if (wid == 0) {
+        if (lane == 0) {
+            if (blk == 0) atomicExch(a.dup_status, kStInc | (unsigned long long)tot);
+            else atomicExch(a.dup_status + blk, kStAgg | (unsigned long long)tot);
+        }
+        const unsigned long long excl = blk == 0 ? 0ull : dup_lookback(a.dup_status, blk);
+        if (lane == 0) {
+            if (blk > 0) atomicExch(a.dup_status + blk, kStInc | (excl + tot));
+            s_gbase = excl;
+            if (blk == (int64_t)gridDim.x - 1) {
+                a.counters[kCntDup] = excl + tot;
+                a.counters[kCntCapOverflow] = excl + tot > (unsigned long long)a.capacity ? 1ull : 0ull;
+            }
+        }
+    }
     __syncthreads();
-    const uint64_t gbase = a.partials[blockIdx.x];
+    const uint64_t gbase = s_gbase;
     // warp wid owns items [wid*256, wid*256+256) of this block
     const int i0 = wid * 32 * kScanItems;
     const uint32_t wbeg = s_off[i0];
@@ -200,8 +199,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
 }
 
 __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
-                              int32_t tile_bits, int32_t tiles, uint32_t *ranges) {
+                              int32_t tile_bits, int32_t tiles, uint32_t *ranges, unsigned long long *dup_status,
+                              int64_t dup_blocks, uint32_t *hist, int32_t hist_words) {
     pdl_prologue();
+    // the next frame's K2 needs clean block states and digit histograms (no memset node)
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < dup_blocks; j += (int64_t)gridDim.x * blockDim.x)
+        dup_status[j] = 0ull;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < hist_words; j += (int64_t)gridDim.x * blockDim.x)
+        hist[j] = 0u;
     int64_t n = (int64_t)counters[kCntDup];
     if (n > capacity) n = capacity;
     const uint64_t tmask = (1ull << tile_bits) - 1ull;
@@ -217,9 +222,8 @@ __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *co
 
 int64_t bin_scan_blocks(int64_t items) { return (items + kScanTile - 1) / kScanTile; }
 
-cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st) {
-    const int64_t items = a.n * a.n_views;
-    const int64_t nb = bin_scan_blocks(items);
+cudaError_t launch_dup(const BinArgs &a, cudaStream_t st) {
+    const int64_t nb = bin_scan_blocks(a.n * a.n_views);
     if (nb == 0) {
         cudaError_t e = cudaMemsetAsync(a.counters + kCntDup, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
@@ -228,30 +232,20 @@ cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st) {
         if (a.n_slots > 0) e = cudaMemsetAsync(a.ranges, 0, sizeof(uint32_t) * 2 * (size_t)a.n_slots, st);
         return e;
     }
-    cudaError_t e0 = launch_hi(k_count_reduce, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a);
-    if (e0 != cudaSuccess) return e0;
-    e0 = launch_hi(k_scan_partials, dim3(1), dim3(1024), 0, st, a, (int64_t)nb);
-    if (e0 != cudaSuccess) return e0;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_dup_only(const BinArgs &a, cudaStream_t st) {
-    const int64_t nb = bin_scan_blocks(a.n * a.n_views);
-    if (nb == 0) return cudaSuccess;
     cudaError_t e0 = launch_hi(k_scan_dup, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a);
     if (e0 != cudaSuccess) return e0;
     return cudaGetLastError();
 }
 
 cudaError_t launch_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
-                               int32_t tile_bits, int32_t tiles, uint32_t *ranges, int64_t n_slots,
+                               int32_t tile_bits, int32_t tiles, uint32_t *ranges, const BinArgs &b,
                                cudaStream_t st) {
-    (void)n_slots;   // cleared by k_count_reduce
     cudaError_t e = cudaSuccess;
     if (capacity == 0) return cudaSuccess;
     int64_t blocks = (capacity + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    e = launch_hi(k_tile_ranges, dim3((unsigned)blocks), dim3(256), 0, st, keys, counters, capacity, tile_bits, tiles, ranges);
+    e = launch_hi(k_tile_ranges, dim3((unsigned)blocks), dim3(256), 0, st, keys, counters, capacity, tile_bits, tiles,
+                  ranges, b.dup_status, bin_scan_blocks(b.n * b.n_views), b.hist, (int32_t)(b.passes * 256));
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -121,19 +121,21 @@ struct BinArgs {
     uint64_t *keys;         // [capacity]
     uint32_t *vals;         // [capacity]
     int64_t capacity;
-    uint32_t *partials;     // scan scratch [num_blocks + 1]
+    unsigned long long *dup_status;   // [num_blocks + 1]: look-back states of the K2 blocks + ticket;
+                                      // zero on entry, cleared again by K4
     unsigned long long *counters;
     uint32_t *hist;         // [passes][256] digit histograms accumulated during duplication
-                            // (zeroed by k_scan_partials)
+                            // (zero on entry, cleared again by K4)
     int32_t passes;
-    uint32_t *ranges;       // [n_slots][2] tile ranges, zeroed by k_count_reduce (filled by K4)
+    uint32_t *ranges;       // [n_slots][2] tile ranges, zeroed by K2 (filled by K4)
     int64_t n_slots;
 };
 int64_t bin_scan_blocks(int64_t items);
-cudaError_t launch_count_scan(const BinArgs &a, cudaStream_t st);   // counts + scan -> counters[kCntDup]
-cudaError_t launch_dup_only(const BinArgs &a, cudaStream_t st);     // needs launch_count_scan first
+// K2, one pass: keys + values (up to capacity), digit histograms, counters[kCntDup]
+cudaError_t launch_dup(const BinArgs &a, cudaStream_t st);
+// K4 (also clears b.dup_status and b.hist for the next frame)
 cudaError_t launch_tile_ranges(const uint64_t *keys, const unsigned long long *counters, int64_t capacity,
-                               int32_t tile_bits, int32_t tiles, uint32_t *ranges, int64_t n_slots,
+                               int32_t tile_bits, int32_t tiles, uint32_t *ranges, const BinArgs &b,
                                cudaStream_t st);
 
 struct SortScratch {
