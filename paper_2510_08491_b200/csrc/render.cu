@@ -692,6 +692,7 @@ __device__ __forceinline__ bool fb_less(const FbSmem &s, int a, int b, int n) {
 }
 
 __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb) {
+    pdl_prologue();   // scheduled while K5 drains; waits for it here
     __shared__ FbSmem sm;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int64_t nq = (int64_t)a.counters[kCntFallbackQueue];
@@ -955,7 +956,10 @@ cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_bat
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback, kFbThreads, 0);
         resident = std::max(1, sms) * std::max(1, per_sm);
     }
-    for (int i = 0; i < n_batches; ++i) k_fallback<<<resident, kFbThreads, 0, st>>>(a, cams[i]);
+    for (int i = 0; i < n_batches; ++i) {
+        cudaError_t e = launch_hi(k_fallback, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i]);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
 }
 
