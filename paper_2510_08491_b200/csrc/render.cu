@@ -60,8 +60,8 @@ struct __align__(16) Smem {
     unsigned long long empty[kStages];        // slot released by all consumer warps
     int32_t tdone[kTileRing];                 // consumer warps finished with tile seq % kTileRing
     int32_t next_tile;
-    uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs:
-    uint8_t ql[kWarps][64];                   //   (record slot j, owner lane)
+    uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs
+    uint8_t ql[kWarps][64];                   //   (record slot j, owner lane), a ring from qhead
     float p_thi[kPend][kWarps * 32];          // pending hits, one column per pixel, kept sorted by
                                               // (t_in, id) in a ring starting at the head: t_in
                                               // (fp32: its 6e-8 rounding is far below the 1e-6
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 #ifdef SNP_INSTRUMENT
             ins_pre += clock64() - _p0;
 #endif
-            int qcount = 0;
+            int qcount = 0, qhead = 0;
             auto round = [&](int n) {
 #ifdef SNP_INSTRUMENT
                 long long _r0 = clock64();
@@ -475,8 +475,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 #endif
                 __syncwarp();
                 const bool valid = lane < n;
-                const int owner = valid ? sm.ql[wid][lane] : lane;
-                const int j = valid ? sm.qj[wid][lane] : 0;
+                const int qi = (qhead + lane) & 63;
+                const int owner = valid ? sm.ql[wid][qi] : lane;
+                const int j = valid ? sm.qj[wid][qi] : 0;
                 Ray ro;
                 ro.dhx = __shfl_sync(0xffffffffu, ray.dhx, owner);
                 ro.dhy = __shfl_sync(0xffffffffu, ray.dhy, owner);
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     const bool cand = !ps.done && q <= 1.0f;
                     const uint32_t cm = __ballot_sync(0xffffffffu, cand);
                     if (cand) {
-                        const int pos = qcount + __popc(cm & lt_mask);
+                        const int pos = (qhead + qcount + __popc(cm & lt_mask)) & 63;
                         sm.qj[wid][pos] = (uint8_t)j;
                         sm.ql[wid][pos] = (uint8_t)lane;
                         ++n_cand;
@@ -571,20 +572,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 if (qcount > 0) {
                     round(qcount < 32 ? qcount : 32);
                     rem = qcount > 32 ? qcount - 32 : 0;
-                    uint8_t vj = 0, vl = 0;
-                    if (lane < rem) {
-                        vj = sm.qj[wid][32 + lane];
-                        vl = sm.ql[wid][32 + lane];
-                    }
-                    __syncwarp();
-                    if (lane < rem) {
-                        sm.qj[wid][lane] = vj;
-                        sm.ql[wid][lane] = vl;
-                    }
-                    __syncwarp();
-                    // every hit this warp has not appended yet comes from a record >= the
+                    qhead = (qhead + 32) & 63;
+                    // every hit this warp has not inserted yet comes from a record >= the
                     // oldest queued one (or > jlast), so that record's L bounds its t_in
-                    if (rem > 0) jn = (int)__shfl_sync(0xffffffffu, (uint32_t)vj, 0);
+                    if (rem > 0) jn = sm.qj[wid][qhead];
                     qcount = rem;
                 }
                 const bool batch_end = (m == 0u) && rem == 0;
