@@ -155,8 +155,8 @@ def run_snp(args):
     torch.cuda.synchronize()
     stats = snp.get_stats(h, st)
     passes = (19 + int(np.ceil(np.log2(((W + 15) // 16) * ((H + 15) // 16)))) + 7) // 8
-    # K1a, K1b, K2 (single-pass dup), K3 x passes, K4, K5, K6
-    launches_per_step = 6 + passes
+    # K1a, K1b, K2 (single-pass dup), K3 x passes, K4, tile order, K5, K6
+    launches_per_step = 7 + passes
 
     clk = ClockSampler(local)
     if ws > 1:

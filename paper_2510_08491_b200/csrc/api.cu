@@ -85,7 +85,7 @@ struct snp_scene_s {
     // render
     DevBuf<uint32_t> fallback;
     int64_t fallback_capacity = 0;
-    DevBuf<float4> fb_scratch;
+    DevBuf<uint32_t> tile_order;     // K5's tile order, per camera batch (kCamsPerLaunch x stripe tiles each)
     DevBuf<float> host_out_staging;
     int32_t pending_limit = 16;
     // counters
@@ -422,6 +422,22 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     // K4
     SNP_CUDA(launch_tile_ranges(sk, s->counters.p, s->key_capacity, s->tile_bits, s->tiles_x * s->tiles_y,
                                 s->ranges.p, b, st));
+    // K5's tile orders (longest tile list first), one per camera batch; they run while
+    // K1b may still be busy on the side stream
+    {
+        const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
+        SNP_CUDA(s->tile_order.ensure(std::max<size_t>(1, order_stride * s->cams.size())));
+        RenderArgs ra{};
+        ra.tiles_x = s->tiles_x;
+        ra.tiles_y = s->tiles_y;
+        ra.tiles_per_view = s->tiles_x * s->tiles_y;
+        ra.row_begin = s->row_begin;
+        ra.row_stride = s->row_stride;
+        ra.stripe_rows = s->stripe_rows;
+        ra.ranges = s->ranges.p;
+        for (size_t k = 0; k < s->cams.size(); ++k)
+            SNP_CUDA(launch_tile_order(ra, s->cams[k], s->tile_order.p + k * order_stride, st));
+    }
     // join K1b: everything after bin_sort on the caller's stream sees the records
     if (s->join_pending) {
         SNP_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
@@ -454,7 +470,6 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
         SNP_CUDA(s->fallback.ensure((size_t)fb_cap * 2));
         s->fallback_capacity = fb_cap;
     }
-    SNP_CUDA(s->fb_scratch.ensure((size_t)fallback_scratch_float4()));
     // stats, fallback queue and tile queue: one memset (contiguous counters)
     SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
                              sizeof(unsigned long long) * (kCntTileQueue - kCntTested + 1), st));
@@ -481,11 +496,14 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     a.out = dout;
     a.fallback = s->fallback.p;
     a.fallback_capacity = s->fallback_capacity;
-    a.fb_scratch = s->fb_scratch.p;
+    const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     a.counters = s->counters.p;
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
-        for (size_t k = 0; k < s->cams.size(); ++k) SNP_CUDA(launch_render(a, s->cams[k], k > 0, st));
+        for (size_t k = 0; k < s->cams.size(); ++k) {
+            a.tile_order = s->tile_order.p + k * order_stride;
+            SNP_CUDA(launch_render(a, s->cams[k], k > 0, st));
+        }
         // (SNP_DEBUG bit 2 skips K6: timing experiments only, overflowed pixels stay unwritten)
         if (s->n > 0 && !(a.debug_flags & 2)) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
     }
@@ -524,7 +542,7 @@ snp_status snp_destroy(snp_scene s) {
     s->sort_scratch.release();
     s->ranges.release();
     s->fallback.release();
-    s->fb_scratch.release();
+    s->tile_order.release();
     s->host_out_staging.release();
     s->counters.release();
     s->flag.release();

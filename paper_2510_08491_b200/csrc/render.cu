@@ -273,12 +273,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 #ifdef SNP_INSTRUMENT
         long long p_wait = 0;
         const long long p_start = clock64();
+        unsigned long long g_start;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_start));
 #endif
         uint32_t gb = 0;            // global batch counter (ring slot / phase)
         int seq = 0;
         while (true) {
             int t = 0;
-            if (lane == 0) t = (int)atomicAdd(a.counters + kCntTileQueue, 1ull);
+            if (lane == 0) {
+                t = (int)atomicAdd(a.counters + kCntTileQueue, 1ull);
+                if (t < total_tiles) t = (int)a.tile_order[t];   // heaviest tiles first
+            }
             t = __shfl_sync(0xffffffffu, t, 0);
             const int slot0 = (int)(gb % kStages);
             if (gb >= kStages) {
@@ -352,6 +357,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         if (lane == 0) {
             atomicAdd(a.counters + 26, (unsigned long long)p_wait);
             atomicAdd(a.counters + 27, (unsigned long long)(clock64() - p_start));
+            unsigned long long g_end;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_end));
+            atomicMax(a.counters + 32, ~g_start);
+            atomicMax(a.counters + 33, g_end);
+            atomicAdd(a.counters + 34, g_end >> 10);
+            atomicAdd(a.counters + 35, 1ull);
         }
 #endif
         return;
@@ -908,9 +919,55 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
     }
 }
 
-}  // namespace
+// One CTA per camera batch: histogram of the slots over 256 length buckets
+// (bucket 0 = longest list), exclusive scan, scatter.  The order inside a bucket is
+// arbitrary: tiles are independent, so the rendered frame does not depend on it.
+__global__ void __launch_bounds__(1024) k_tile_order(RenderArgs a, CamBatch cb, uint32_t *order) {
+    pdl_prologue();
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t wsum[32];
+    const int stripe_tiles = a.tiles_x * a.stripe_rows;
+    const int total = stripe_tiles * cb.nv;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    auto bucket = [&](int t) -> int {
+        const int vloc = t / stripe_tiles;
+        const int st = t - vloc * stripe_tiles;
+        const int tx = st % a.tiles_x;
+        const int ty = a.row_begin + (st / a.tiles_x) * a.row_stride;
+        const int64_t slot = (int64_t)(cb.view0 + vloc) * a.tiles_per_view + ty * a.tiles_x + tx;
+        const uint32_t len = a.ranges[2 * slot + 1] - a.ranges[2 * slot];
+        if (len == 0) return 255;
+        const int lz = __clz(len);                                  // len in [2^(31-lz), 2^(32-lz))
+        const int frac = (int)((len << lz << 1) >> 29);             // 3 bits below the leading one
+        const int lg8 = (31 - lz) * 8 + frac;                       // ~ 8 log2(len)
+        return 254 - (lg8 < 254 ? lg8 : 254);
+    };
+    for (int t = tid; t < total; t += 1024) atomicAdd(&hist[bucket(t)], 1u);
+    __syncthreads();
+    if (tid < 256) {   // exclusive scan over the 256 buckets (8 warps)
+        const uint32_t v = hist[tid];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        hist[tid] = x - v;   // exclusive within the warp
+    }
+    __syncthreads();
+    if (tid < 256) {
+        uint32_t before = 0;
+        for (int w = 0; w < wid; ++w) before += wsum[w];
+        hist[tid] += before;
+    }
+    __syncthreads();
+    for (int t = tid; t < total; t += 1024) order[atomicAdd(&hist[bucket(t)], 1u)] = (uint32_t)t;
+}
 
-int64_t fallback_scratch_float4() { return 1; }   // K6 keeps its hits in shared memory
+}  // namespace
 
 cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st) {
     static bool attr_set = false;
@@ -937,6 +994,11 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
     const int grid = std::min(tiles, resident);
     k_render<<<grid, kThreads, smem, st>>>(a, cams);
     return cudaGetLastError();
+}
+
+cudaError_t launch_tile_order(const RenderArgs &a, const CamBatch &cams, uint32_t *order, cudaStream_t st) {
+    if (a.tiles_x * a.stripe_rows * cams.nv == 0) return cudaSuccess;
+    return launch_hi(k_tile_order, dim3(1), dim3(1024), 0, st, a, cams, order);
 }
 
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {

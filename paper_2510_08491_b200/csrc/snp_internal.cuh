@@ -90,7 +90,7 @@ enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecW
 // The render counters kCntTested..kCntTileQueue are contiguous: one memset per render.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
                kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
-               kNumCounters = 32 };   // 16..31: SNP_INSTRUMENT builds only
+               kNumCounters = 40 };   // 10..39: instrumented (A/B) builds only
 
 struct ProjectArgs {
     int64_t n;
@@ -173,10 +173,12 @@ struct RenderArgs {
     float *out;                    // [V][H][W][4]
     uint32_t *fallback;            // [capacity][2] (view, pixel) of overflowed pixels
     int64_t fallback_capacity;
-    float4 *fb_scratch;            // K6 per-warp stored hits [fallback_scratch_float4()]
+    const uint32_t *tile_order;    // K5 claims tiles in this order (heaviest list first)
     unsigned long long *counters;
 };
-int64_t fallback_scratch_float4();
+// LPT order of one camera batch's (view, stripe tile) slots into order[]: descending
+// tile-list length (8 buckets per octave), so that K5's dynamic queue ends on light tiles
+cudaError_t launch_tile_order(const RenderArgs &a, const CamBatch &cams, uint32_t *order, cudaStream_t st);
 // reset_queue: zero the tile queue first (needed for every camera batch after the
 // first; the caller zeroes all render counters once per snp_render)
 cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st);

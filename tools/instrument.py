@@ -16,7 +16,8 @@ snp.render_views(h, cams, snp.make_opts(bg, sync_check=1), out)
 opts = snp.make_opts(bg, sync_check=0)
 snp.render_views(h, cams, opts, out)
 torch.cuda.synchronize()
-c = snp.get_debug_counters(h).astype(np.float64)
+c = snp.get_debug_counters(h, 40).astype(np.float64)
+ci = snp.get_debug_counters(h, 40)
 tot = c[21]
 names = {16: "wait", 17: "rounds", 18: "emit", 22: "fill", 23: "pre", 24: "setup", 25: "finish"}
 parts = "  ".join("%s %.1f%%" % (nm, 100 * c[k] / tot) for k, nm in names.items())
@@ -27,3 +28,6 @@ print(cfg, "producer: waiting on free slots %.1f%% of its time" % (100 * c[26] /
 print(cfg, "touching (warp, record) pairs %.3g, with no candidate lane %.1f%%; emit calls (lane) %.3g, with empty list %.1f%%" % (
     c[12], 100 * c[13] / max(c[12], 1), c[14], 100 * c[15] / max(c[14], 1)))
 print(cfg, "insertion steps per round %.2f" % (c[10] / max(c[19], 1)))
+t0 = int(~np.uint64(ci[32])); tmax = int(ci[33]); tmean = int(ci[34]) * 1024.0 / max(int(ci[35]), 1)
+print(cfg, "CTA end times after the first start: mean %.1f us, last %.1f us (tail %.1f us)" % (
+    (tmean - t0) / 1e3, (tmax - t0) / 1e3, (tmax - tmean) / 1e3))
