@@ -317,20 +317,24 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
     }
 }
 
-// One CTA per slice; a slice with no visible primitive is never loaded.
+// One CTA per slice.  The slice load is issued first (its latency overlaps the
+// visibility read); a CTA whose slice has no visible primitive only waits for it.
 __global__ void __launch_bounds__(kProjThreads, 4) k_records(ProjectArgs a, CamBatch cb) {
     extern __shared__ __align__(128) unsigned char psm_raw[];
     ProjSmem &ps = *reinterpret_cast<ProjSmem *>(psm_raw);
     const int64_t i0 = (int64_t)blockIdx.x * kProjThreads;
-    const uint32_t vis = vis_mask_of(a, cb, i0 + threadIdx.x);
-    if (!__syncthreads_or(vis != 0)) return;
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&ps.bar_geo)) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&ps.bar_rest)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         issue_slice(a, ps.buf, &ps.bar_geo, &ps.bar_rest, i0);
     }
-    __syncthreads();
+    const uint32_t vis = vis_mask_of(a, cb, i0 + threadIdx.x);
+    if (!__syncthreads_or(vis != 0)) {   // (also publishes the barrier init)
+        mbar_wait0(&ps.bar_geo);         // the copies must land before the CTA's smem is freed
+        mbar_wait0(&ps.bar_rest);
+        return;
+    }
     mbar_wait0(&ps.bar_geo);
     if (vis) {
         const int li = threadIdx.x;
