@@ -83,7 +83,7 @@ struct snp_scene_s {
     int sorted_idx = 0;
     DevBuf<uint32_t> ranges;
     // render
-    DevBuf<uint32_t> fallback;
+    DevBuf<unsigned long long> fallback;
     int64_t fallback_capacity = 0;
     DevBuf<uint32_t> tile_order;     // K5's tile order, per camera batch (kCamsPerLaunch x stripe tiles each)
     DevBuf<float> host_out_staging;
@@ -467,12 +467,13 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     }
     const int64_t fb_cap = std::min<int64_t>((int64_t)s->n_views * s->W * s->H, (int64_t)1 << 22);
     if (s->fallback_capacity < fb_cap) {
-        SNP_CUDA(s->fallback.ensure((size_t)fb_cap * 2));
+        SNP_CUDA(s->fallback.ensure((size_t)fb_cap));
+        SNP_CUDA(cudaMemsetAsync(s->fallback.p, 0, sizeof(unsigned long long) * (size_t)fb_cap, st));
         s->fallback_capacity = fb_cap;
     }
     // stats, fallback queue and tile queue: one memset (contiguous counters)
     SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
-                             sizeof(unsigned long long) * (kCntTileQueue - kCntTested + 1), st));
+                             sizeof(unsigned long long) * (kCntK5Done - kCntTested + 1), st));
     RenderArgs a{};
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
@@ -498,6 +499,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     a.fallback_capacity = s->fallback_capacity;
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     a.counters = s->counters.p;
+    a.k5_grid = render_grid(s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
         for (size_t k = 0; k < s->cams.size(); ++k) {

@@ -60,6 +60,7 @@ struct __align__(16) Smem {
     unsigned long long empty[kStages];        // slot released by all consumer warps
     int32_t tdone[kTileRing];                 // consumer warps finished with tile seq % kTileRing
     int32_t next_tile;
+    int32_t warps_done;                       // warps of this CTA that have finished (K5 exit signal)
     uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs
     uint8_t ql[kWarps][64];                   //   (record slot j, owner lane), a ring from qhead
     float p_thi[kPend][kWarps * 32];          // pending hits, one column per pixel, kept sorted by
@@ -264,9 +265,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             mbar_init(&sm.empty[s], kConsumers);
         }
         for (int s = 0; s < kTileRing; ++s) sm.tdone[s] = 0;
+        sm.warps_done = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
+    // K6 may be scheduled as soon as every K5 CTA is resident: it only takes the SM
+    // space that finished K5 CTAs free (see k_fallback)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // the last warp of the CTA to finish publishes the CTA's exit (after its queue pushes)
+    auto warp_exit = [&]() {
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            if (atomicAdd(&sm.warps_done, 1) == kConsumers) {
+                __threadfence();
+                atomicAdd(a.counters + kCntK5Done, 1ull);
+            }
+        }
+    };
 
     if (wid == kConsumers) {
         // =============================== producer warp
@@ -365,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             atomicAdd(a.counters + 35, 1ull);
         }
 #endif
+        warp_exit();
         return;
     }
 
@@ -393,10 +410,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         if (inside) {
             if (ps.overflow) {
                 const unsigned long long q = atomicAdd(a.counters + kCntFallbackQueue, 1ull);
-                if ((int64_t)q < a.fallback_capacity) {
-                    a.fallback[2 * q] = (uint32_t)view;
-                    a.fallback[2 * q + 1] = (uint32_t)(y * cam->W + x);
-                }
+                if ((int64_t)q < a.fallback_capacity)
+                    atomicExch(a.fallback + q, (1ull << 63) | ((unsigned long long)view << 32) |
+                                                   (unsigned long long)(uint32_t)(y * cam->W + x));
                 ++n_ovf;
             } else {
                 const float4 o = make_float4(fmaf(ps.T, a.bg[0], ps.cr), fmaf(ps.T, a.bg[1], ps.cg),
@@ -635,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         atomicAdd(a.counters + 25, (unsigned long long)ins_finish);
         atomicAdd(a.counters + 12, (unsigned long long)ins_touch);
         atomicAdd(a.counters + 13, (unsigned long long)ins_empty);
-        atomicAdd(a.counters + 10, (unsigned long long)ins_steps);
+        atomicAdd(a.counters + 36, (unsigned long long)ins_steps);
     }
     {
         const unsigned long long ec = __reduce_add_sync(0xffffffffu, (uint32_t)ins_ecalls);
@@ -653,6 +669,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         const uint32_t s = __reduce_add_sync(0xffffffffu, v[c]);   // per-warp totals fit 32 bits
         if (lane == 0 && s) atomicAdd(a.counters + kCntTested + c, (unsigned long long)s);
     }
+    warp_exit();
 }
 
 __device__ __forceinline__ bool fb_hit(const float4 *rec, const Ray &ray, float pxf, float pyf, float &th,
@@ -694,17 +711,56 @@ __device__ __forceinline__ bool fb_less(const FbSmem &s, int a, int b, int n) {
     return before(s.t[a], s.l[a], s.id[a], s.t[b], s.l[b], s.id[b]);
 }
 
-__global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb) {
-    pdl_prologue();   // scheduled while K5 drains; waits for it here
+__device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long *p) {
+    return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+
+// overlap = true (one camera batch): launched as K5's programmatic dependent; entries
+// are claimed one at a time as K5 queues them, and the CTA leaves once every K5 CTA has
+// exited and no entry is left.  overlap = false: K5 has completed; CTAs stride over the
+// queue and take the entries of this batch's views.
+__global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb, int overlap) {
+    if (!overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ FbSmem sm;
+    __shared__ unsigned long long s_entry;
+    __shared__ int64_t s_q;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    int64_t nq = (int64_t)a.counters[kCntFallbackQueue];
+    int64_t nq = overlap ? 0 : (int64_t)a.counters[kCntFallbackQueue];
     if (nq > a.fallback_capacity) nq = a.fallback_capacity;
-    for (int64_t qi = blockIdx.x; qi < nq; qi += gridDim.x) {
-        const int64_t view = a.fallback[2 * qi];
+    for (int64_t it = blockIdx.x;; it += gridDim.x) {
+        if (tid == 0) {
+            unsigned long long v = 0;
+            int64_t q = it;
+            if (overlap) {
+                q = (int64_t)atomicAdd(a.counters + kCntFallbackClaim, 1ull);
+                while (q < a.fallback_capacity) {
+                    v = ld_vol64(a.fallback + q);
+                    if (v) break;
+                    if (ld_vol64(a.counters + kCntK5Done) == (unsigned long long)a.k5_grid) {
+                        v = ld_vol64(a.fallback + q);   // (pushed before K5's exit signal)
+                        break;
+                    }
+                    __nanosleep(200);
+                }
+            } else if (q < nq) {
+                v = a.fallback[q];
+            } else {
+                v = ~0ull;   // end
+            }
+            s_entry = v;
+            s_q = q;
+        }
+        __syncthreads();
+        const unsigned long long ent = s_entry;
+        const int64_t qi = s_q;
+        __syncthreads();
+        if (overlap ? ent == 0 : ent == ~0ull) break;
+        if (!(ent >> 63)) continue;
+        const int64_t view = (int64_t)((ent >> 32) & 0x7fffffffull);
         if (view < cb.view0 || view >= cb.view0 + cb.nv) continue;
+        if (tid == 0) a.fallback[qi] = 0ull;   // consumed: the queue is all zero between renders
         const DevCam &cam = cb.cams[view - cb.view0];
-        const uint32_t pix = a.fallback[2 * qi + 1];
+        const uint32_t pix = (uint32_t)ent;
         const int x = (int)(pix % (uint32_t)cam.W), y = (int)(pix / (uint32_t)cam.W);
         const int tile = (y / kTile) * a.tiles_x + (x / kTile);
         const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
@@ -917,6 +973,8 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
         }
         __syncthreads();
     }
+    // (the grid completes only after K5: later work in the stream sees both)
+    if (overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // One CTA per camera batch: histogram of the slots over 256 length buckets
@@ -983,17 +1041,21 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
         cudaError_t e = cudaMemsetAsync(a.counters + kCntTileQueue, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
     }
+    k_render<<<render_grid(tiles), kThreads, smem, st>>>(a, cams);
+    return cudaGetLastError();
+}
+
+int render_grid(int tiles) {
     static int resident = 0;   // persistent grid: every CTA that fits, all SMs
     if (!resident) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render, kThreads, smem);
+        cudaFuncSetAttribute(k_render, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render, kThreads, sizeof(Smem));
         resident = std::max(1, sms) * std::max(1, per_sm);
     }
-    const int grid = std::min(tiles, resident);
-    k_render<<<grid, kThreads, smem, st>>>(a, cams);
-    return cudaGetLastError();
+    return std::min(tiles, resident);
 }
 
 cudaError_t launch_tile_order(const RenderArgs &a, const CamBatch &cams, uint32_t *order, cudaStream_t st) {
@@ -1010,8 +1072,9 @@ cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_bat
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback, kFbThreads, 0);
         resident = std::max(1, sms) * std::max(1, per_sm);
     }
+    const int overlap = n_batches == 1 ? 1 : 0;
     for (int i = 0; i < n_batches; ++i) {
-        cudaError_t e = launch_hi(k_fallback, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i]);
+        cudaError_t e = launch_hi(k_fallback, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i], overlap);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();

@@ -87,9 +87,10 @@ enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecW
                   kRecWh1 = 5, kRecUnits = 6, kRecW2 = 14 };
 
 // Device-side counters (one 64-bit slot each), see snp_stats.
-// The render counters kCntTested..kCntTileQueue are contiguous: one memset per render.
+// The render counters kCntTested..kCntK5Done are contiguous: one memset per render.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
                kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
+               kCntFallbackClaim = 10, kCntK5Done = 11,
                kNumCounters = 40 };   // 10..39: instrumented (A/B) builds only
 
 struct ProjectArgs {
@@ -171,9 +172,11 @@ struct RenderArgs {
     int32_t pending_limit;
     int32_t debug_flags;           // SNP_DEBUG env bits (1: no sub-tile culling); 0 in production
     float *out;                    // [V][H][W][4]
-    uint32_t *fallback;            // [capacity][2] (view, pixel) of overflowed pixels
+    unsigned long long *fallback;  // [capacity] overflowed pixels: 1 << 63 | view << 32 | pixel; 0 = empty
+                                   // (K6 clears every entry it consumes: all zero between renders)
     int64_t fallback_capacity;
     const uint32_t *tile_order;    // K5 claims tiles in this order (heaviest list first)
+    int32_t k5_grid;               // K5's CTA count (K6 overlapping K5 waits for that many exits)
     unsigned long long *counters;
 };
 // LPT order of one camera batch's (view, stripe tile) slots into order[]: descending
@@ -182,6 +185,10 @@ cudaError_t launch_tile_order(const RenderArgs &a, const CamBatch &cams, uint32_
 // reset_queue: zero the tile queue first (needed for every camera batch after the
 // first; the caller zeroes all render counters once per snp_render)
 cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st);
+// K6.  With one camera batch it overlaps K5: its CTAs start on the SMs K5's finished
+// CTAs leave, take overflowed pixels as K5 queues them and end once every K5 CTA has
+// exited.  With several batches it runs after all of them.
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
+int render_grid(int tiles);   // K5's persistent grid for `tiles` work units
 
 }  // namespace snp
