@@ -212,35 +212,51 @@ def run_snp(args):
         except Exception:
             traffic = None
 
-    # ---- e2e through the C ABI with HOST buffers: upload scene from pinned host memory,
-    # render, read the frame back to host; copies inside the timed region
+    # ---- e2e through the C ABI with HOST buffers: every step uploads the scene from pinned
+    # host memory (snp_update_scene: H2D + device validation) and reads its frame back into
+    # pinned host memory (SNP_MEM_HOST_ASYNC); copies inside the timed region.  Two scene
+    # handles alternate so that step i+1's upload overlaps step i's render and read-back
+    # (PCIe is full duplex), as a serving loop would run it.
     host = {}
     for f in ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh"):
         host[f] = torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).pin_memory()
     import types
     hscene = types.SimpleNamespace(omega=scene.omega, sh_degree=scene.sh_degree, **host)
-    hout = torch.empty((1, H, W, 4)).pin_memory()
-    opts_host = snp.make_opts(bg, 1e-4, out_memory=snp.SNP_MEM_HOST, sync_check=1)
+    hout = [torch.empty((1, H, W, 4)).pin_memory() for _ in range(2)]
+    opts_first = snp.make_opts(bg, 1e-4, out_memory=snp.SNP_MEM_HOST, sync_check=1)
+    opts_async = snp.make_opts(bg, 1e-4, out_memory=snp.SNP_MEM_HOST_ASYNC, sync_check=0)
     h2d = sum(int(v.numel()) * 4 for v in host.values()) + 88
-    d2h = int(hout.numel()) * 4
-    e2e_steps = max(5, min(args.steps, 50))
-    he = snp.create_scene(hscene, local, st)
+    d2h = int(hout[0].numel()) * 4
+    e2e_steps = max(6, min(args.steps, 50))
+    s_up, s_rn = torch.cuda.Stream(), torch.cuda.Stream()
+    he = [snp.create_scene(hscene, local, s_up) for _ in range(2)]
+    for k in range(2):
+        snp.render_views(he[k], cams_c, opts_first, hout[k], s_rn)   # sizing call (outside timing)
+    ev_up = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    for k in range(2):
+        ev_done[k].record(s_rn)
 
-    def e2e_step():
-        # the step's inputs cross PCIe: parameters from pinned host memory (validated on the
-        # device), the frame back to pinned host memory; both inside the timed region
-        snp.update_scene(he, hscene, st)
-        snp.render_views(he, cams_c, opts_host, hout, st)
+    def e2e_step(i):
+        k = i & 1
+        s_up.wait_event(ev_done[k])            # handle k's previous render and read-back are done
+        snp.update_scene(he[k], hscene, s_up)  # H2D + validation (returns once validated)
+        ev_up[k].record(s_up)
+        s_rn.wait_event(ev_up[k])
+        snp.render_views(he[k], cams_c, opts_async, hout[k], s_rn)
+        ev_done[k].record(s_rn)
 
-    e2e_step()
+    e2e_step(0)
+    torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
+    for i in range(e2e_steps):
+        e2e_step(i)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    snp.destroy(he)
+    for k in range(2):
+        snp.destroy(he[k])
     e2e_fps = ws * e2e_steps / mg.max_over_ranks(e2e_s, dev)
 
     # X2: gather the last frames to rank 0 once (outside the timed region)
@@ -274,7 +290,9 @@ def run_snp(args):
             "e2e": {"value": round(e2e_fps, 3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "what": "per step: snp_update_scene from pinned host arrays (H2D + device validation) + "
-                            "snp_render_views into a pinned host frame (D2H); wall clock"},
+                            "snp_render_views into a pinned host frame (SNP_MEM_HOST_ASYNC D2H); two scene "
+                            "handles alternate so that one step's upload overlaps the previous step's render "
+                            "and read-back; wall clock"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }

@@ -57,7 +57,10 @@ typedef enum {
 
 typedef struct snp_scene_s *snp_scene;  /* opaque, owned by the library */
 
-enum { SNP_MEM_HOST = 0, SNP_MEM_DEVICE = 1 };
+/* SNP_MEM_HOST_ASYNC (snp_render output only): host memory, written by a copy
+ * enqueued on the call's stream without synchronising -- the buffer should be
+ * pinned, and is valid once the caller has synchronised that stream. */
+enum { SNP_MEM_HOST = 0, SNP_MEM_DEVICE = 1, SNP_MEM_HOST_ASYNC = 2 };
 
 /* One primitive = 99 fp32 parameters for N = 8 ("99 parameters in total";
  * P:751 "41 parameters from its 8-neuron MLP"). */
@@ -90,7 +93,7 @@ typedef struct {
     float transmittance_floor;  /* stop compositing once T < floor; 1e-4 */
     int32_t tile_row_begin;     /* image-stripe partition: only tile rows r = begin + k*stride */
     int32_t tile_row_stride;    /*   are binned/rendered; (0, 1) = whole image */
-    int32_t out_memory;         /* snp_render output: SNP_MEM_DEVICE or SNP_MEM_HOST */
+    int32_t out_memory;         /* snp_render output: SNP_MEM_DEVICE, SNP_MEM_HOST or SNP_MEM_HOST_ASYNC */
     int32_t sync_check;         /* snp_bin_sort: 1 = synchronise once to size the key buffer
                                    exactly (default); 0 = never synchronise (CUDA-graph safe):
                                    an undersized buffer is reported by snp_get_stats and the
@@ -140,8 +143,9 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
 
 /* K5 (+K6): writes out_rgba[n_views][height][width][4] fp32 (R, G, B, opacity =
  * 1 - T).  out_rgba is device memory (or host memory when opts->out_memory is
- * SNP_MEM_HOST; the call then synchronises).  Pixels outside the stripe are
- * left untouched. */
+ * SNP_MEM_HOST -- the call then synchronises -- or SNP_MEM_HOST_ASYNC -- the copy
+ * is only enqueued).  Device output: pixels outside the stripe are left untouched;
+ * host output: they are written as 0. */
 snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba, void *cuda_stream);
 
 /* Convenience: snp_project + snp_bin_sort + snp_render. */

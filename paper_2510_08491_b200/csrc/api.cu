@@ -455,15 +455,19 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     if (s->state < kBinned) return fail(SNP_ERR_BAD_STATE, "snp_render before snp_bin_sort");
     if (!(opts->transmittance_floor >= 0.f) || !(opts->transmittance_floor < 1.f))
         return fail(SNP_ERR_INVALID_ARGUMENT, "transmittance_floor must be in [0, 1)");
-    if (opts->out_memory != SNP_MEM_HOST && opts->out_memory != SNP_MEM_DEVICE)
-        return fail(SNP_ERR_INVALID_ARGUMENT, "out_memory must be SNP_MEM_HOST or SNP_MEM_DEVICE");
+    if (opts->out_memory != SNP_MEM_HOST && opts->out_memory != SNP_MEM_DEVICE &&
+        opts->out_memory != SNP_MEM_HOST_ASYNC)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "out_memory must be SNP_MEM_HOST, SNP_MEM_DEVICE or SNP_MEM_HOST_ASYNC");
+    const bool host_out = opts->out_memory != SNP_MEM_DEVICE;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const size_t out_floats = (size_t)s->n_views * s->W * s->H * 4;
     float *dout = out_rgba;
-    if (opts->out_memory == SNP_MEM_HOST) {
+    if (host_out) {
         SNP_CUDA(s->host_out_staging.ensure(out_floats));
         dout = s->host_out_staging.p;
-        SNP_CUDA(cudaMemsetAsync(dout, 0, out_floats * sizeof(float), st));
+        // pixels outside the stripe come back as 0 (every pixel is written otherwise)
+        if (s->row_begin != 0 || s->row_stride != 1)
+            SNP_CUDA(cudaMemsetAsync(dout, 0, out_floats * sizeof(float), st));
     }
     const int64_t fb_cap = std::min<int64_t>((int64_t)s->n_views * s->W * s->H, (int64_t)1 << 22);
     if (s->fallback_capacity < fb_cap) {
@@ -509,9 +513,9 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
         // (SNP_DEBUG bit 2 skips K6: timing experiments only, overflowed pixels stay unwritten)
         if (s->n > 0 && !(a.debug_flags & 2)) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
     }
-    if (opts->out_memory == SNP_MEM_HOST) {
+    if (host_out) {
         SNP_CUDA(cudaMemcpyAsync(out_rgba, dout, out_floats * sizeof(float), cudaMemcpyDeviceToHost, st));
-        SNP_CUDA(cudaStreamSynchronize(st));
+        if (opts->out_memory == SNP_MEM_HOST) SNP_CUDA(cudaStreamSynchronize(st));
     }
     return SNP_OK;
 }

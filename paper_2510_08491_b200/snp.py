@@ -22,6 +22,7 @@ STATUS = {0: "SNP_OK", 1: "SNP_ERR_INVALID_ARGUMENT", 2: "SNP_ERR_OUT_OF_MEMORY"
           4: "SNP_ERR_UNSUPPORTED", 5: "SNP_ERR_BAD_STATE", 6: "SNP_ERR_CAPACITY"}
 SNP_MEM_HOST = 0
 SNP_MEM_DEVICE = 1
+SNP_MEM_HOST_ASYNC = 2   # snp_render output only: copy enqueued on the stream, no synchronisation
 
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",

@@ -253,3 +253,29 @@ def test_stream_ordering_and_graph_capture():
         assert s["composited"] > 0 and s["capacity_overflow"] == 0
     finally:
         snp.destroy(h)
+
+
+def test_async_host_output():
+    """SNP_MEM_HOST_ASYNC: the frame lands in (pinned) host memory once the stream is
+    synchronised, bit-identical to the device output; SNP_MEM_HOST and stripes write 0
+    outside the stripe."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene, cams, bg = synth.make_config("C2", n=2000)
+    V, H, W = len(cams), cams[0].height, cams[0].width
+    ref = gpu_render(scene, cams, bg)["img"]
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        st = torch.cuda.Stream()
+        out = torch.full((V, H, W, 4), float("nan")).pin_memory()
+        snp.render_views(h, cams, snp.make_opts(bg, out_memory=snp.SNP_MEM_HOST_ASYNC), out, st)
+        st.synchronize()
+        assert np.array_equal(out.numpy(), ref)
+        part = np.full((V, H, W, 4), np.nan, np.float32)
+        snp.render_views(h, cams, snp.make_opts(bg, tile_row_begin=1, tile_row_stride=2,
+                                                out_memory=snp.SNP_MEM_HOST), part)
+        rows = np.array([(y // 16) % 2 == 1 for y in range(H)])
+        assert np.array_equal(part[:, rows], ref[:, rows]) and not part[:, ~rows].any()
+    finally:
+        snp.destroy(h)
