@@ -169,9 +169,10 @@ snp_status snp_get_binning(snp_scene s, int32_t *rects, uint32_t *depth_keys, ui
 /* Counters of the last project/bin_sort/render (synchronises the stream). */
 snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream);
 
-/* Debug readback of the raw device counters [0, n) (n <= 32; synchronises the
- * stream).  Slots >= 16 are only written by builds with -DSNP_INSTRUMENT
- * (per-warp clock64 accounting of K5); not part of the hot path. */
+/* Debug readback of the raw device counters [0, n) (n <= 48; synchronises the
+ * stream).  Slots >= 16 are only written by instrumented A/B builds (per-warp
+ * clock64 accounting); the call clears them after reading.  Not part of the hot
+ * path. */
 snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *cuda_stream);
 
 /* Test hook: caps the per-pixel pending buffer of K5 at `k` entries (1..16) so

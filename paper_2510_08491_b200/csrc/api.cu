@@ -98,6 +98,7 @@ struct snp_scene_s {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool join_pending = false;
+    bool render_dirty = false;       // a render has used the counters since the last binning
 };
 
 namespace snp {
@@ -307,7 +308,10 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
         SNP_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
         s->join_pending = false;
     }
-    SNP_CUDA(cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kNumCounters, st));
+    // (no memset: K2 moves K1a's visible count out of its accumulator and clears it; a
+    // projection that was never binned leaves it to clear here)
+    if (s->state == kProjected)
+        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntVisibleAcc, 0, sizeof(unsigned long long), st));
     ProjectArgs a{};
     fill_args(s, a);
     for (const CamBatch &cb : s->cams) SNP_CUDA(launch_bin_geom(a, cb, st));
@@ -444,6 +448,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
         s->join_pending = false;
     }
     s->state = kBinned;
+    s->render_dirty = false;
     return SNP_OK;
 }
 
@@ -475,9 +480,12 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
         SNP_CUDA(cudaMemsetAsync(s->fallback.p, 0, sizeof(unsigned long long) * (size_t)fb_cap, st));
         s->fallback_capacity = fb_cap;
     }
-    // stats, fallback queue and tile queue: one memset (contiguous counters)
-    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
-                             sizeof(unsigned long long) * (kCntK5Done - kCntTested + 1), st));
+    // stats, fallback queue, tile queue: K4 cleared them for the first render of this
+    // binning; a further render clears them with one memset (contiguous counters)
+    if (s->render_dirty)
+        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
+                                 sizeof(unsigned long long) * (kCntK5Done - kCntTested + 1), st));
+    s->render_dirty = true;
     RenderArgs a{};
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
@@ -626,6 +634,9 @@ snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *c
                              cudaMemcpyDeviceToHost, st));
     SNP_CUDA(cudaStreamSynchronize(st));
     for (int i = 0; i < n; ++i) out[i] = s->h_counters[i];
+    // the instrumented slots accumulate until read: clear them for the next measurement
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + 16, 0, sizeof(unsigned long long) * (kNumCounters - 16), st));
+    SNP_CUDA(cudaStreamSynchronize(st));
     return SNP_OK;
 }
 

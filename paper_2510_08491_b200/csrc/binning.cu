@@ -155,6 +155,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
             if (blk > 0) atomicExch(a.dup_status + blk, kStInc | (excl + tot));
             s_gbase = excl;
             if (blk == (int64_t)gridDim.x - 1) {
+                // (every block has published its aggregate, so K1a is long complete)
+                a.counters[kCntVisible] = atomicAdd(a.counters + kCntVisibleAcc, 0ull);   // (K4 clears it)
                 a.counters[kCntDup] = excl + tot;
                 a.counters[kCntCapOverflow] = excl + tot > (unsigned long long)a.capacity ? 1ull : 0ull;
             }
@@ -202,7 +204,11 @@ __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *co
                               int32_t tile_bits, int32_t tiles, uint32_t *ranges, unsigned long long *dup_status,
                               int64_t dup_blocks, uint32_t *hist, int32_t hist_words) {
     pdl_prologue();
-    // the next frame's K2 needs clean block states and digit histograms (no memset node)
+    // the first render of this binning needs clean render counters, the next frame's K2
+    // clean block states and digit histograms (no memset node)
+    if (blockIdx.x == 0 && threadIdx.x <= kCntK5Done - kCntTested)
+        const_cast<unsigned long long *>(counters)[kCntTested + threadIdx.x] = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<unsigned long long *>(counters)[kCntVisibleAcc] = 0ull;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < dup_blocks; j += (int64_t)gridDim.x * blockDim.x)
         dup_status[j] = 0ull;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < hist_words; j += (int64_t)gridDim.x * blockDim.x)
@@ -228,6 +234,8 @@ cudaError_t launch_dup(const BinArgs &a, cudaStream_t st) {
         cudaError_t e = cudaMemsetAsync(a.counters + kCntDup, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(a.counters + kCntCapOverflow, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(a.counters + kCntVisible, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
         if (a.n_slots > 0) e = cudaMemsetAsync(a.ranges, 0, sizeof(uint32_t) * 2 * (size_t)a.n_slots, st);
         return e;

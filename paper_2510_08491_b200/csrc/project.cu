@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kGeomThreads) k_bin_geom(ProjectArgs a, CamBat
     }
     // warp-aggregated visible count
     const uint32_t vb = __reduce_add_sync(0xffffffffu, (uint32_t)n_vis);
-    if ((threadIdx.x & 31) == 0 && vb) atomicAdd(a.counters + kCntVisible, (unsigned long long)vb);
+    if ((threadIdx.x & 31) == 0 && vb) atomicAdd(a.counters + kCntVisibleAcc, (unsigned long long)vb);
 }
 
 // Input validation: q nonzero, s > 0, every value finite.

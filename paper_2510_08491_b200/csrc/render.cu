@@ -649,16 +649,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         atomicAdd(a.counters + 23, (unsigned long long)ins_pre);
         atomicAdd(a.counters + 24, (unsigned long long)ins_setup);
         atomicAdd(a.counters + 25, (unsigned long long)ins_finish);
-        atomicAdd(a.counters + 12, (unsigned long long)ins_touch);
-        atomicAdd(a.counters + 13, (unsigned long long)ins_empty);
+        atomicAdd(a.counters + 37, (unsigned long long)ins_touch);
+        atomicAdd(a.counters + 38, (unsigned long long)ins_empty);
         atomicAdd(a.counters + 36, (unsigned long long)ins_steps);
     }
     {
         const unsigned long long ec = __reduce_add_sync(0xffffffffu, (uint32_t)ins_ecalls);
         const unsigned long long en = __reduce_add_sync(0xffffffffu, (uint32_t)ins_enone);
         if (lane == 0) {
-            atomicAdd(a.counters + 14, ec);
-            atomicAdd(a.counters + 15, en);
+            atomicAdd(a.counters + 39, ec);
+            atomicAdd(a.counters + 40, en);
         }
     }
 #endif

@@ -87,11 +87,14 @@ enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecW
                   kRecWh1 = 5, kRecUnits = 6, kRecW2 = 14 };
 
 // Device-side counters (one 64-bit slot each), see snp_stats.
-// The render counters kCntTested..kCntK5Done are contiguous: one memset per render.
+// The render counters kCntTested..kCntK5Done are contiguous: K4 clears them for the
+// first render after a binning (a further render of the same binning clears them with
+// one memset).  kCntVisibleAcc is K1a's accumulator, moved to kCntVisible (and cleared)
+// by K2's last block.  No memset node in a project -> bin_sort -> render frame.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
                kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
-               kCntFallbackClaim = 10, kCntK5Done = 11,
-               kNumCounters = 40 };   // 10..39: instrumented (A/B) builds only
+               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12,
+               kNumCounters = 48 };   // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
     int64_t n;

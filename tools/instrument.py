@@ -14,10 +14,11 @@ h = snp.create_scene(ns, 0)
 out = torch.empty((1, cams[0].height, cams[0].width, 4), device="cuda")
 snp.render_views(h, cams, snp.make_opts(bg, sync_check=1), out)
 opts = snp.make_opts(bg, sync_check=0)
+snp.get_debug_counters(h)   # clears the instrumented slots
 snp.render_views(h, cams, opts, out)
 torch.cuda.synchronize()
-c = snp.get_debug_counters(h, 40).astype(np.float64)
-ci = snp.get_debug_counters(h, 40)
+ci = snp.get_debug_counters(h, 48)
+c = ci.astype(np.float64)
 tot = c[21]
 names = {16: "wait", 17: "rounds", 18: "emit", 22: "fill", 23: "pre", 24: "setup", 25: "finish"}
 parts = "  ".join("%s %.1f%%" % (nm, 100 * c[k] / tot) for k, nm in names.items())
@@ -26,8 +27,8 @@ print(cfg, "consumer-warp cycles:", parts, " other %.1f%%" % (100 * other / tot)
       " rounds=%d avg_lanes=%.1f total=%.3g" % (c[19], c[20] / max(c[19], 1), tot))
 print(cfg, "producer: waiting on free slots %.1f%% of its time" % (100 * c[26] / max(c[27], 1)))
 print(cfg, "touching (warp, record) pairs %.3g, with no candidate lane %.1f%%; emit calls (lane) %.3g, with empty list %.1f%%" % (
-    c[12], 100 * c[13] / max(c[12], 1), c[14], 100 * c[15] / max(c[14], 1)))
-print(cfg, "insertion steps per round %.2f" % (c[10] / max(c[19], 1)))
+    c[37], 100 * c[38] / max(c[37], 1), c[39], 100 * c[40] / max(c[39], 1)))
+print(cfg, "insertion steps per round %.2f" % (c[36] / max(c[19], 1)))
 t0 = int(~np.uint64(ci[32])); tmax = int(ci[33]); tmean = int(ci[34]) * 1024.0 / max(int(ci[35]), 1)
 print(cfg, "CTA end times after the first start: mean %.1f us, last %.1f us (tail %.1f us)" % (
     (tmean - t0) / 1e3, (tmax - t0) / 1e3, (tmax - tmean) / 1e3))

@@ -16,6 +16,8 @@ h = snp.create_scene(ns, 0)
 opts = snp.make_opts(bg, sync_check=1)
 cc = snp.make_cameras(cams)
 for it in range(3):
+    if it == 2:
+        snp.get_debug_counters(h)   # clears the instrumented slots
     snp.project(h, cc)
     snp.bin_sort(h, opts)
     torch.cuda.synchronize()
