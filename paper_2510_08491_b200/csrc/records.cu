@@ -110,7 +110,7 @@ __device__ __forceinline__ void sh_rgb(int degree, const float4 *sh4, double xd,
     }
 }
 
-constexpr int kProjThreads = 128;
+constexpr int kProjThreads = 64;
 
 // One slice = the parameters of kProjThreads consecutive primitives, staged with
 // cp.async.bulk and reused by every view of the launch.
@@ -319,7 +319,7 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
 
 // One CTA per slice.  The slice load is issued first (its latency overlaps the
 // visibility read); a CTA whose slice has no visible primitive only waits for it.
-__global__ void __launch_bounds__(kProjThreads, 4) k_records(ProjectArgs a, CamBatch cb) {
+__global__ void __launch_bounds__(kProjThreads, 8) k_records(ProjectArgs a, CamBatch cb) {
     extern __shared__ __align__(128) unsigned char psm_raw[];
     ProjSmem &ps = *reinterpret_cast<ProjSmem *>(psm_raw);
     const int64_t i0 = (int64_t)blockIdx.x * kProjThreads;
