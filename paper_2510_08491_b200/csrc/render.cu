@@ -37,7 +37,8 @@ constexpr int kConsumers = 8;                      // consumer warps = 8x4 pixel
 constexpr int kThreads = (kConsumers + 1) * 32;    // + 1 producer warp
 constexpr int kWarps = kConsumers;
 constexpr int kBatch = 32;          // records per stage (one per producer lane)
-constexpr int kStages = 7;          // TMA ring depth (2 CTAs x ~113 KB per SM)
+constexpr int kStages = 6;          // TMA ring depth (2 CTAs x ~106 KB per SM)
+constexpr int kQueue = 128;         // per-warp candidate ring (power of two, >= 31 + 2 x 32)
 constexpr int kRecStride = 17;      // float4 per staged record (16 + 1 pad)
 constexpr int kPend = 16;           // per-pixel pending hits (sorted ring)
 static_assert((kPend & (kPend - 1)) == 0, "the pending ring needs a power of two");
@@ -61,8 +62,8 @@ struct __align__(16) Smem {
     int32_t tdone[kTileRing];                 // consumer warps finished with tile seq % kTileRing
     int32_t next_tile;
     int32_t warps_done;                       // warps of this CTA that have finished (K5 exit signal)
-    uint8_t qj[kWarps][64];                   // per-warp compaction queue of candidate pairs
-    uint8_t ql[kWarps][64];                   //   (record slot j, owner lane), a ring from qhead
+    uint8_t qj[kWarps][kQueue];               // per-warp compaction queue of candidate pairs
+    uint8_t ql[kWarps][kQueue];               //   (record slot j, owner lane), a ring from qhead
     float p_thi[kPend][kWarps * 32];          // pending hits, one column per pixel, kept sorted by
                                               // (t_in, id) in a ring starting at the head: t_in
                                               // (fp32: its 6e-8 rounding is far below the 1e-6
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 #endif
                 __syncwarp();
                 const bool valid = lane < n;
-                const int qi = (qhead + lane) & 63;
+                const int qi = (qhead + lane) & (kQueue - 1);
                 const int owner = valid ? sm.ql[wid][qi] : lane;
                 const int j = valid ? sm.qj[wid][qi] : 0;
                 Ray ro;
@@ -570,26 +571,43 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 #ifdef SNP_INSTRUMENT
                 long long _f0 = clock64();
 #endif
+                // two records per step (independent loads and tests); the queue holds
+                // up to 31 + 2 x 32 pairs
                 while (m && qcount < 32) {
-                    const int j = __ffs(m) - 1;
+                    const int j1 = __ffs(m) - 1;
                     m &= m - 1u;
-                    jlast = j;
-                    const float4 c0 = sm.rec[slot][j][kRecConic];
-                    const float cc = sm.rec[slot][j][kRecConicRgb].x;
-                    const float dx = pxf - c0.x, dy = pyf - c0.y;
-                    const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
-                    const bool cand = !ps.done && q <= 1.0f;
-                    const uint32_t cm = __ballot_sync(0xffffffffu, cand);
-                    if (cand) {
-                        const int pos = (qhead + qcount + __popc(cm & lt_mask)) & 63;
-                        sm.qj[wid][pos] = (uint8_t)j;
+                    const int j2 = m ? __ffs(m) - 1 : j1;
+                    const bool two = m != 0u;
+                    m &= m - 1u;
+                    jlast = two ? j2 : j1;
+                    const float4 c1 = sm.rec[slot][j1][kRecConic];
+                    const float cc1 = sm.rec[slot][j1][kRecConicRgb].x;
+                    const float4 c2 = sm.rec[slot][j2][kRecConic];
+                    const float cc2 = sm.rec[slot][j2][kRecConicRgb].x;
+                    const float dx1 = pxf - c1.x, dy1 = pyf - c1.y;
+                    const float dx2 = pxf - c2.x, dy2 = pyf - c2.y;
+                    const float q1 = fmaf(cc1 * dy1, dy1, dx1 * fmaf(c1.w, dy1, c1.z * dx1));
+                    const float q2 = fmaf(cc2 * dy2, dy2, dx2 * fmaf(c2.w, dy2, c2.z * dx2));
+                    const bool cand1 = !ps.done && q1 <= 1.0f;
+                    const bool cand2 = two && !ps.done && q2 <= 1.0f;
+                    const uint32_t cm1 = __ballot_sync(0xffffffffu, cand1);
+                    const uint32_t cm2 = __ballot_sync(0xffffffffu, cand2);
+                    const int n1 = __popc(cm1);
+                    if (cand1) {
+                        const int pos = (qhead + qcount + __popc(cm1 & lt_mask)) & (kQueue - 1);
+                        sm.qj[wid][pos] = (uint8_t)j1;
                         sm.ql[wid][pos] = (uint8_t)lane;
-                        ++n_cand;
                     }
-                    qcount += __popc(cm);
+                    if (cand2) {
+                        const int pos = (qhead + qcount + n1 + __popc(cm2 & lt_mask)) & (kQueue - 1);
+                        sm.qj[wid][pos] = (uint8_t)j2;
+                        sm.ql[wid][pos] = (uint8_t)lane;
+                    }
+                    n_cand += cand1 + cand2;
+                    qcount += n1 + __popc(cm2);
 #ifdef SNP_INSTRUMENT
-                    ++ins_touch;
-                    ins_empty += (cm == 0u);
+                    ins_touch += 1 + two;
+                    ins_empty += (cm1 == 0u) + (two && cm2 == 0u);
 #endif
                 }
 #ifdef SNP_INSTRUMENT
@@ -599,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 if (qcount > 0) {
                     round(qcount < 32 ? qcount : 32);
                     rem = qcount > 32 ? qcount - 32 : 0;
-                    qhead = (qhead + 32) & 63;
+                    qhead = (qhead + 32) & (kQueue - 1);
                     // every hit this warp has not inserted yet comes from a record >= the
                     // oldest queued one (or > jlast), so that record's L bounds its t_in
                     if (rem > 0) jn = sm.qj[wid][qhead];
