@@ -299,6 +299,8 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
             std::memcpy(dc.R, c.R_wc, sizeof dc.R);
             std::memcpy(dc.C, c.C_w, sizeof dc.C);
             dc.fx = c.fx; dc.fy = c.fy; dc.cx = c.cx; dc.cy = c.cy;
+            dc.ifx = 1.0 / (double)c.fx;
+            dc.ify = 1.0 / (double)c.fy;
             dc.W = c.width; dc.H = c.height;
             dc.t_near = c.t_near; dc.t_far = c.t_far;
         }

@@ -234,7 +234,7 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
                     const double qc = kq + l0 * u0 + l1 * v0;
                     if (qc < 0.0) {
                         const double fx = cam.fx, fy = cam.fy;
-                        const double iq = -rcp64(qc), ifx = rcp64(fx), ify = rcp64(fy);
+                        const double iq = -rcp64(qc), ifx = cam.ifx, ify = cam.ify;
                         const double an = A00 * iq * (ifx * ifx);
                         const double bn = A01 * iq * (ifx * ify);
                         const double cn = A11 * iq * (ify * ify);

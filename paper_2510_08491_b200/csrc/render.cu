@@ -114,8 +114,8 @@ struct Ray {
 
 __device__ __forceinline__ Ray make_ray(const DevCam &cam, int x, int y) {
     // d = normalize(R_wc ((x+.5-cx)/fx, (y+.5-cy)/fy, 1)) in FP64 (R6), split into hi + lo
-    const double u = ((double)x + 0.5 - (double)cam.cx) * (1.0 / (double)cam.fx);
-    const double v = ((double)y + 0.5 - (double)cam.cy) * (1.0 / (double)cam.fy);
+    const double u = ((double)x + 0.5 - (double)cam.cx) * cam.ifx;
+    const double v = ((double)y + 0.5 - (double)cam.cy) * cam.ify;
     double r[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)

@@ -66,6 +66,7 @@ struct DevCam {
     float fx, fy, cx, cy;
     int32_t W, H;
     float t_near, t_far;
+    double ifx, ify;  // 1 / fx, 1 / fy (host-computed: no FP64 division per pixel ray)
 };
 
 struct CamBatch {
