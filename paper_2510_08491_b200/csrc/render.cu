@@ -42,8 +42,6 @@ constexpr int kQueue = 128;         // per-warp candidate ring (power of two, >=
 constexpr int kRecStride = 17;      // float4 per staged record (16 + 1 pad)
 constexpr int kPend = 16;           // per-pixel pending hits (sorted ring)
 static_assert((kPend & (kPend - 1)) == 0, "the pending ring needs a power of two");
-constexpr int kCountMask = 0xff;    // p_nh: pending count (bits 0-7), overflow flag (bit 8), head (16+)
-constexpr int kOvf = 0x100;
 constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
 
 struct __align__(16) Smem {
@@ -70,8 +68,7 @@ struct __align__(16) Smem {
                                               // near-tie flag of R23), kappa, primitive id
     float p_kap[kPend][kWarps * 32];
     uint32_t p_id[kPend][kWarps * 32];
-    int32_t p_nh[kWarps * 32];                // pending count | kOvf | ring slot of the smallest pending
-                                              // hit << 16 (one load for the inserting lanes)
+    uint32_t p_in[kWarps * 32];               // per owner pixel: lanes holding a hit for it this round
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -215,6 +212,15 @@ __device__ __forceinline__ bool before(float ah, float al, uint32_t aid, float b
     return ah < bh || (ah == bh && (al < bl || (al == bl && aid < bid)));
 }
 
+// The owner lane's view of its pixel's pending ring (the entries live in shared
+// memory, column tid; count, head and the largest entry are kept in registers).
+struct Pending {
+    int n, head;
+    float tail_t;
+    uint32_t tail_id;
+    bool ovf;
+};
+
 struct PixelState {
     float T, cr, cg, cb;
     bool done;
@@ -226,11 +232,11 @@ struct PixelState {
 // (strictly): every hit not yet inserted has t_in >= L (R19), so these are
 // exactly the next hits of the ray in (t_in, id) order (Eq. 4).  The
 // list is sorted, so they are popped from its head.
-__device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_floor, const float4 *recs) {
+__device__ __forceinline__ void emit(Smem &sm, PixelState &ps, Pending &pd, float L, float t_floor,
+                                     const float4 *recs) {
     const int tid = threadIdx.x;
-    const int nh = sm.p_nh[tid];
-    int n = nh & kCountMask;
-    int h = nh >> 16;
+    int n = pd.n;
+    int h = pd.head;
     while (n > 0) {
         const float t = sm.p_thi[h][tid];
         if (!(t < L)) break;
@@ -249,7 +255,41 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, float L, float t_
             break;
         }
     }
-    sm.p_nh[tid] = n | (nh & kOvf) | (h << 16);
+    pd.n = n;
+    pd.head = h;
+}
+
+// Owner-local sorted insertion of one hit into this lane's pending ring: appended
+// when it is the largest (t_in, id) so far (the usual case: records stream in L
+// order), else shifted into place.  A full ring drops the hit and marks the pixel.
+__device__ __forceinline__ void insert_local(Smem &sm, Pending &pd, int plimit, float tn, float kn, uint32_t in) {
+    const int tid = threadIdx.x;
+    if (pd.n >= plimit) {
+        pd.ovf = true;
+        return;
+    }
+    int k = pd.n;
+    if (k == 0 || pd.tail_t < tn || (pd.tail_t == tn && pd.tail_id < in)) {
+        pd.tail_t = tn;
+        pd.tail_id = in;
+    } else {
+        while (k > 0) {
+            const int sp = (pd.head + k - 1) & (kPend - 1);
+            const float tp = sm.p_thi[sp][tid];
+            const uint32_t ip = sm.p_id[sp][tid];
+            if (!(tn < tp || (tn == tp && in < ip))) break;
+            const int sd = (pd.head + k) & (kPend - 1);
+            sm.p_thi[sd][tid] = tp;
+            sm.p_kap[sd][tid] = sm.p_kap[sp][tid];
+            sm.p_id[sd][tid] = ip;
+            --k;
+        }
+    }
+    const int sd = (pd.head + k) & (kPend - 1);
+    sm.p_thi[sd][tid] = tn;
+    sm.p_kap[sd][tid] = kn;
+    sm.p_id[sd][tid] = in;
+    ++pd.n;
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
@@ -389,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     // =============================== consumer warps
 #ifdef SNP_INSTRUMENT
     long long ins_wait = 0, ins_round = 0, ins_emit = 0, ins_rounds = 0, ins_lanes = 0, ins_fill = 0, ins_pre = 0,
-              ins_setup = 0, ins_finish = 0, ins_touch = 0, ins_empty = 0, ins_ecalls = 0, ins_enone = 0, ins_steps = 0;
+              ins_setup = 0, ins_finish = 0, ins_touch = 0, ins_empty = 0, ins_ecalls = 0, ins_enone = 0, ins_steps = 0, ins_ins = 0;
     const long long ins_start = clock64();
 #endif
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
@@ -406,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     Ray ray{0, 0, 1, 0, 0, 0, 0, 0};
     float pxf = 0.f, pyf = 0.f, bx0 = 0.f, by0 = 0.f;
     PixelState ps{1.f, 0.f, 0.f, 0.f, true, false, 0u};
+    Pending pd{0, 0, 0.f, 0u, false};
 
     auto finish_tile = [&]() {   // write this warp's pixels; count the warp as done with the tile
         if (inside) {
@@ -462,7 +503,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             bx0 = (float)bx + 0.5f;
             by0 = (float)by + 0.5f;
             ps = PixelState{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
-            sm.p_nh[tid] = 0;
+            pd = Pending{0, 0, 0.f, 0u, false};
+            sm.p_in[tid] = 0u;
             tile_finished = false;
         }
 #ifdef SNP_INSTRUMENT
@@ -519,47 +561,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 float th = 0.f, tl = 0.f, kap = 0.f;
                 if (valid) hit = exact_hit(&sm.rec[slot][j][0], ro, th, tl, kap);
                 n_hit += hit;
-                // insert each hit into its owner's sorted pending ring; the hits of one
-                // owner in this round go in one at a time (peer rank order).  Records
-                // stream in L order, so a new hit usually lands at the tail (one compare).
-                const uint32_t peers = __match_any_sync(0xffffffffu, hit ? owner : 64 + lane);
-                const int ot = wid * 32 + owner;
-                const int rank = __popc(peers & lt_mask);
-                const int steps = __reduce_max_sync(0xffffffffu, hit ? (uint32_t)rank + 1u : 0u);
+#ifdef SNP_INSTRUMENT
+                long long _i0 = clock64();
+#endif
+                // route every hit to its owner pixel's lane, which inserts it into its
+                // own sorted ring: each hitting lane adds its bit to the owner's mask; the
+                // owner then fetches its hits one per step by shuffle (no cross-lane
+                // writes to a ring, no dependent shared-memory round trips per step)
                 const uint32_t idn = hit ? sm.id[slot][j] : 0u;
+                if (hit) atomicOr(&sm.p_in[wid * 32 + owner], 1u << lane);
+                __syncwarp();
+                uint32_t inc = sm.p_in[tid];
+                sm.p_in[tid] = 0u;
+                const int steps = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(inc));
 #ifdef SNP_INSTRUMENT
                 ins_steps += steps;
 #endif
                 for (int r = 0; r < steps; ++r) {
-                    if (hit && rank == r) {
-                        const int nh = sm.p_nh[ot];
-                        const int n = nh & kCountMask;
-                        if (n >= plimit) {
-                            sm.p_nh[ot] = nh | kOvf;   // dropped: the pixel goes to K6
-                        } else {
-                            const int hd = nh >> 16;
-                            int k = n;
-                            while (k > 0) {
-                                const int sp = (hd + k - 1) & (kPend - 1);
-                                const float tp = sm.p_thi[sp][ot];
-                                const uint32_t ip = sm.p_id[sp][ot];
-                                if (!(th < tp || (th == tp && idn < ip))) break;
-                                const int sd = (hd + k) & (kPend - 1);
-                                sm.p_thi[sd][ot] = tp;
-                                sm.p_kap[sd][ot] = sm.p_kap[sp][ot];
-                                sm.p_id[sd][ot] = ip;
-                                --k;
-                            }
-                            const int sd = (hd + k) & (kPend - 1);
-                            sm.p_thi[sd][ot] = th;
-                            sm.p_kap[sd][ot] = kap;
-                            sm.p_id[sd][ot] = idn;
-                            sm.p_nh[ot] = nh + 1;
-                        }
+                    const int src = inc ? __ffs(inc) - 1 : lane;
+                    const float tn = __shfl_sync(0xffffffffu, th, src);
+                    const float kn = __shfl_sync(0xffffffffu, kap, src);
+                    const uint32_t in = __shfl_sync(0xffffffffu, idn, src);
+                    if (inc) {
+                        inc &= inc - 1u;
+                        insert_local(sm, pd, plimit, tn, kn, in);
                     }
-                    __syncwarp();
                 }
 #ifdef SNP_INSTRUMENT
+                ins_ins += clock64() - _i0;
                 ins_round += clock64() - _r0;
 #endif
             };
@@ -624,19 +653,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     qcount = rem;
                 }
                 const bool batch_end = (m == 0u) && rem == 0;
-                if (!ps.done && (sm.p_nh[tid] & kOvf)) {   // a hit was dropped: nothing may be blended
+                if (!ps.done && pd.ovf) {   // a hit was dropped: nothing may be blended
                     ps.overflow = true;
                     ps.done = true;
                 }
                 // batch end: everything in later batches has t_in >= L of the next key;
                 // mid-batch: only when the pending list runs full
-                if (!ps.done && (batch_end || (sm.p_nh[tid] & kCountMask) > plimit - 4)) {
+                if (!ps.done && (batch_end || pd.n > plimit - 4)) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
                     ++ins_ecalls;
-                    ins_enone += ((sm.p_nh[tid] & kCountMask) == 0);
+                    ins_enone += (pd.n == 0);
 #endif
-                    emit(sm, ps, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                    emit(sm, ps, pd, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
                          a.t_floor, recs);
 #ifdef SNP_INSTRUMENT
                     ins_emit += clock64() - _e0;
@@ -670,6 +699,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         atomicAdd(a.counters + 37, (unsigned long long)ins_touch);
         atomicAdd(a.counters + 38, (unsigned long long)ins_empty);
         atomicAdd(a.counters + 36, (unsigned long long)ins_steps);
+        atomicAdd(a.counters + 41, (unsigned long long)ins_ins);
     }
     {
         const unsigned long long ec = __reduce_add_sync(0xffffffffu, (uint32_t)ins_ecalls);

@@ -32,3 +32,4 @@ print(cfg, "insertion steps per round %.2f" % (c[36] / max(c[19], 1)))
 t0 = int(~np.uint64(ci[32])); tmax = int(ci[33]); tmean = int(ci[34]) * 1024.0 / max(int(ci[35]), 1)
 print(cfg, "CTA end times after the first start: mean %.1f us, last %.1f us (tail %.1f us)" % (
     (tmean - t0) / 1e3, (tmax - t0) / 1e3, (tmax - tmean) / 1e3))
+print(cfg, "insertion share of the rounds %.1f%%" % (100 * c[41] / max(c[17], 1)))
