@@ -166,15 +166,20 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
     const float bx = fmaf(w0.y, pz, fmaf(w0.x, py, ml.w * px));
     const float by = fmaf(w1.x, pz, fmaf(w0.w, py, w0.z * px));
     const float bz = fmaf(w1.w, pz, fmaf(w1.z, py, w1.y * px));
+    // roots about the ray's closest approach to the centre in the unit-sphere metric,
+    // tau* = -(a.b)/|a|^2, from the perpendicular offset b_perp = b + tau* a (one FMA
+    // per component): 1 - |b_perp|^2 is O(1) accurate even for needle- or sheet-like
+    // ellipsoids, where B^2 - AC cancels catastrophically in fp32
     const float A = fmaf(az, az, fmaf(ay, ay, ax * ax));
     const float B = fmaf(az, bz, fmaf(ay, by, ax * bx));
-    const float Cq = fmaf(bz, bz, fmaf(by, by, bx * bx)) - 1.0f;
-    const float disc = fmaf(B, B, -A * Cq);
-    if (!(disc > 0.0f)) return false;
-    const float sq = disc * rsqrtf(disc);
-    const float qq = -(B + copysignf(sq, B));
-    float t0 = qq * rcp_fast(A), t1 = Cq * rcp_fast(qq);
-    if (t0 > t1) { const float t = t0; t0 = t1; t1 = t; }
+    const float iA = rcp_fast(A);
+    const float ts = -B * iA;
+    const float qx = fmaf(ts, ax, bx), qy = fmaf(ts, ay, by), qz = fmaf(ts, az, bz);
+    const float q1 = 1.0f - fmaf(qz, qz, fmaf(qy, qy, qx * qx));
+    if (!(q1 > 0.0f)) return false;
+    const float hq = q1 * iA;
+    const float hc = hq * rsqrtf(hq);   // half chord
+    const float t0 = ts - hc, t1 = ts + hc;
     const float lo_lim = r.t_near - tc, hi_lim = r.t_far - tc;
     const bool clipped = !(t0 > lo_lim);
     const float tlo = clipped ? lo_lim : t0;

@@ -279,3 +279,33 @@ def test_async_host_output():
         assert np.array_equal(part[:, rows], ref[:, rows]) and not part[:, ~rows].any()
     finally:
         snp.destroy(h)
+
+
+def test_degenerate_primitives_and_clipping(orc):
+    """Needle- and sheet-like ellipsoids (axis ratios up to 1e3), a primitive covering
+    most of the image, zero-density and near-opaque primitives, primitives cut by
+    t_near and by t_far, an off-centre principal point and fx != fy: every pixel
+    against the oracle (P:298-299 clipping, Eq. 9 clamp, Eq. 4 termination)."""
+    rng = np.random.default_rng(11)
+    base = synth.make_scene(12, 240, box=0.8)
+    m = base.n
+    sc = base.subset(np.arange(m))
+    k = rng.permutation(m)
+    thin, sheet, zero, opaque = k[:30], k[30:60], k[60:90], k[90:120]
+    sc.scales[thin] = np.stack([np.full(30, 4e-4), np.full(30, 0.4), np.full(30, 3e-4)], 1).astype(np.float32)
+    sc.scales[sheet] = np.stack([np.full(30, 0.35), np.full(30, 0.3), np.full(30, 5e-4)], 1).astype(np.float32)
+    sc.w2[zero] = 0.0
+    sc.b2[zero] = 0.0
+    sc.b2[opaque] = (40.0 / sc.scales[opaque].max(1)).astype(np.float32)
+    big = synth.make_scene(13, 1, box=0.1)
+    big.centers[:] = 0.0
+    big.scales[:] = np.float32([[1.1, 0.9, 0.7]])
+    big.b2[:] = np.float32([0.05])
+    sc = synth.concat_scenes(sc, big)
+    cam = synth.look_at((0.0, -2.6, 0.9), (0.1, 0.0, 0.0), 83, 61, 70.0, fy=55.0, cx=30.3, cy=35.7,
+                        t_near=1.9, t_far=3.3)
+    res = gpu_render(sc, [cam], (0.1, 0.2, 0.3))
+    img_o, fl, _ = orc.render_frame(sc, cam, (0.1, 0.2, 0.3))
+    c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+    assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
+    assert res["stats"]["composited"] > 0
