@@ -309,3 +309,32 @@ def test_degenerate_primitives_and_clipping(orc):
     c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
     assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
     assert res["stats"]["composited"] > 0
+
+
+@pytest.mark.parametrize("omega", [1.0, 10.0])
+def test_other_omega(orc, omega):
+    """omega is a scene parameter (P:394 uses 30; P:664-675 studies 1 and 10): the
+    phase scaling of K1b's units and the oracle's Eq. 8 agree for other values."""
+    scene, cams, bg = synth.make_config("C1")
+    scene.omega = omega
+    res = gpu_render(scene, cams, bg)
+    img_o, fl, _ = orc.render_frame(scene, cams[0], bg)
+    c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+    assert c["max_unflagged"] <= TOL, c
+
+
+def test_subpixel_primitives_far_away(orc):
+    """Primitives smaller than a pixel at large depth: the pixel-centre rect (1/256 px
+    slack) and the conic margin must not drop their hits."""
+    rng = np.random.default_rng(21)
+    sc = synth.make_scene(22, 400, box=0.8)
+    d = np.stack([rng.uniform(-0.13, 0.13, 400), -np.ones(400), rng.uniform(-0.11, 0.11, 400)], 1)
+    sc.centers[:] = (d * rng.uniform(20, 60, (400, 1))).astype(np.float32)
+    sc.scales[:] = rng.uniform(0.005, 0.04, (400, 3)).astype(np.float32)
+    sc.b2[:] = (2.0 / sc.scales.max(1)).astype(np.float32)
+    cam = synth.look_at((0.0, 0.0, 0.0), (0.0, -1.0, 0.0), 96, 80, 400.0)
+    res = gpu_render(sc, [cam])
+    img_o, fl, _ = orc.render_frame(sc, cam)
+    c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+    assert c["max_unflagged"] <= TOL, c
+    assert (img_o[..., 3] > 1e-3).sum() > 50   # the test does see primitives
