@@ -70,7 +70,8 @@ int orc_quat_to_rot(const double q[4], double R[9])
 {
     double nq = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
     if (!(nq > 0.0)) return -1;
-    double w = q[0] / nq, x = q[1] / nq, y = q[2] / nq, z = q[3] / nq;
+    double inq = 1.0 / nq;   /* one division (binning definition) */
+    double w = q[0] * inq, x = q[1] * inq, y = q[2] * inq, z = q[3] * inq;
     R[0] = 1.0 - 2.0 * (y * y + z * z);
     R[1] = 2.0 * (x * y - w * z);
     R[2] = 2.0 * (x * z + w * y);
@@ -545,15 +546,16 @@ int orc_bin_one(const double mu[3], const double qin[4], const double s[3], cons
         double discx = bx * bx - a * cxq;
         if (!(discx > 0.0)) discx = 0.0;
         double rx = sqrt(discx);
-        xlo = cam->fx * ((bx - rx) / a) + cam->cx;
-        xhi = cam->fx * ((bx + rx) / a) + cam->cx;
+        double ia = 1.0 / a;
+        xlo = cam->fx * ((bx - rx) * ia) + cam->cx;
+        xhi = cam->fx * ((bx + rx) * ia) + cam->cx;
         double by = m[1] * m[2] - S[5];
         double cyq = m[1] * m[1] - S[4];
         double discy = by * by - a * cyq;
         if (!(discy > 0.0)) discy = 0.0;
         double ry = sqrt(discy);
-        ylo = cam->fy * ((by - ry) / a) + cam->cy;
-        yhi = cam->fy * ((by + ry) / a) + cam->cy;
+        ylo = cam->fy * ((by - ry) * ia) + cam->cy;
+        yhi = cam->fy * ((by + ry) * ia) + cam->cy;
     }
     double px0 = ceil(xlo - 0.5 - ORC_EPS_PX), px1 = floor(xhi - 0.5 + ORC_EPS_PX);
     double py0 = ceil(ylo - 0.5 - ORC_EPS_PX), py1 = floor(yhi - 0.5 + ORC_EPS_PX);

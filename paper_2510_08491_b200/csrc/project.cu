@@ -21,7 +21,8 @@ __device__ __forceinline__ bool quat_rot(const float *q4, double R[9]) {
     double q0 = q4[0], q1 = q4[1], q2 = q4[2], q3 = q4[3];
     double nq = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
     if (!(nq > 0.0)) return false;
-    double w = q0 / nq, x = q1 / nq, y = q2 / nq, z = q3 / nq;
+    double inq = 1.0 / nq;   // one division (binning definition)
+    double w = q0 * inq, x = q1 * inq, y = q2 * inq, z = q3 * inq;
     R[0] = 1.0 - 2.0 * (y * y + z * z);
     R[1] = 2.0 * (x * y - w * z);
     R[2] = 2.0 * (x * z + w * y);
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kGeomThreads) k_bin_geom(ProjectArgs a, CamBat
                 const double Wd = (double)cam.W, Hd = (double)cam.H;
                 const double pn[4][3] = {{fx, 0.0, cx}, {-fx, 0.0, Wd - cx}, {0.0, fy, cy}, {0.0, -fy, Hd - cy}};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 4 && keep; ++k) {
                     const double *nn = pn[k];
                     double dot = nn[0] * m[0] + nn[1] * m[1] + nn[2] * m[2];
                     double quad = nn[0] * (nn[0] * S[0] + nn[1] * S[1] + nn[2] * S[2])
@@ -117,15 +118,16 @@ __global__ void __launch_bounds__(kGeomThreads) k_bin_geom(ProjectArgs a, CamBat
                         double discx = bx * bx - aq * cxq;
                         if (!(discx > 0.0)) discx = 0.0;
                         double rx = sqrt(discx);
-                        xlo = fx * ((bx - rx) / aq) + cx;
-                        xhi = fx * ((bx + rx) / aq) + cx;
+                        const double iaq = 1.0 / aq;
+                        xlo = fx * ((bx - rx) * iaq) + cx;
+                        xhi = fx * ((bx + rx) * iaq) + cx;
                         double by = m[1] * m[2] - S[5];
                         double cyq = m[1] * m[1] - S[4];
                         double discy = by * by - aq * cyq;
                         if (!(discy > 0.0)) discy = 0.0;
                         double ry = sqrt(discy);
-                        ylo = fy * ((by - ry) / aq) + cy;
-                        yhi = fy * ((by + ry) / aq) + cy;
+                        ylo = fy * ((by - ry) * iaq) + cy;
+                        yhi = fy * ((by + ry) * iaq) + cy;
                     }
                     const double eps = 1.0 / 256.0;
                     double px0 = ceil(xlo - 0.5 - eps), px1 = floor(xhi - 0.5 + eps);
