@@ -525,7 +525,8 @@ int orc_bin_one(const double mu[3], const double qin[4], const double s[3], cons
     double sz = sqrt(S[8]);
     double zmin = m[2] - sz, zmax = m[2] + sz;
     if (!(zmax > 0.0)) return 0;
-    /* exact frustum side-plane cull: n.m + sqrt(n^T S n) < 0 */
+    /* exact frustum side-plane cull: n.m + sqrt(n^T S n) < 0, evaluated without the
+       square root as n.m < 0 && (n.m)^2 > n^T S n (binning definition) */
     const double Wd = (double)cam->width, Hd = (double)cam->height;
     const double pn[4][3] = {{cam->fx, 0.0, cam->cx}, {-cam->fx, 0.0, Wd - cam->cx},
                              {0.0, cam->fy, cam->cy}, {0.0, -cam->fy, Hd - cam->cy}};
@@ -535,7 +536,7 @@ int orc_bin_one(const double mu[3], const double qin[4], const double s[3], cons
         double quad = nn[0] * (nn[0] * S[0] + nn[1] * S[1] + nn[2] * S[2])
                     + nn[1] * (nn[0] * S[3] + nn[1] * S[4] + nn[2] * S[5])
                     + nn[2] * (nn[0] * S[6] + nn[1] * S[7] + nn[2] * S[8]);
-        if (dot + sqrt(quad) < 0.0) return 0;
+        if (dot < 0.0 && dot * dot > quad) return 0;
     }
     /* silhouette bbox from the tangent planes through the camera centre */
     double xlo = -INFINITY, xhi = INFINITY, ylo = -INFINITY, yhi = INFINITY;

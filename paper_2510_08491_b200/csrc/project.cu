@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kGeomThreads) k_bin_geom(ProjectArgs a, CamBat
                     double quad = nn[0] * (nn[0] * S[0] + nn[1] * S[1] + nn[2] * S[2])
                                 + nn[1] * (nn[0] * S[3] + nn[1] * S[4] + nn[2] * S[5])
                                 + nn[2] * (nn[0] * S[6] + nn[1] * S[7] + nn[2] * S[8]);
-                    if (dot + sqrt(quad) < 0.0) keep = false;
+                    if (dot < 0.0 && dot * dot > quad) keep = false;   // n.m + sqrt(n^T S n) < 0
                 }
                 if (keep) {
                     double xlo = -INFINITY, xhi = INFINITY, ylo = -INFINITY, yhi = INFINITY;
