@@ -422,7 +422,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     sc.max_partitions = s->sort_max_partitions;
     int final_idx = 0;
     SNP_CUDA(launch_onesweep(s->keys0.p, s->vals0.p, s->keys1.p, s->vals1.p, s->key_capacity, s->counters.p,
-                             passes, sc, true, s->known_ndup + s->known_ndup / 8, st, &final_idx));
+                             passes, sc, s->known_ndup + s->known_ndup / 8, st, &final_idx));
     s->sorted_idx = final_idx;
     const uint64_t *sk = final_idx ? s->keys1.p : s->keys0.p;
     // K4

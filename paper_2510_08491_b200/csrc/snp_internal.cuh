@@ -156,10 +156,8 @@ size_t sort_scratch_words(int passes, int64_t max_partitions);
 // [0, 8*passes).  Ping-pongs between (k0,v0) and (k1,v1); returns in *final_idx
 // which buffer (0 or 1) holds the result.  expected_n (the last host-known key
 // count, or 0) only sizes the persistent grid.
-// hist_ready: the digit histograms were already accumulated (by the key
-// duplication kernel, zeroed before it); otherwise a histogram pass runs first.
 cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
-                            const unsigned long long *counters, int passes, SortScratch scratch, bool hist_ready,
+                            const unsigned long long *counters, int passes, SortScratch scratch,
                             int64_t expected_n, cudaStream_t st, int *final_idx);
 
 struct RenderArgs {

@@ -3,13 +3,14 @@
 // LSD radix sort over 64-bit tile|depth keys").  Realises the tile-granular
 // part of "depth-sorted"; the exact per-ray order is restored in K5.
 //
-// Structure (one global histogram pass + one pass per digit):
-//   k_hist   : all digit histograms in one read of the keys (smem atomics)
-//   k_pass   : per partition of kPart keys (partition id from an atomic ticket,
-//              so every lower partition is already resident -> forward
-//              progress on sm_100a); warp-level match-any ranking (stable),
-//              decoupled look-back over partitions per digit, smem shuffle to
-//              block-sorted order, then coalesced-run scatter.
+// Structure: the digit histograms of every pass are accumulated by K2 while it
+// duplicates the keys; then one k_pass launch per 8-bit digit (LSD first):
+//   k_pass : persistent CTAs (grid <= resident CTAs, partition c, c + G, ... in
+//            order, so every partition a look-back waits on is resident); per
+//            partition of kPart keys: stable warp ranking from 8 ballots, per-digit
+//            decoupled look-back over the earlier partitions (windows of 24 loads),
+//            shuffle into block-sorted order in shared memory, coalesced-run scatter.
+//            Each pass also clears the look-back region of the next one.
 #include "snp_internal.cuh"
 
 namespace snp {
@@ -27,24 +28,6 @@ constexpr uint32_t kValMask = (1u << 30) - 1u;
 __device__ __forceinline__ int64_t sort_n(const unsigned long long *counters, int64_t capacity) {
     int64_t n = (int64_t)counters[kCntDup];
     return n > capacity ? capacity : n;
-}
-
-__global__ void __launch_bounds__(kThreads) k_hist(const uint64_t *keys, int64_t capacity,
-                                                   const unsigned long long *counters, int passes,
-                                                   uint32_t *hist) {
-    __shared__ uint32_t h[8][256];
-    for (int i = threadIdx.x; i < passes * 256; i += kThreads) h[i >> 8][i & 255] = 0;
-    __syncthreads();
-    const int64_t n = sort_n(counters, capacity);
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
-        const uint64_t k = keys[i];
-        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < passes * 256; i += kThreads) {
-        uint32_t v = h[i >> 8][i & 255];
-        if (v) atomicAdd(&hist[i], v);
-    }
 }
 
 #ifdef SNP_SORT_INSTRUMENT
@@ -259,7 +242,7 @@ size_t sort_scratch_words(int passes, int64_t max_partitions) {
 }
 
 cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, int64_t capacity,
-                            const unsigned long long *counters, int passes, SortScratch sc, bool hist_ready,
+                            const unsigned long long *counters, int passes, SortScratch sc,
                             int64_t expected_n, cudaStream_t st, int *final_idx) {
     *final_idx = 0;
     if (capacity == 0 || passes == 0) return cudaSuccess;
@@ -274,15 +257,6 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
         resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
     }
     cudaError_t e;
-    if (!hist_ready) {
-        e = cudaMemsetAsync(sc.hist, 0, sizeof(uint32_t) * 256 * passes, st);
-        if (e != cudaSuccess) return e;
-    }
-    if (!hist_ready) {
-        int64_t hb = (capacity + kThreads * 16 - 1) / (kThreads * 16);
-        if (hb > 148 * 4) hb = 148 * 4;
-        k_hist<<<(unsigned)hb, kThreads, 0, st>>>(k0, capacity, counters, passes, sc.hist);
-    }
     // persistent partitions: any grid size is correct; size it for the expected key
     // count so that idle CTAs do not hold SM slots that concurrent work (K1b) could use
     int64_t want = expected_n > 0 ? (expected_n + kPart - 1) / kPart : maxp;
