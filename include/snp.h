@@ -17,12 +17,16 @@
  *
  * Pipeline (each call asynchronous on the caller's CUDA stream):
  *   snp_create_scene  copy + validate primitives           (a1 ingest)
- *   snp_project       K1 project/cull per (view, primitive) (a2)
- *   snp_bin_sort      K2 count/scan/duplicate keys, K3 onesweep radix sort,
- *                     K4 tile ranges                          (a3-a5)
+ *   snp_project       K1a project/cull + tile rect + depth key per (view,
+ *                     primitive); K1b render records, forked onto the scene's
+ *                     internal stream                      (a2)
+ *   snp_bin_sort      K2 one-pass key duplication, K3 onesweep radix sort,
+ *                     K4 tile ranges, tile order; joins K1b (a3-a5)
  *   snp_render        K5 per-pixel integral + blend, K6 exact fallback (a6)
  *   snp_destroy
- * Stages must run in this order; re-projecting invalidates later stages.
+ * Stages must run in this order; re-projecting invalidates later stages.  The
+ * fork/join of K1b uses events, so a sequence of calls on one stream may be
+ * captured into a CUDA graph (snp_bin_sort with sync_check = 0).
  *
  * Conventions: all arrays are fp32, row-major, structure-of-arrays over
  * primitives.  Quaternions are (w,x,y,z), normalised on read (R8); scales are
@@ -52,7 +56,7 @@ typedef enum {
     SNP_ERR_CUDA = 3,
     SNP_ERR_UNSUPPORTED = 4,       /* e.g. n_hidden != 8 (P:394 default; other widths are future work) */
     SNP_ERR_BAD_STATE = 5,         /* stage called out of order */
-    SNP_ERR_CAPACITY = 6           /* key buffer too small in no-sync mode (see snp_render_opts.sync_check) */
+    SNP_ERR_CAPACITY = 6           /* reserved (no-sync capacity overflow is reported by snp_get_stats) */
 } snp_status;
 
 typedef struct snp_scene_s *snp_scene;  /* opaque, owned by the library */
@@ -96,8 +100,9 @@ typedef struct {
     int32_t out_memory;         /* snp_render output: SNP_MEM_DEVICE, SNP_MEM_HOST or SNP_MEM_HOST_ASYNC */
     int32_t sync_check;         /* snp_bin_sort: 1 = synchronise once to size the key buffer
                                    exactly (default); 0 = never synchronise (CUDA-graph safe):
-                                   an undersized buffer is reported by snp_get_stats and the
-                                   next snp_bin_sort returns SNP_ERR_CAPACITY */
+                                   keys beyond an undersized buffer are dropped (the frame is
+                                   then incomplete) and snp_get_stats reports
+                                   capacity_overflow = 1; a call with 1 resizes */
 } snp_render_opts;
 
 typedef struct {
