@@ -338,3 +338,35 @@ def test_subpixel_primitives_far_away(orc):
     c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
     assert c["max_unflagged"] <= TOL, c
     assert (img_o[..., 3] > 1e-3).sum() > 50   # the test does see primitives
+
+
+def test_fallback_pixels_full_size_C5(orc, monkeypatch):
+    """The pixels K5 hands to K6 at full C5 size (found by rendering once with K6
+    disabled: they stay unwritten), checked one by one against the oracle."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene, cams, bg = synth.make_config("C5")
+    V, H, W = 1, cams[0].height, cams[0].width
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        out = torch.full((V, H, W, 4), float("nan"), device="cuda")
+        monkeypatch.setenv("SNP_DEBUG", "2")          # skip K6
+        snp.render_views(h, cams, snp.make_opts(bg), out)
+        torch.cuda.synchronize()
+        miss = torch.isnan(out[0, ..., 3]).nonzero().cpu().numpy()
+        n_ovf = snp.get_stats(h)["overflow_pixels"]
+        assert len(miss) == n_ovf > 0
+        monkeypatch.delenv("SNP_DEBUG")
+        out.fill_(float("nan"))
+        snp.render_views(h, cams, snp.make_opts(bg, sync_check=0), out)
+        torch.cuda.synchronize()
+        img = out[0].cpu().numpy()
+    finally:
+        snp.destroy(h)
+    assert not np.isnan(img).any()
+    sel = miss[np.random.default_rng(3).permutation(len(miss))[:200]]
+    py, px = sel[:, 0].astype(np.int64), sel[:, 1].astype(np.int64)
+    out_o, fl, _ = orc.render_pixels(scene, cams[0], px, py, bg)
+    c = compare(img[py, px], out_o, fl)
+    assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.1 * c["n"], c
