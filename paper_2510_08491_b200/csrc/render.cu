@@ -528,8 +528,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 const float hb = 0.5f * c0.w;
                 const float det = fmaf(c0.z, cc, -hb * hb);
                 if (det > 0.f) {
-                    const float rx = sqrtf(cc / det) * 1.001f + 1e-3f;
-                    const float ry = sqrtf(c0.z / det) * 1.001f + 1e-3f;
+                    // half extents of the conic's bounding box, with a 0.1% + 1e-3 px margin
+                    // (which also covers the approximate reciprocal and square roots)
+                    const float rdet = rcp_fast(det);
+                    const float rx = __fsqrt_rn(cc * rdet) * 1.001f + 1e-3f;
+                    const float ry = __fsqrt_rn(c0.z * rdet) * 1.001f + 1e-3f;
                     touch = c0.x + rx >= bx0 && c0.x - rx <= bx0 + 7.0f && c0.y + ry >= by0 &&
                             c0.y - ry <= by0 + 3.0f;
                 } else {
