@@ -285,7 +285,7 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
     s->view_bits = bits_for(n_views);
     if (kDepthBits + s->tile_bits + s->view_bits > 64) return fail(SNP_ERR_UNSUPPORTED, "key exceeds 64 bits");
     const size_t items = (size_t)n_views * (size_t)s->n;
-    SNP_CUDA(s->rects.ensure(items));
+    SNP_CUDA(s->rects.ensure(items + 2));   // (+2: K1b bulk-copies rect rows rounded up to 16 bytes)
     SNP_CUDA(s->depth.ensure(items));
     SNP_CUDA(s->records.ensure(items * 16));
     s->cams.clear();

@@ -126,6 +126,7 @@ struct Slice {
 };
 struct ProjSmem {
     Slice buf;
+    short4 rects[kProjThreads];    // K1a's tile rects of this slice (single-view launches)
     unsigned long long bar_geo;    // centers, rotations, scales, b2 (what the conic needs)
     unsigned long long bar_rest;   // w1, b1, w2, sh: streams in while the conic is computed
 };
@@ -144,8 +145,10 @@ __device__ __forceinline__ uint32_t vis_mask_of(const ProjectArgs &a, const CamB
 }
 
 __device__ __forceinline__ void issue_slice(const ProjectArgs &a, Slice &dst, unsigned long long *bar_geo,
-                                            unsigned long long *bar_rest, int64_t i0) {
+                                            unsigned long long *bar_rest, int64_t i0, short4 *rects_dst,
+                                            const short4 *rects_src) {
     const int cnt = (int)(a.n - i0 < kProjThreads ? a.n - i0 : kProjThreads);
+    const uint32_t rbytes = rects_dst ? (((uint32_t)cnt * 8u + 15u) & ~15u) : 0u;
     const float *src[8] = {a.centers, a.rotations, a.scales, a.b2, a.w1, a.b1, a.w2, a.sh};
     float *d[8] = {dst.centers, dst.rot, dst.scales, dst.b2, dst.w1, dst.b1, dst.w2, dst.sh};
     const int per[8] = {3, 4, 3, 1, 24, 8, 8, 48};
@@ -154,8 +157,14 @@ __device__ __forceinline__ void issue_slice(const ProjectArgs &a, Slice &dst, un
         bytes[k] = ((uint32_t)(cnt * per[k] * 4) + 15u) & ~15u;   // arrays are padded in the allocation
         (k < 4 ? geo : rest) += bytes[k];
     }
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar_geo)), "r"(geo)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar_geo)), "r"(geo + rbytes)
                  : "memory");
+    if (rects_dst)   // the visibility this CTA needs arrives with its geometry (no separate round trip)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                psmem_u32(rects_dst)),
+            "l"(rects_src), "r"(rbytes), "r"(psmem_u32(bar_geo))
+            : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar_rest)), "r"(rest)
                  : "memory");
     for (int k = 0; k < 8; ++k)
@@ -327,9 +336,20 @@ __global__ void __launch_bounds__(kProjThreads, 8) k_records(ProjectArgs a, CamB
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&ps.bar_geo)) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&ps.bar_rest)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        issue_slice(a, ps.buf, &ps.bar_geo, &ps.bar_rest, i0);
     }
-    const uint32_t vis = vis_mask_of(a, cb, i0 + threadIdx.x);
+    // single view with a 16-byte aligned rect row: the rects come with the slice
+    const bool rect_smem = cb.nv == 1 && ((cb.view0 * a.n + i0) & 1) == 0;
+    if (threadIdx.x == 0)
+        issue_slice(a, ps.buf, &ps.bar_geo, &ps.bar_rest, i0, rect_smem ? ps.rects : nullptr,
+                    a.rects + cb.view0 * a.n + i0);
+    uint32_t vis;
+    if (rect_smem) {
+        __syncthreads();                 // (publishes the barrier init)
+        mbar_wait0(&ps.bar_geo);
+        vis = (i0 + threadIdx.x < a.n && ps.rects[threadIdx.x].x >= 0) ? 1u : 0u;
+    } else {
+        vis = vis_mask_of(a, cb, i0 + threadIdx.x);
+    }
     if (!__syncthreads_or(vis != 0)) {   // (also publishes the barrier init)
         mbar_wait0(&ps.bar_geo);         // the copies must land before the CTA's smem is freed
         mbar_wait0(&ps.bar_rest);
