@@ -660,6 +660,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     if (rem > 0) jn = sm.qj[wid][qhead];
                     qcount = rem;
                 }
+                // records after jlast that do not touch this warp's block cannot hit its
+                // pixels: the next touching one (or the next batch) bounds what is left
+                if (rem == 0) jn = m ? __ffs(m) - 1 : cnt;
                 const bool batch_end = (m == 0u) && rem == 0;
                 if (!ps.done && pd.ovf) {   // a hit was dropped: nothing may be blended
                     ps.overflow = true;
