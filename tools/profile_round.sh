@@ -8,4 +8,5 @@ python bench.py --impl reference --steps 3 --warmup 1 > $OUT/r01_reference.json 
 python tools/prof_step.py > $OUT/r01_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/r01_launches.csv python tools/prof_step.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_render -s 1 -c 1 -o $OUT/r01_k_render python tools/prof_step.py > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file $OUT/r01_kernel_metrics.csv python tools/prof_step.py --frames 1 > /dev/null 2>&1
 echo done

@@ -84,6 +84,47 @@ open(os.path.join(dst, f"{tag}_k_render_summary.md"), "w").write("\n".join(lines
 json.dump({"kernel": "k_render", "config": "C3", "bytes_per_launch": traffic,
            "source": f"profiles/{tag}_k_render_summary.md (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"},
           open(os.path.join(dst, "render_traffic_bytes.json"), "w"), indent=1)
+# ---- every kernel of one frame: DRAM traffic and duration (cold, serialised)
+km = os.path.join(src, f"{tag}_kernel_metrics.csv")
+if os.path.exists(km):
+    rows = [r for r in csv.reader(open(km)) if len(r) > 10]
+    h = rows[0]
+    ki, mi, ui, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+    idi = h.index("ID")
+    per = collections.OrderedDict()
+    for r in rows[1:]:
+        key = (r[idi], r[ki].split("(")[0].split("::")[-1].strip())
+        v = float(r[vi].replace(",", ""))
+        v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
+              "nsecond": 1e-9, "msecond": 1e-3}.get(r[ui], 1)
+        per.setdefault(key, {})[r[mi]] = v
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    hbm = float(peaks.get("hbm_gbs", 6536.0))
+    lines = [f"# Round {tag[1:]} -- DRAM traffic and duration of every kernel of one C3 frame", "",
+             "Command: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
+             "smsp__issue_active...,sm__warps_active... --clock-control none --csv python tools/prof_step.py "
+             "--frames 1` (the last profiled frame; cold caches, serialised).",
+             f"HBM peak = {hbm:.0f} GB/s (MEASURED_PEAKS.json).  Only K1a/K1b move enough bytes to approach it;",
+             "K2-K4 are latency-bound (short chains of dependent partitions), K5 is ALU/latency-bound (bench.py roofline).", "",
+             "| kernel | µs | DRAM read MB | DRAM write MB | GB/s | frac of HBM peak | issue active % | warps active % |",
+             "|---|---|---|---|---|---|---|---|"]
+    ids = sorted({k[0] for k in per}, key=lambda x: int(x))
+    last = {}
+    for i in ids:
+        for (id_, name), m in per.items():
+            if id_ == i:
+                last.setdefault(name, []).append(m)
+    for name, ms in last.items():
+        m = ms[-1]
+        t = m.get("gpu__time_duration.sum", 0.0)
+        rd = m.get("dram__bytes_read.sum", 0.0)
+        wr = m.get("dram__bytes_write.sum", 0.0)
+        bw = (rd + wr) / t / 1e9 if t else 0.0
+        lines.append(f"| {name} | {t * 1e6:.1f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | {bw:.0f} | {bw / hbm:.2f} | "
+                     f"{m.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.0f} | "
+                     f"{m.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):.0f} |")
+    open(os.path.join(dst, f"{tag}_kernel_rooflines.md"), "w").write("\n".join(lines) + "\n")
+    print("wrote", f"{tag}_kernel_rooflines.md")
 for f in (f"{tag}_bench.json", f"{tag}_reference.json"):
     if os.path.exists(os.path.join(src, f)):
         shutil.copy(os.path.join(src, f), os.path.join(dst, f))
