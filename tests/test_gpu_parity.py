@@ -370,3 +370,35 @@ def test_fallback_pixels_full_size_C5(orc, monkeypatch):
     out_o, fl, _ = orc.render_pixels(scene, cams[0], px, py, bg)
     c = compare(img[py, px], out_o, fl)
     assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.1 * c["n"], c
+
+
+def _deep_scene(n=2600):
+    """n faint spheres strung along the view axis, 0.01 apart, radii cycling through
+    four values: every ray hits all n (t_in order = a fixed permutation of the centre
+    order, consecutive gaps >= ~1e-3, so no near-tie flags) and T stays ~0.1."""
+    scene = synth.make_scene(21, n, box=0.3)
+    i = np.arange(n)
+    scene.centers[:] = np.stack([5.0 + 0.01 * i, np.zeros(n), np.zeros(n)], 1).astype(np.float32)
+    r = 1.2 + 0.035 * (i % 4)
+    scene.scales[:] = np.stack([r, r, r], 1).astype(np.float32)
+    scene.w2 *= np.float32(1e-4)
+    scene.b2[:] = np.float32(3e-4)
+    return scene
+
+
+@pytest.mark.parametrize("limit", [0, 1])
+def test_deep_overlap_long_lists(orc, limit):
+    """2600 hits on every ray of a 2x2-tile image: 2600-key tile lists (sort, ranges),
+    long pending lists in K5 and, with a pending limit of 1, every pixel in K6 with
+    more hits than its shared-memory capacity (kFbHits = 2048: the repeated-selection
+    path)."""
+    scene = _deep_scene()
+    cam = synth.look_at((0, 0, 0), (1, 0, 0), 32, 24, 1600.0)
+    res = gpu_render(scene, [cam], pending_limit=limit, binning=True)
+    _check_binning(orc, scene, [cam], res)
+    img_o, fl, st = orc.render_frame(scene, cam)
+    assert st[..., 1].min() == 2600 and fl.sum() == 0
+    if limit == 1:
+        assert res["stats"]["overflow_pixels"] == 32 * 24
+    c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+    assert c["max_unflagged"] <= TOL, c
