@@ -54,7 +54,7 @@ typedef enum {
     SNP_ERR_INVALID_ARGUMENT = 1,  /* null pointer, bad size, |q| = 0, s <= 0, non-finite value */
     SNP_ERR_OUT_OF_MEMORY = 2,
     SNP_ERR_CUDA = 3,
-    SNP_ERR_UNSUPPORTED = 4,       /* e.g. n_hidden != 8 (P:394 default; other widths are future work) */
+    SNP_ERR_UNSUPPORTED = 4,       /* e.g. n_hidden not in {4, 8, 16, 32} */
     SNP_ERR_BAD_STATE = 5,         /* stage called out of order */
     SNP_ERR_CAPACITY = 6           /* reserved (no-sync capacity overflow is reported by snp_get_stats) */
 } snp_status;
@@ -70,7 +70,8 @@ enum { SNP_MEM_HOST = 0, SNP_MEM_DEVICE = 1, SNP_MEM_HOST_ASYNC = 2 };
  * P:751 "41 parameters from its 8-neuron MLP"). */
 typedef struct {
     int64_t n;               /* number of primitives, >= 0 (0 renders background) */
-    int32_t n_hidden;        /* N_sigma, must be 8 */
+    int32_t n_hidden;        /* N_sigma: 4, 8 (the paper's), 16 or 32; w1 is [n][N][3],
+                                b1 and w2 [n][N] */
     int32_t sh_degree;       /* 0..3; 3 = four bands, 16 coefficients */
     float omega;             /* frequency multiplier, 30 in the paper; > 0 */
     int32_t memory;          /* SNP_MEM_HOST or SNP_MEM_DEVICE (device of the scene) */

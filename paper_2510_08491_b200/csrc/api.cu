@@ -59,6 +59,7 @@ struct snp_scene_s {
     int device = 0;
     int64_t n = 0;
     int32_t sh_degree = 3;
+    int32_t n_hidden = kHidden;
     float omega = 30.f;
     // parameters (SoA)
     DevBuf<float> params;
@@ -123,6 +124,7 @@ int bits_for(int64_t n) {
 
 void fill_args(snp_scene s, ProjectArgs &a) {
     a.n = s->n;
+    a.n_hidden = s->n_hidden;
     a.sh_degree = s->sh_degree;
     a.omega = s->omega;
     a.centers = s->centers; a.rotations = s->rotations; a.scales = s->scales;
@@ -150,7 +152,8 @@ const char *snp_last_error(void) { return g_err.c_str(); }
 // Copies the parameters into the scene's device buffers and validates them on
 // the device (one reduction kernel + one stream synchronisation).
 static snp_status upload_and_validate(snp_scene s, const snp_scene_desc *d, cudaStream_t st) {
-    static const int64_t per[8] = {3, 4, 3, 24, 8, 8, 1, 48};
+    const int64_t N = s->n_hidden;
+    const int64_t per[8] = {3, 4, 3, 3 * N, N, N, 1, 48};
     const float *src[8] = {d->centers, d->rotations, d->scales, d->w1, d->b1, d->w2, d->b2, d->sh};
     float *dst[8] = {s->centers, s->rotations, s->scales, s->w1, s->b1, s->w2, s->b2, s->sh};
     const int64_t n = s->n;
@@ -174,7 +177,8 @@ static snp_status upload_and_validate(snp_scene s, const snp_scene_desc *d, cuda
 static snp_status check_desc(const snp_scene_desc *d) {
     if (!d) return fail(SNP_ERR_INVALID_ARGUMENT, "desc is NULL");
     if (d->n < 0) return fail(SNP_ERR_INVALID_ARGUMENT, "n < 0");
-    if (d->n_hidden != kHidden) return fail(SNP_ERR_UNSUPPORTED, "n_hidden must be 8 (P:394)");
+    if (!hidden_supported(d->n_hidden))
+        return fail(SNP_ERR_UNSUPPORTED, "n_hidden must be 4, 8 (P:394), 16 or 32");
     if (d->sh_degree < 0 || d->sh_degree > 3) return fail(SNP_ERR_INVALID_ARGUMENT, "sh_degree must be 0..3");
     if (!(d->omega > 0.f) || !std::isfinite(d->omega)) return fail(SNP_ERR_INVALID_ARGUMENT, "omega must be > 0");
     if (d->memory != SNP_MEM_HOST && d->memory != SNP_MEM_DEVICE)
@@ -194,13 +198,15 @@ snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stre
     snp_status r = check_desc(d);
     if (r != SNP_OK) return r;
     const int64_t n = d->n;
-    static const int64_t per[8] = {3, 4, 3, 24, 8, 8, 1, 48};
+    const int64_t N = d->n_hidden;
+    const int64_t per[8] = {3, 4, 3, 3 * N, N, N, 1, 48};
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return fail(SNP_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
     cudaStream_t st = (cudaStream_t)cuda_stream;
     snp_scene s = new snp_scene_s();
     s->device = device;
     s->n = n;
+    s->n_hidden = d->n_hidden;
     s->sh_degree = d->sh_degree;
     s->omega = d->omega;
     // one allocation, each array 256-byte aligned
@@ -246,6 +252,8 @@ snp_status snp_update_scene(snp_scene s, const snp_scene_desc *d, void *cuda_str
     r = check_desc(d);
     if (r != SNP_OK) return r;
     if (d->n != s->n) return fail(SNP_ERR_INVALID_ARGUMENT, "snp_update_scene: n differs from the scene's");
+    if (d->n_hidden != s->n_hidden)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "snp_update_scene: n_hidden differs from the scene's");
     s->sh_degree = d->sh_degree;
     s->omega = d->omega;
     if (s->join_pending) {   // K1b may still read the parameters being replaced
@@ -287,7 +295,7 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
     const size_t items = (size_t)n_views * (size_t)s->n;
     SNP_CUDA(s->rects.ensure(items + 2));   // (+2: K1b bulk-copies rect rows rounded up to 16 bytes)
     SNP_CUDA(s->depth.ensure(items));
-    SNP_CUDA(s->records.ensure(items * 16));
+    SNP_CUDA(s->records.ensure(items * rec_f4(s->n_hidden)));
     s->cams.clear();
     for (int v0 = 0; v0 < n_views; v0 += kCamsPerLaunch) {
         CamBatch cb{};
@@ -489,6 +497,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
                                  sizeof(unsigned long long) * (kCntK5Done - kCntTested + 1), st));
     s->render_dirty = true;
     RenderArgs a{};
+    a.n_hidden = s->n_hidden;
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
     a.tiles_per_view = s->tiles_x * s->tiles_y;
@@ -513,7 +522,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     a.fallback_capacity = s->fallback_capacity;
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     a.counters = s->counters.p;
-    a.k5_grid = render_grid(s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
+    a.k5_grid = render_grid(s->n_hidden, s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
         for (size_t k = 0; k < s->cams.size(); ++k) {

@@ -184,8 +184,9 @@ __global__ void k_validate(ProjectArgs a, int *bad) {
         if (!isfinite(s) || !isfinite(c)) b |= 1;
         if (!(s > 0.f)) b |= 4;
     }
-    for (int k = 0; k < 24; ++k) if (!isfinite(a.w1[24 * i + k])) b |= 1;
-    for (int k = 0; k < 8; ++k) if (!isfinite(a.b1[8 * i + k]) || !isfinite(a.w2[8 * i + k])) b |= 1;
+    const int N = a.n_hidden;
+    for (int k = 0; k < 3 * N; ++k) if (!isfinite(a.w1[3 * N * i + k])) b |= 1;
+    for (int k = 0; k < N; ++k) if (!isfinite(a.b1[N * i + k]) || !isfinite(a.w2[N * i + k])) b |= 1;
     if (!isfinite(a.b2[i])) b |= 1;
     for (int k = 0; k < 48; ++k) if (!isfinite(a.sh[48 * i + k])) b |= 1;
     if (b) {

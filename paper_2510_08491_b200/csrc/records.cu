@@ -1,4 +1,4 @@
-// records.cu -- K1b: the 256-byte render record of every visible (view, primitive)
+// records.cu -- K1b: the render record (256 B at N = 8) of every visible (view, primitive)
 // pair (K1a's rect.x >= 0), see snp_internal.cuh "Render record".  It runs on the
 // scene's side stream concurrently with K2-K4 and is joined before K5.
 //
@@ -112,20 +112,22 @@ __device__ __forceinline__ void sh_rgb(int degree, const float4 *sh4, double xd,
 
 constexpr int kProjThreads = 64;
 
-// One slice = the parameters of kProjThreads consecutive primitives, staged with
-// cp.async.bulk and reused by every view of the launch.
+// One slice = the parameters of kProjThreads consecutive primitives (N hidden units),
+// staged with cp.async.bulk and reused by every view of the launch.
+template <int N>
 struct Slice {
     float centers[kProjThreads * 3];
     float rot[kProjThreads * 4];
     float scales[kProjThreads * 3];
-    float w1[kProjThreads * 24];
-    float b1[kProjThreads * 8];
-    float w2[kProjThreads * 8];
+    float w1[kProjThreads * 3 * N];
+    float b1[kProjThreads * N];
+    float w2[kProjThreads * N];
     float b2[kProjThreads];
     float sh[kProjThreads * 48];
 };
+template <int N>
 struct ProjSmem {
-    Slice buf;
+    Slice<N> buf;
     short4 rects[kProjThreads];    // K1a's tile rects of this slice (single-view launches)
     unsigned long long bar_geo;    // centers, rotations, scales, b2 (what the conic needs)
     unsigned long long bar_rest;   // w1, b1, w2, sh: streams in while the conic is computed
@@ -144,14 +146,15 @@ __device__ __forceinline__ uint32_t vis_mask_of(const ProjectArgs &a, const CamB
     return m;
 }
 
-__device__ __forceinline__ void issue_slice(const ProjectArgs &a, Slice &dst, unsigned long long *bar_geo,
+template <int N>
+__device__ __forceinline__ void issue_slice(const ProjectArgs &a, Slice<N> &dst, unsigned long long *bar_geo,
                                             unsigned long long *bar_rest, int64_t i0, short4 *rects_dst,
                                             const short4 *rects_src) {
     const int cnt = (int)(a.n - i0 < kProjThreads ? a.n - i0 : kProjThreads);
     const uint32_t rbytes = rects_dst ? (((uint32_t)cnt * 8u + 15u) & ~15u) : 0u;
     const float *src[8] = {a.centers, a.rotations, a.scales, a.b2, a.w1, a.b1, a.w2, a.sh};
     float *d[8] = {dst.centers, dst.rot, dst.scales, dst.b2, dst.w1, dst.b1, dst.w2, dst.sh};
-    const int per[8] = {3, 4, 3, 1, 24, 8, 8, 48};
+    const int per[8] = {3, 4, 3, 1, 3 * N, N, N, 48};
     uint32_t geo = 0, rest = 0, bytes[8];
     for (int k = 0; k < 8; ++k) {
         bytes[k] = ((uint32_t)(cnt * per[k] * 4) + 15u) & ~15u;   // arrays are padded in the allocation
@@ -193,6 +196,7 @@ struct PrimParams {
     float b2;
 };
 
+template <int N>
 __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch &cb, const PrimParams &pp,
                                            int64_t i, uint32_t vis_mask, unsigned long long *bar_rest) {
     const float mu0 = pp.center[0], mu1 = pp.center[1], mu2 = pp.center[2];
@@ -292,7 +296,7 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
 #pragma unroll
                 for (int j = 0; j < 3; ++j) Wh[3 * k + j] = (float)R[3 * j + k] * is[k];
         }
-        float4 *rec = a.records + o * 16;
+        float4 *rec = a.records + o * rec_f4(N);
         const float b2 = pp.b2;
         rec[kRecConic] = make_float4(cx0, cy0, ca, cb2);
         rec[kRecConicRgb] = make_float4(cc, rgb[0], rgb[1], rgb[2]);
@@ -305,32 +309,34 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
         const float4 *w1v = pp.w1;
         const float4 *b1v = pp.b1;
         const float4 *w2v = pp.w2;
-        float w1[24], b1[8];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            float4 t = w1v[k];
-            w1[4 * k] = t.x; w1[4 * k + 1] = t.y; w1[4 * k + 2] = t.z; w1[4 * k + 3] = t.w;
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            float4 t = b1v[k];
-            b1[4 * k] = t.x; b1[4 * k + 1] = t.y; b1[4 * k + 2] = t.z; b1[4 * k + 3] = t.w;
-        }
         const float scf = (float)(om * rcp64(smax)), omf = a.omega;
+        // four units at a time: three float4 of W1 rows and one of b1
 #pragma unroll
-        for (int k = 0; k < kHidden; ++k)
-            rec[kRecUnits + k] = make_float4(scf * w1[3 * k], scf * w1[3 * k + 1], scf * w1[3 * k + 2],
-                                             omf * b1[k]);
-        rec[kRecW2] = w2v[0];
-        rec[kRecW2 + 1] = w2v[1];
+        for (int g = 0; g < N / 4; ++g) {
+            float w1[12], b1[4];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float4 t = w1v[3 * g + k];
+                w1[4 * k] = t.x; w1[4 * k + 1] = t.y; w1[4 * k + 2] = t.z; w1[4 * k + 3] = t.w;
+            }
+            const float4 tb = b1v[g];
+            b1[0] = tb.x; b1[1] = tb.y; b1[2] = tb.z; b1[3] = tb.w;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                rec[kRecUnits + 4 * g + k] = make_float4(scf * w1[3 * k], scf * w1[3 * k + 1], scf * w1[3 * k + 2],
+                                                         omf * b1[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < N / 4; ++j) rec[rec_w2(N) + j] = w2v[j];
     }
 }
 
 // One CTA per slice.  The slice load is issued first (its latency overlaps the
 // visibility read); a CTA whose slice has no visible primitive only waits for it.
+template <int N>
 __global__ void __launch_bounds__(kProjThreads, 8) k_records(ProjectArgs a, CamBatch cb) {
     extern __shared__ __align__(128) unsigned char psm_raw[];
-    ProjSmem &ps = *reinterpret_cast<ProjSmem *>(psm_raw);
+    ProjSmem<N> &ps = *reinterpret_cast<ProjSmem<N> *>(psm_raw);
     const int64_t i0 = (int64_t)blockIdx.x * kProjThreads;
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&ps.bar_geo)) : "memory");
@@ -358,32 +364,47 @@ __global__ void __launch_bounds__(kProjThreads, 8) k_records(ProjectArgs a, CamB
     mbar_wait0(&ps.bar_geo);
     if (vis) {
         const int li = threadIdx.x;
-        const Slice &sl = ps.buf;
+        const Slice<N> &sl = ps.buf;
         PrimParams pp;
         pp.center = sl.centers + 3 * li;
         pp.scale = sl.scales + 3 * li;
         pp.rot = reinterpret_cast<const float4 *>(sl.rot) + li;
         pp.sh = reinterpret_cast<const float4 *>(sl.sh + 48 * li);
-        pp.w1 = reinterpret_cast<const float4 *>(sl.w1 + 24 * li);
-        pp.b1 = reinterpret_cast<const float4 *>(sl.b1 + 8 * li);
-        pp.w2 = reinterpret_cast<const float4 *>(sl.w2 + 8 * li);
+        pp.w1 = reinterpret_cast<const float4 *>(sl.w1 + 3 * N * li);
+        pp.b1 = reinterpret_cast<const float4 *>(sl.b1 + N * li);
+        pp.w2 = reinterpret_cast<const float4 *>(sl.w2 + N * li);
         pp.b2 = sl.b2[li];   // (geometry part of the slice)
-        record_one(a, cb, pp, i0 + li, vis, &ps.bar_rest);
+        record_one<N>(a, cb, pp, i0 + li, vis, &ps.bar_rest);
     }
 }
 
 
 }  // namespace
 
-cudaError_t launch_records(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
-    if (a.n == 0) return cudaSuccess;
+namespace {
+template <int N>
+cudaError_t launch_records_n(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_records, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ProjSmem));
+        cudaError_t e = cudaFuncSetAttribute(k_records<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(ProjSmem<N>));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_records<<<(unsigned)((a.n + kProjThreads - 1) / kProjThreads), kProjThreads, sizeof(ProjSmem), st>>>(a, cams);
+    k_records<N><<<(unsigned)((a.n + kProjThreads - 1) / kProjThreads), kProjThreads, sizeof(ProjSmem<N>), st>>>(a,
+                                                                                                             cams);
     return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_records(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
+    if (a.n == 0) return cudaSuccess;
+    switch (a.n_hidden) {
+        case 4: return launch_records_n<4>(a, cams, st);
+        case 8: return launch_records_n<8>(a, cams, st);
+        case 16: return launch_records_n<16>(a, cams, st);
+        case 32: return launch_records_n<32>(a, cams, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 }  // namespace snp

@@ -37,17 +37,26 @@ constexpr int kConsumers = 8;                      // consumer warps = 8x4 pixel
 constexpr int kThreads = (kConsumers + 1) * 32;    // + 1 producer warp
 constexpr int kWarps = kConsumers;
 constexpr int kBatch = 32;          // records per stage (one per producer lane)
-constexpr int kStages = 6;          // TMA ring depth (2 CTAs x ~106 KB per SM)
 constexpr int kQueue = 128;         // per-warp candidate ring (power of two, >= 31 + 2 x 32)
-constexpr int kRecStride = 17;      // float4 per staged record (16 + 1 pad)
+// Per hidden width N: the staged record stride (rec_f4(N) float4, made odd so that the
+// distinct records one warp reads fall in distinct bank groups: 17 at N = 8) and the
+// TMA ring depth (6 at N <= 8: 2 CTAs x ~106 KB per SM; fewer for the longer records).
+template <int N>
+struct Cfg {
+    static constexpr int kRecStride = rec_f4(N) | 1;
+    static constexpr int kStages = N <= 8 ? 6 : (N == 16 ? 4 : 2);
+    static constexpr uint32_t kRecBytes = 16u * rec_f4(N);
+};
 constexpr int kPend = 16;           // per-pixel pending hits (sorted ring)
 static_assert((kPend & (kPend - 1)) == 0, "the pending ring needs a power of two");
 constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
 
+template <int N>
 struct __align__(16) Smem {
-    float4 rec[kStages][kBatch][kRecStride];  // records, cp.async.bulk-staged, padded to 17 float4 so
-                                              // that 8 distinct records read by one warp hit 8
-                                              // distinct 16-byte bank groups
+    static constexpr int kStages = Cfg<N>::kStages;
+    float4 rec[kStages][kBatch][Cfg<N>::kRecStride];  // records, cp.async.bulk-staged, padded to an odd
+                                                      // float4 count so that 8 distinct records read by
+                                                      // one warp hit 8 distinct 16-byte bank groups
     float L[kStages][kBatch + 1];             // depth lower bounds (+ the next batch's first)
     uint32_t id[kStages][kBatch];
     // slot metadata written by the producer before its arrive (release)
@@ -147,7 +156,8 @@ __device__ __forceinline__ float sinc_f(float x) {
     return fabsf(x) < 0.25f ? poly : s;
 }
 
-// Exact hit + kernel for one (ray, record).  Returns false on a miss.
+// Exact hit + kernel for one (ray, record) of N hidden units.  Returns false on a miss.
+template <int N>
 __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const Ray &r, float &t_hi, float &t_lo,
                                           float &kap) {
     const float4 mh = rec[kRecMh];
@@ -189,10 +199,14 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
     const float tm = 0.5f * (tlo + thi);
     const float hdt = 0.5f * dt;
     float acc = 0.f;
-    const float4 W2a = rec[kRecW2], W2b = rec[kRecW2 + 1];
-    const float W2[8] = {W2a.x, W2a.y, W2a.z, W2a.w, W2b.x, W2b.y, W2b.z, W2b.w};
+    float W2[N];
 #pragma unroll
-    for (int k = 0; k < kHidden; ++k) {
+    for (int j = 0; j < N / 4; ++j) {
+        const float4 w = rec[rec_w2(N) + j];
+        W2[4 * j] = w.x; W2[4 * j + 1] = w.y; W2[4 * j + 2] = w.z; W2[4 * j + 3] = w.w;
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
         const float4 u = rec[kRecUnits + k];
         const float h = fmaf(u.z, r.dhz, fmaf(u.y, r.dhy, u.x * r.dhx));
         const float g = fmaf(u.z, pz, fmaf(u.y, py, fmaf(u.x, px, u.w)));
@@ -237,7 +251,8 @@ struct PixelState {
 // (strictly): every hit not yet inserted has t_in >= L (R19), so these are
 // exactly the next hits of the ray in (t_in, id) order (Eq. 4).  The
 // list is sorted, so they are popped from its head.
-__device__ __forceinline__ void emit(Smem &sm, PixelState &ps, Pending &pd, float L, float t_floor,
+template <int N>
+__device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, float L, float t_floor,
                                      const float4 *recs) {
     const int tid = threadIdx.x;
     int n = pd.n;
@@ -246,7 +261,7 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, Pending &pd, floa
         const float t = sm.p_thi[h][tid];
         if (!(t < L)) break;
         const float kap = sm.p_kap[h][tid];
-        const float4 rgb = __ldg(recs + (size_t)sm.p_id[h][tid] * 16 + kRecConicRgb);
+        const float4 rgb = __ldg(recs + (size_t)sm.p_id[h][tid] * rec_f4(N) + kRecConicRgb);
         const float w = ps.T * kap;
         ps.cr = fmaf(w, rgb.y, ps.cr);
         ps.cg = fmaf(w, rgb.z, ps.cg);
@@ -267,7 +282,8 @@ __device__ __forceinline__ void emit(Smem &sm, PixelState &ps, Pending &pd, floa
 // Owner-local sorted insertion of one hit into this lane's pending ring: appended
 // when it is the largest (t_in, id) so far (the usual case: records stream in L
 // order), else shifted into place.  A full ring drops the hit and marks the pixel.
-__device__ __forceinline__ void insert_local(Smem &sm, Pending &pd, int plimit, float tn, float kn, uint32_t in) {
+template <int N>
+__device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimit, float tn, float kn, uint32_t in) {
     const int tid = threadIdx.x;
     if (pd.n >= plimit) {
         pd.ovf = true;
@@ -297,9 +313,11 @@ __device__ __forceinline__ void insert_local(Smem &sm, Pending &pd, int plimit, 
     ++pd.n;
 }
 
+template <int N>
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
+    constexpr int kStages = Cfg<N>::kStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
+    Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     const int stripe_tiles = a.tiles_x * a.stripe_rows;
@@ -375,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
             const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
             const int nb = max(1, (int)((end - beg + kBatch - 1) / kBatch));
-            const float4 *recs = a.records + (size_t)view * (size_t)a.n * 16;
+            const float4 *recs = a.records + (size_t)view * (size_t)a.n * rec_f4(N);
             if (lane == 0) *(volatile int32_t *)&sm.tdone[seq % kTileRing] = 0;
             for (int bt = 0; bt < nb; ++bt) {
                 const int slot = (int)(gb % kStages);
@@ -398,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     const uint32_t id = a.vals[e0 + lane];
                     sm.id[slot][lane] = id;
                     sm.L[slot][lane] = key_depth(a.keys[e0 + lane]);
-                    bulk_g2s(&sm.rec[slot][lane][0], recs + (size_t)id * 16, 256u, &sm.full[slot]);
+                    bulk_g2s(&sm.rec[slot][lane][0], recs + (size_t)id * rec_f4(N), Cfg<N>::kRecBytes,
+                             &sm.full[slot]);
                 }
                 if (lane == 0) {
                     const uint32_t nx = e0 + cnt;
@@ -410,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 }
                 // the arrive (release) publishes id/L/metadata with the phase
                 __syncwarp();
-                if (lane == 0) mbar_arrive_expect_tx(&sm.full[slot], cnt * 256u);
+                if (lane == 0) mbar_arrive_expect_tx(&sm.full[slot], cnt * Cfg<N>::kRecBytes);
                 ++gb;
             }
             ++seq;
@@ -497,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             const int ty = a.row_begin + (st / a.tiles_x) * a.row_stride;
             view = cb.view0 + vloc;
             cam = &cb.cams[vloc];
-            recs = a.records + (size_t)view * (size_t)a.n * 16;
+            recs = a.records + (size_t)view * (size_t)a.n * rec_f4(N);
             const int bx = tx * kTile + (wid & 1) * 8, by = ty * kTile + (wid >> 1) * 4;
             x = bx + (lane & 7);
             y = by + (lane >> 3);
@@ -567,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 ro.t_far = cam->t_far;
                 bool hit = false;
                 float th = 0.f, tl = 0.f, kap = 0.f;
-                if (valid) hit = exact_hit(&sm.rec[slot][j][0], ro, th, tl, kap);
+                if (valid) hit = exact_hit<N>(&sm.rec[slot][j][0], ro, th, tl, kap);
                 n_hit += hit;
 #ifdef SNP_INSTRUMENT
                 long long _i0 = clock64();
@@ -592,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     const uint32_t in = __shfl_sync(0xffffffffu, idn, src);
                     if (inc) {
                         inc &= inc - 1u;
-                        insert_local(sm, pd, plimit, tn, kn, in);
+                        insert_local<N>(sm, pd, plimit, tn, kn, in);
                     }
                 }
 #ifdef SNP_INSTRUMENT
@@ -676,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     ++ins_ecalls;
                     ins_enone += (pd.n == 0);
 #endif
-                    emit(sm, ps, pd, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                    emit<N>(sm, ps, pd, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
                          a.t_floor, recs);
 #ifdef SNP_INSTRUMENT
                     ins_emit += clock64() - _e0;
@@ -731,6 +750,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     warp_exit();
 }
 
+template <int N>
 __device__ __forceinline__ bool fb_hit(const float4 *rec, const Ray &ray, float pxf, float pyf, float &th,
                                        float &tl, float &kap) {
     const float4 c0 = rec[kRecConic];
@@ -738,7 +758,7 @@ __device__ __forceinline__ bool fb_hit(const float4 *rec, const Ray &ray, float 
     const float dx = pxf - c0.x, dy = pyf - c0.y;
     const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
     if (!(q <= 1.0f)) return false;
-    return exact_hit(rec, ray, th, tl, kap);
+    return exact_hit<N>(rec, ray, th, tl, kap);
 }
 
 // K6: exact per-pixel fallback, one CTA per overflowed pixel.  Phase A: the
@@ -778,6 +798,7 @@ __device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long 
 // are claimed one at a time as K5 queues them, and the CTA leaves once every K5 CTA has
 // exited and no entry is left.  overlap = false: K5 has completed; CTAs stride over the
 // queue and take the entries of this batch's views.
+template <int N>
 __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb, int overlap) {
     if (!overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ FbSmem sm;
@@ -824,7 +845,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
         const int tile = (y / kTile) * a.tiles_x + (x / kTile);
         const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
         const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
-        const float4 *recs = a.records + (size_t)view * (size_t)a.n * 16;
+        const float4 *recs = a.records + (size_t)view * (size_t)a.n * rec_f4(N);
         const Ray ray = make_ray(cam, x, y);
         const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
         if (tid == 0) sm.count = 0;
@@ -847,7 +868,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
             for (int u = 0; u < kFbIlp; ++u) {
                 cand[u] = false;
                 if (ids[u] != 0xffffffffu) {
-                    const float4 *rec = recs + (size_t)ids[u] * 16;
+                    const float4 *rec = recs + (size_t)ids[u] * rec_f4(N);
                     const float4 c0 = rec[kRecConic];
                     const float cc = rec[kRecConicRgb].x;
                     const float dx = pxf - c0.x, dy = pyf - c0.y;
@@ -857,7 +878,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
 #pragma unroll
             for (int u = 0; u < kFbIlp; ++u) {
                 float th, tl, kap;
-                if (cand[u] && exact_hit(recs + (size_t)ids[u] * 16, ray, th, tl, kap)) {
+                if (cand[u] && exact_hit<N>(recs + (size_t)ids[u] * rec_f4(N), ray, th, tl, kap)) {
                     const int pos = atomicAdd(&sm.count, 1);
                     if (pos < kFbHits) {
                         sm.t[pos] = th; sm.l[pos] = tl; sm.k[pos] = kap; sm.id[pos] = ids[u];
@@ -951,7 +972,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
                 if (i < n && Tb >= a.t_floor) {
                     const int h = sm.idx[i];
                     const float kap = sm.k[h];
-                    const float4 rgb = __ldg(recs + (size_t)sm.id[h] * 16 + kRecConicRgb);
+                    const float4 rgb = __ldg(recs + (size_t)sm.id[h] * rec_f4(N) + kRecConicRgb);
                     const float w = Tb * kap;
                     wr = fmaf(w, rgb.y, wr);
                     wg = fmaf(w, rgb.z, wg);
@@ -994,7 +1015,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
                 for (uint32_t e = beg + tid; e < end; e += kFbThreads) {
                     const uint32_t id = a.vals[e];
                     float th, tl, kap;
-                    if (!fb_hit(recs + (size_t)id * 16, ray, pxf, pyf, th, tl, kap)) continue;
+                    if (!fb_hit<N>(recs + (size_t)id * rec_f4(N), ray, pxf, pyf, th, tl, kap)) continue;
                     if (!first && !before(lh, ll, lid, th, tl, id)) continue;
                     if (before(th, tl, id, bh, bl, bid)) { bh = th; bl = tl; bid = id; bk = kap; }
                 }
@@ -1014,7 +1035,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
                         bh = sm.t[w]; bl = sm.l[w]; bid = sm.id[w]; bk = sm.k[w];
                     }
                 if (bid == 0xffffffffu) break;
-                const float4 rgb = __ldg(recs + (size_t)bid * 16 + kRecConicRgb);
+                const float4 rgb = __ldg(recs + (size_t)bid * rec_f4(N) + kRecConicRgb);
                 const float w = T * bk;
                 cr = fmaf(w, rgb.y, cr);
                 cg = fmaf(w, rgb.z, cg);
@@ -1086,35 +1107,76 @@ __global__ void __launch_bounds__(1024) k_tile_order(RenderArgs a, CamBatch cb, 
 
 }  // namespace
 
-cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st) {
+namespace {
+template <int N>
+int render_grid_n(int tiles) {
+    static int resident = 0;   // persistent grid: every CTA that fits, all SMs
+    if (!resident) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_render<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<N>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N>, kThreads, sizeof(Smem<N>));
+        resident = std::max(1, sms) * std::max(1, per_sm);
+    }
+    return std::min(tiles, resident);
+}
+
+template <int N>
+cudaError_t launch_render_n(const RenderArgs &a, const CamBatch &cams, int tiles, cudaStream_t st) {
     static bool attr_set = false;
-    const int smem = (int)sizeof(Smem);
+    const int smem = (int)sizeof(Smem<N>);
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_render, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_render<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
+    k_render<N><<<render_grid_n<N>(tiles), kThreads, smem, st>>>(a, cams);
+    return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_fallback_n(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
+    static int resident = 0;   // every CTA that fits, all SMs (the queue loop strides by the grid)
+    if (!resident) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback<N>, kFbThreads, 0);
+        resident = std::max(1, sms) * std::max(1, per_sm);
+    }
+    const int overlap = n_batches == 1 ? 1 : 0;
+    for (int i = 0; i < n_batches; ++i) {
+        cudaError_t e = launch_hi(k_fallback<N>, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i], overlap);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st) {
     const int tiles = a.tiles_x * a.stripe_rows * cams.nv;
     if (tiles == 0) return cudaSuccess;
     if (reset_queue) {
         cudaError_t e = cudaMemsetAsync(a.counters + kCntTileQueue, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
     }
-    k_render<<<render_grid(tiles), kThreads, smem, st>>>(a, cams);
-    return cudaGetLastError();
+    switch (a.n_hidden) {
+        case 4: return launch_render_n<4>(a, cams, tiles, st);
+        case 8: return launch_render_n<8>(a, cams, tiles, st);
+        case 16: return launch_render_n<16>(a, cams, tiles, st);
+        case 32: return launch_render_n<32>(a, cams, tiles, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
-int render_grid(int tiles) {
-    static int resident = 0;   // persistent grid: every CTA that fits, all SMs
-    if (!resident) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_render, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render, kThreads, sizeof(Smem));
-        resident = std::max(1, sms) * std::max(1, per_sm);
+int render_grid(int n_hidden, int tiles) {
+    switch (n_hidden) {
+        case 4: return render_grid_n<4>(tiles);
+        case 16: return render_grid_n<16>(tiles);
+        case 32: return render_grid_n<32>(tiles);
+        default: return render_grid_n<8>(tiles);
     }
-    return std::min(tiles, resident);
 }
 
 cudaError_t launch_tile_order(const RenderArgs &a, const CamBatch &cams, uint32_t *order, cudaStream_t st) {
@@ -1123,20 +1185,13 @@ cudaError_t launch_tile_order(const RenderArgs &a, const CamBatch &cams, uint32_
 }
 
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
-    static int resident = 0;   // every CTA that fits, all SMs (the queue loop strides by the grid)
-    if (!resident) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback, kFbThreads, 0);
-        resident = std::max(1, sms) * std::max(1, per_sm);
+    switch (a.n_hidden) {
+        case 4: return launch_fallback_n<4>(a, cams, n_batches, st);
+        case 8: return launch_fallback_n<8>(a, cams, n_batches, st);
+        case 16: return launch_fallback_n<16>(a, cams, n_batches, st);
+        case 32: return launch_fallback_n<32>(a, cams, n_batches, st);
+        default: return cudaErrorInvalidValue;
     }
-    const int overlap = n_batches == 1 ? 1 : 0;
-    for (int i = 0; i < n_batches; ++i) {
-        cudaError_t e = launch_hi(k_fallback, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i], overlap);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaGetLastError();
 }
 
 }  // namespace snp

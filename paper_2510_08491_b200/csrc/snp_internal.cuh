@@ -41,9 +41,14 @@ cudaError_t launch_hi(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
 }
 
 constexpr int kTile = 16;                 // BASELINE north_star: 16x16 tiles (R18)
-constexpr int kHidden = 8;                // N_sigma = 8
+constexpr int kHidden = 8;                // N_sigma = 8, the paper's width
+// Supported widths N_sigma: every N-dependent kernel is a template
+// instantiated for these; N = 8 is the measured configuration.
+__host__ __device__ constexpr bool hidden_supported(int N) { return N == 4 || N == 8 || N == 16 || N == 32; }
 constexpr int kCamsPerLaunch = 32;        // cameras passed by value per launch
-constexpr int kRecordFloats = 64;         // one render record = 256 B = 16 float4
+// float4 per render record: 6 (conic, colour, centre, whitening) + N units + N/4 for W2
+// = 11 / 16 / 26 / 46 for N = 4 / 8 / 16 / 32 (256 B at N = 8)
+__host__ __device__ constexpr int rec_f4(int N) { return 6 + N + N / 4; }
 // Key = view << (tile_bits + 19) | tile << 19 | (bits(L) >> 12): the depth code is
 // the fp32 lower bound L truncated to 11 mantissa bits (still a lower bound, R19).
 constexpr int kDepthBits = 19;
@@ -82,10 +87,12 @@ struct CamBatch {
 //  f4[3]  = ml.x, ml.y, ml.z, Wh00
 //  f4[4]  = Wh01, Wh02, Wh10, Wh11   Wh = diag(1/s) R^T (world -> unit-sphere frame)
 //  f4[5]  = Wh12, Wh20, Wh21, Wh22
-//  f4[6+k]= W1'_k.x, W1'_k.y, W1'_k.z, omega*b1_k   W1'_k = omega W1_k / ||s||_inf  (k < 8)
-//  f4[14] = W2_0..3, f4[15] = W2_4..7
+//  f4[6+k]= W1'_k.x, W1'_k.y, W1'_k.z, omega*b1_k   W1'_k = omega W1_k / ||s||_inf  (k < N)
+//  f4[6+N+j] = W2_{4j..4j+3}                        (j < N/4)
+// (N hidden units; rec_f4(N) float4 in all)
 enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecWh0 = 4,
-                  kRecWh1 = 5, kRecUnits = 6, kRecW2 = 14 };
+                  kRecWh1 = 5, kRecUnits = 6 };
+__host__ __device__ constexpr int rec_w2(int N) { return kRecUnits + N; }
 
 // Device-side counters (one 64-bit slot each), see snp_stats.
 // The render counters kCntTested..kCntK5Done are contiguous: K4 clears them for the
@@ -99,6 +106,7 @@ enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3
 
 struct ProjectArgs {
     int64_t n;
+    int32_t n_hidden;       // N_sigma (hidden_supported)
     int32_t sh_degree;
     float omega;
     const float *centers, *rotations, *scales, *w1, *b1, *w2, *b2, *sh;
@@ -161,6 +169,7 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
                             int64_t expected_n, cudaStream_t st, int *final_idx);
 
 struct RenderArgs {
+    int32_t n_hidden;              // N_sigma (hidden_supported): selects the kernel instantiation
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;
@@ -191,6 +200,6 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
 // CTAs leave, take overflowed pixels as K5 queues them and end once every K5 CTA has
 // exited.  With several batches it runs after all of them.
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
-int render_grid(int tiles);   // K5's persistent grid for `tiles` work units
+int render_grid(int n_hidden, int tiles);   // K5's persistent grid for `tiles` work units
 
 }  // namespace snp

@@ -122,7 +122,7 @@ def _is_device(x):
 FIELDS = ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh")
 
 
-def _desc(scene, n_hidden=8, sh_degree=None, omega=None):
+def _desc(scene, n_hidden=None, sh_degree=None, omega=None):
     arrs = []
     for f in FIELDS:
         a = getattr(scene, f)
@@ -133,13 +133,15 @@ def _desc(scene, n_hidden=8, sh_degree=None, omega=None):
         arrs.append(a)
     mem = SNP_MEM_DEVICE if _is_device(arrs[0]) else SNP_MEM_HOST
     n = int(arrs[0].shape[0])
+    if n_hidden is None:   # w1 is [n, N, 3]
+        n_hidden = int(arrs[3].shape[1]) if len(arrs[3].shape) == 3 else 8
     desc = SceneDesc(n, n_hidden, int(getattr(scene, "sh_degree", 3) if sh_degree is None else sh_degree),
                      float(getattr(scene, "omega", 30.0) if omega is None else omega), mem,
                      *[_ptr(a) for a in arrs])
     return desc, arrs
 
 
-def create_scene(scene, device=0, stream=None, n_hidden=8, sh_degree=None, omega=None):
+def create_scene(scene, device=0, stream=None, n_hidden=None, sh_degree=None, omega=None):
     """``scene`` has float32 C-contiguous arrays ``centers [n,3] ... sh [n,16,3]``
     (numpy = host memory, torch CUDA tensors = device memory)."""
     desc, keep = _desc(scene, n_hidden, sh_degree, omega)
@@ -149,7 +151,7 @@ def create_scene(scene, device=0, stream=None, n_hidden=8, sh_degree=None, omega
     return h.value
 
 
-def update_scene(h, scene, stream=None, n_hidden=8, sh_degree=None, omega=None):
+def update_scene(h, scene, stream=None, n_hidden=None, sh_degree=None, omega=None):
     desc, keep = _desc(scene, n_hidden, sh_degree, omega)
     _check(lib().snp_update_scene(h, C.byref(desc), _stream(stream)))
     del keep

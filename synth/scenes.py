@@ -216,14 +216,16 @@ CONFIGS = {
 }
 
 
-def make_config(name, variant="trained", n=None, views=None) -> Tuple[Scene, List[Camera], Tuple]:
-    """Returns (scene, cameras, background) for a BASELINE config name."""
+def make_config(name, variant="trained", n=None, views=None,
+                n_hidden=N_HIDDEN) -> Tuple[Scene, List[Camera], Tuple]:
+    """Returns (scene, cameras, background) for a BASELINE config name (n_hidden: the
+    MLP width N_sigma; the configs are quoted at the paper's 8)."""
     cfg = CONFIGS[name]
     n = cfg["n"] if n is None else n
     views = cfg["views"] if views is None else views
     sc = dict(cfg["scene"])
     sc.pop("kind")
-    scene = make_scene(cfg["seed"], n, variant=variant, **sc)
+    scene = make_scene(cfg["seed"], n, variant=variant, n_hidden=n_hidden, **sc)
     if views == 1:
         cams = orbit_cameras(1, 4.0, cfg["width"], cfg["height"], cfg["fx"],
                              elev_deg=(20.0, 20.0), az0_deg=30.0)

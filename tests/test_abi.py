@@ -51,8 +51,9 @@ def test_argument_validation_without_gpu(snp):
     h = C.c_void_p()
     assert L.snp_create_scene(None, 0, None, C.byref(h)) == 1
     sc = synth.make_scene(0, 16)
-    d, keep = _desc(snp, sc, n_hidden=4)
-    assert L.snp_create_scene(C.byref(d), 0, None, C.byref(h)) == 4          # UNSUPPORTED
+    for n_hidden in (0, 6, 12, 64):                                             # widths 4/8/16/32 only
+        d, keep = _desc(snp, sc, n_hidden=n_hidden)
+        assert L.snp_create_scene(C.byref(d), 0, None, C.byref(h)) == 4      # UNSUPPORTED
     d, keep = _desc(snp, sc, sh_degree=4)
     assert L.snp_create_scene(C.byref(d), 0, None, C.byref(h)) == 1
     d, keep = _desc(snp, sc, n=-1)

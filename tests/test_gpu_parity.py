@@ -402,3 +402,26 @@ def test_deep_overlap_long_lists(orc, limit):
         assert res["stats"]["overflow_pixels"] == 32 * 24
     c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
     assert c["max_unflagged"] <= TOL, c
+
+
+@pytest.mark.parametrize("n_hidden", [4, 16, 32])
+def test_hidden_widths(orc, n_hidden):
+    """N_sigma in {4, 16, 32} -- records of 6 + N + N/4 float4, K1b, K5
+    and K6 instantiated per N -- against the oracle on a full C1-sized frame, also with
+    pending overflow (K6), and on sampled pixels of a C2-sized view."""
+    _, cams, bg = synth.make_config("C1")
+    scene = synth.make_scene(31 + n_hidden, 400, n_hidden=n_hidden)
+    assert scene.w1.shape[1] == n_hidden
+    img_o, fl, _ = orc.render_frame(scene, cams[0], bg)
+    for limit in (0, 2):
+        res = gpu_render(scene, cams, bg, pending_limit=limit)
+        assert limit == 0 or res["stats"]["overflow_pixels"] > 0
+        c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+        assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.01 * c["n"], (limit, c)
+    big, cams2, bg2 = synth.make_config("C2")
+    scene2 = synth.make_scene(41 + n_hidden, 10000, n_hidden=n_hidden)
+    res = gpu_render(scene2, cams2, bg2)
+    px, py = sample_pixels(cams2[0], 1500, 3, seed=n_hidden)
+    out_o, fl2, _ = orc.render_pixels(scene2, cams2[0], px, py, bg2)
+    c = compare(res["img"][0][py, px], out_o, fl2)
+    assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c

@@ -45,11 +45,14 @@ def test_density_spec_examples(orc):
     assert abs(v - math.cos(1.0)) < 1e-15
 
 
-def test_integral_vs_bruteforce_quadrature(orc):
-    rng = np.random.default_rng(7)
+@pytest.mark.parametrize("N", [8, 4, 16, 32])
+def test_integral_vs_bruteforce_quadrature(orc, N):
+    """Eq. 8 closed form vs midpoint quadrature of Eq. 6, for the paper's width and the
+    other supported widths N_sigma."""
+    rng = np.random.default_rng(7 + N)
     worst = 0.0
-    for case in range(60):
-        mu, s, smax, W1, b1, W2, b2 = _rand_prim(rng, trained=case % 2 == 0)
+    for case in range(60 if N == 8 else 20):
+        mu, s, smax, W1, b1, W2, b2 = _rand_prim(rng, trained=case % 2 == 0, N=N)
         o = mu + rng.normal(size=3) * 5 * smax
         d = rng.normal(size=3); d /= np.linalg.norm(d)
         t_in = rng.uniform(0, 3 * smax)

@@ -10,8 +10,9 @@ ap.add_argument("--config", default="C3")
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--views", type=int, default=0)
 ap.add_argument("--plimit", type=int, default=0)
+ap.add_argument("--n-hidden", type=int, default=8)
 args = ap.parse_args()
-scene, cams, bg = synth.make_config(args.config, views=args.views or None)
+scene, cams, bg = synth.make_config(args.config, views=args.views or None, n_hidden=args.n_hidden)
 ns = types.SimpleNamespace(omega=scene.omega, sh_degree=scene.sh_degree)
 for f in snp.FIELDS:
     setattr(ns, f, torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).cuda())
