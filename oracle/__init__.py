@@ -66,6 +66,7 @@ def lib():
             L = C.CDLL(_LIB)
             dp = C.POINTER(C.c_double)
             L.orc_render_pixels.restype = C.c_int
+            L.orc_render_pixels_ex.restype = C.c_int
             L.orc_render_frame.restype = C.c_int
             L.orc_bin_sort.restype = C.c_int64
             L.orc_pixel_hits.restype = C.c_int64
@@ -126,9 +127,10 @@ def _camera(cam) -> _Camera:
 # ------------------------------------------------------------------- renderer
 
 def render_pixels(scene, cam, px, py, bg=(0.0, 0.0, 0.0), t_floor=T_FLOOR, nthreads=0,
-                  tie_eps=TIE_EPS, graze_eps=GRAZE_EPS):
+                  tie_eps=TIE_EPS, graze_eps=GRAZE_EPS, colour_per_ray=False):
     """Oracle RGBA (float64) for the listed pixels plus flags and per-pixel stats
-    (hits, composited, stop index)."""
+    (hits, composited, stop index).  colour_per_ray: SH colour at each pixel's ray
+    direction instead of at normalize(mu - o)."""
     L = lib()
     px = np.ascontiguousarray(px, np.int32)
     py = np.ascontiguousarray(py, np.int32)
@@ -139,20 +141,21 @@ def render_pixels(scene, cam, px, py, bg=(0.0, 0.0, 0.0), t_floor=T_FLOOR, nthre
     sref = _SceneRef(scene)
     cam_c = _camera(cam)
     bgv = np.asarray([float(np.float32(b)) for b in bg], np.float64)
-    r = L.orc_render_pixels(C.byref(sref.s), C.byref(cam_c), _p(bgv), C.c_double(float(np.float32(t_floor))),
-                            C.c_int64(n), _p(px), _p(py), _p(out), _p(flags), _p(stats),
-                            C.c_int(nthreads), C.c_double(tie_eps), C.c_double(graze_eps))
+    r = L.orc_render_pixels_ex(C.byref(sref.s), C.byref(cam_c), _p(bgv), C.c_double(float(np.float32(t_floor))),
+                               C.c_int64(n), _p(px), _p(py), _p(out), _p(flags), _p(stats),
+                               C.c_int(nthreads), C.c_double(tie_eps), C.c_double(graze_eps),
+                               C.c_int(1 if colour_per_ray else 0))
     if r != 0:
         raise ValueError(f"oracle render failed ({r}): invalid scene or out of memory")
     return out, flags, stats
 
 
 def render_frame(scene, cam, bg=(0.0, 0.0, 0.0), t_floor=T_FLOOR, nthreads=0,
-                 tie_eps=TIE_EPS, graze_eps=GRAZE_EPS):
+                 tie_eps=TIE_EPS, graze_eps=GRAZE_EPS, colour_per_ray=False):
     H, W = int(cam.height), int(cam.width)
     yy, xx = np.mgrid[0:H, 0:W]
     out, flags, stats = render_pixels(scene, cam, xx.ravel(), yy.ravel(), bg, t_floor, nthreads,
-                                      tie_eps, graze_eps)
+                                      tie_eps, graze_eps, colour_per_ray)
     return out.reshape(H, W, 4), flags.reshape(H, W), stats.reshape(H, W, 3)
 
 

@@ -323,10 +323,14 @@ int orc_validate(const orc_scene *sc)
  *   T-floor:  a transmittance after a composite with |T/floor - 1| < 1e-3
  * (R23: parity is scored on unflagged pixels; flagged counts are reported.)
  */
-int orc_render_pixels(const orc_scene *sc, const orc_camera *cam, const double bg[3],
-                      double t_floor, int64_t npix, const int32_t *px, const int32_t *py,
-                      double *out_rgba, int32_t *flags, int32_t *stats, int nthreads,
-                      double tie_eps, double graze_eps)
+/* colour_per_ray = 0: each primitive's colour is its SH at dir = normalize(mu - o), once
+ * per primitive and view (R14, the 3DGS convention).  colour_per_ray = 1 (SURVEY §8(f)
+ * 2c, the other reading of P:286): the SH is evaluated at the pixel's own unit ray
+ * direction d, once per (ray, hit). */
+int orc_render_pixels_ex(const orc_scene *sc, const orc_camera *cam, const double bg[3],
+                         double t_floor, int64_t npix, const int32_t *px, const int32_t *py,
+                         double *out_rgba, int32_t *flags, int32_t *stats, int nthreads,
+                         double tie_eps, double graze_eps, int colour_per_ray)
 {
     if (orc_validate(sc) != 0) return -1;
     const int64_t n = sc->n;
@@ -404,7 +408,13 @@ int orc_render_pixels(const orc_scene *sc, const orc_camera *cam, const double b
             for (int64_t h = 0; h < nh; ++h) {
                 const orc_prim *P = &prims[hits[h].id];
                 double k = hits[h].kappa;
-                for (int c = 0; c < 3; ++c) C[c] += T * k * P->rgb[c];
+                double ray_rgb[3];
+                const double *rgb = P->rgb;
+                if (colour_per_ray) {
+                    orc_sh_color(sc->sh_degree, sc->sh + (int64_t)48 * hits[h].id, d, ray_rgb);
+                    rgb = ray_rgb;
+                }
+                for (int c = 0; c < 3; ++c) C[c] += T * k * rgb[c];
                 T *= (1.0 - k);
                 ++ncomp;
                 if (fabs(T / t_floor - 1.0) < 1e-3) fl |= ORC_FLAG_TFLOOR;
@@ -456,6 +466,15 @@ int64_t orc_pixel_hits(const orc_scene *sc, const orc_camera *cam, int32_t px, i
         ++nh;
     }
     return nh;
+}
+
+int orc_render_pixels(const orc_scene *sc, const orc_camera *cam, const double bg[3],
+                      double t_floor, int64_t npix, const int32_t *px, const int32_t *py,
+                      double *out_rgba, int32_t *flags, int32_t *stats, int nthreads,
+                      double tie_eps, double graze_eps)
+{
+    return orc_render_pixels_ex(sc, cam, bg, t_floor, npix, px, py, out_rgba, flags, stats, nthreads,
+                                tie_eps, graze_eps, 0);
 }
 
 /* Full-frame convenience: every pixel in row-major order. */

@@ -296,3 +296,37 @@ def test_invalid_scene_rejected(orc, bad):
         sc.scales[2, 1] = 0
     with pytest.raises(ValueError):
         orc.render_pixels(sc, _axis_cam(), [0], [0])
+
+
+def test_colour_per_ray(orc):
+    """with colour_per_ray the SH colour is taken at each pixel's own
+    ray direction.  One primitive of constant density in front of an axis camera:
+    out_rgb / alpha is the colour, which must equal SH(d) for d built here from the
+    pinhole model (x + 0.5 - cx) / fx, (y + 0.5 - cy) / fy, 1 (SH basis pinned against
+    scipy in test_oracle_colour); at the pixel whose ray passes through mu the two modes
+    agree, elsewhere they differ; at SH degree 0 the modes give identical images."""
+    rng = np.random.default_rng(12)
+    sh = rng.normal(0, 0.3, (16, 3))
+    W, H, fx = 9, 7, 20.0
+    cam = _axis_cam(W, H, fx)
+    px0, py0 = 6, 2                     # mu on this pixel's ray
+    d0 = np.array([(px0 + 0.5 - W / 2.0) / fx, (py0 + 0.5 - H / 2.0) / fx, 1.0])
+    sc = _prims([dict(mu=5.0 * d0, s=(1.5, 1.5, 1.5), b2=0.4, sh=sh)])
+    sc.sh_degree = 3
+    ray, fl, _ = orc.render_frame(sc, cam, colour_per_ray=True)
+    prim, _, _ = orc.render_frame(sc, cam)
+    assert not fl.any()
+    yy, xx = np.mgrid[0:H, 0:W]
+    hit = ray[..., 3] > 0
+    assert hit.sum() > 20
+    for y, x in zip(yy[hit], xx[hit]):
+        d = np.array([(x + 0.5 - W / 2.0) / fx, (y + 0.5 - H / 2.0) / fx, 1.0])
+        d /= np.linalg.norm(d)
+        c = orc.sh_color(sh, d, 3)
+        assert np.allclose(ray[y, x, :3] / ray[y, x, 3], c, rtol=1e-12, atol=1e-12), (x, y)
+    assert np.allclose(ray[py0, px0], prim[py0, px0], rtol=1e-12, atol=1e-14)
+    assert np.abs(ray - prim)[hit].max() > 1e-3
+    sc.sh_degree = 0
+    a, _, _ = orc.render_frame(sc, cam, colour_per_ray=True)
+    b, _, _ = orc.render_frame(sc, cam)
+    assert np.array_equal(a, b)
