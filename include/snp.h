@@ -66,6 +66,13 @@ typedef struct snp_scene_s *snp_scene;  /* opaque, owned by the library */
  * pinned, and is valid once the caller has synchronised that stream. */
 enum { SNP_MEM_HOST = 0, SNP_MEM_DEVICE = 1, SNP_MEM_HOST_ASYNC = 2 };
 
+/* Colour of a primitive (snp_render_opts.colour_mode): its SH colour
+ * c = max(0, sum_lm Y_lm(dir) sh_lm + 0.5) evaluated at
+ *   SNP_COLOUR_PRIMITIVE: dir = normalize(mu - C), once per primitive and view (the 3DGS
+ *                         convention; R14) -- the default and the measured mode;
+ *   SNP_COLOUR_RAY:       dir = the pixel's own unit ray direction d, per (ray, hit). */
+enum { SNP_COLOUR_PRIMITIVE = 0, SNP_COLOUR_RAY = 1 };
+
 /* One primitive = 99 fp32 parameters for N = 8 ("99 parameters in total";
  * P:751 "41 parameters from its 8-neuron MLP"). */
 typedef struct {
@@ -104,6 +111,7 @@ typedef struct {
                                    keys beyond an undersized buffer are dropped (the frame is
                                    then incomplete) and snp_get_stats reports
                                    capacity_overflow = 1; a call with 1 resizes */
+    int32_t colour_mode;        /* snp_render: SNP_COLOUR_PRIMITIVE (0) or SNP_COLOUR_RAY */
 } snp_render_opts;
 
 typedef struct {

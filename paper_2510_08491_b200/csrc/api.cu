@@ -473,6 +473,8 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     if (opts->out_memory != SNP_MEM_HOST && opts->out_memory != SNP_MEM_DEVICE &&
         opts->out_memory != SNP_MEM_HOST_ASYNC)
         return fail(SNP_ERR_INVALID_ARGUMENT, "out_memory must be SNP_MEM_HOST, SNP_MEM_DEVICE or SNP_MEM_HOST_ASYNC");
+    if (opts->colour_mode != SNP_COLOUR_PRIMITIVE && opts->colour_mode != SNP_COLOUR_RAY)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "colour_mode must be SNP_COLOUR_PRIMITIVE or SNP_COLOUR_RAY");
     const bool host_out = opts->out_memory != SNP_MEM_DEVICE;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const size_t out_floats = (size_t)s->n_views * s->W * s->H * 4;
@@ -498,6 +500,9 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     s->render_dirty = true;
     RenderArgs a{};
     a.n_hidden = s->n_hidden;
+    a.colour_ray = opts->colour_mode == SNP_COLOUR_RAY ? 1 : 0;
+    a.sh = s->sh;
+    a.sh_degree = s->sh_degree;
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
     a.tiles_per_view = s->tiles_x * s->tiles_y;
@@ -522,7 +527,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     a.fallback_capacity = s->fallback_capacity;
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     a.counters = s->counters.p;
-    a.k5_grid = render_grid(s->n_hidden, s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
+    a.k5_grid = render_grid(s->n_hidden, a.colour_ray != 0, s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
         for (size_t k = 0; k < s->cams.size(); ++k) {

@@ -137,6 +137,50 @@ __device__ __forceinline__ Ray make_ray(const DevCam &cam, int x, int y) {
     return ray;
 }
 
+// Colour of primitive id for this pixel, as (_, r, g, b) like the record's kRecConicRgb
+// slot.  kRay = false: the record's colour (SH at normalize(mu - C), per primitive and
+// view, R14).  kRay = true: the SH of the scene's coefficients at the
+// pixel's own unit ray direction, c = max(0, sum_lm Y_lm(d) sh_lm + 0.5) (R15);
+// fp32 suffices, colour enters the pixel linearly.
+template <bool kRay>
+__device__ __forceinline__ float4 hit_rgb(const float4 *rec, const float *sh_all, int degree, uint32_t id,
+                                          const Ray &r) {
+    if (!kRay) return __ldg(rec + kRecConicRgb);
+    const float4 *sh4 = reinterpret_cast<const float4 *>(sh_all + (size_t)48 * id);
+    const float x = r.dhx, y = r.dhy, z = r.dhz;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    float Y[16];
+    Y[0] = 0.28209479177387814f;
+    Y[1] = -0.4886025119029199f * y;
+    Y[2] = 0.4886025119029199f * z;
+    Y[3] = -0.4886025119029199f * x;
+    Y[4] = 1.0925484305920792f * (x * y);
+    Y[5] = -1.0925484305920792f * (y * z);
+    Y[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+    Y[7] = -1.0925484305920792f * (x * z);
+    Y[8] = 0.5462742152960396f * (xx - yy);
+    Y[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+    Y[10] = 2.890611442640554f * (x * y) * z;
+    Y[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+    Y[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    Y[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+    Y[14] = 1.445305721320277f * z * (xx - yy);
+    Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+    const int nc = (degree + 1) * (degree + 1);
+    float acc[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {       // coefficients 4q/3 .. : 4 floats per load, RGB innermost
+        const float4 t = __ldg(sh4 + q);
+        const float v[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = 4 * q + u, i = f / 3, c = f % 3;
+            if (i < nc) acc[c] = fmaf(Y[i], v[u], acc[c]);
+        }
+    }
+    return make_float4(0.f, fmaxf(acc[0], 0.f), fmaxf(acc[1], 0.f), fmaxf(acc[2], 0.f));
+}
+
 // MUFU sin/cos take the argument through one FMUL by 1/(2 pi): for |phase| <= 60 rad
 // (|omega W1| <= 17 rad per unit radius, |omega b1| <= 30) that rounding costs <= 4e-6 rad,
 // i.e. <= 4e-6 * |W2 dt| per hidden unit -- well inside the 1e-4 pixel tolerance.
@@ -251,9 +295,9 @@ struct PixelState {
 // (strictly): every hit not yet inserted has t_in >= L (R19), so these are
 // exactly the next hits of the ray in (t_in, id) order (Eq. 4).  The
 // list is sorted, so they are popped from its head.
-template <int N>
+template <int N, bool kRay>
 __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, float L, float t_floor,
-                                     const float4 *recs) {
+                                     const float4 *recs, const RenderArgs &a, const Ray &ray) {
     const int tid = threadIdx.x;
     int n = pd.n;
     int h = pd.head;
@@ -261,7 +305,8 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
         const float t = sm.p_thi[h][tid];
         if (!(t < L)) break;
         const float kap = sm.p_kap[h][tid];
-        const float4 rgb = __ldg(recs + (size_t)sm.p_id[h][tid] * rec_f4(N) + kRecConicRgb);
+        const uint32_t pid = sm.p_id[h][tid];
+        const float4 rgb = hit_rgb<kRay>(recs + (size_t)pid * rec_f4(N), a.sh, a.sh_degree, pid, ray);
         const float w = ps.T * kap;
         ps.cr = fmaf(w, rgb.y, ps.cr);
         ps.cg = fmaf(w, rgb.z, ps.cg);
@@ -313,7 +358,7 @@ __device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimi
     ++pd.n;
 }
 
-template <int N>
+template <int N, bool kRay>
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
     constexpr int kStages = Cfg<N>::kStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -695,8 +740,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     ++ins_ecalls;
                     ins_enone += (pd.n == 0);
 #endif
-                    emit<N>(sm, ps, pd, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
-                         a.t_floor, recs);
+                    emit<N, kRay>(sm, ps, pd, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                                  a.t_floor, recs, a, ray);
 #ifdef SNP_INSTRUMENT
                     ins_emit += clock64() - _e0;
 #endif
@@ -798,7 +843,7 @@ __device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long 
 // are claimed one at a time as K5 queues them, and the CTA leaves once every K5 CTA has
 // exited and no entry is left.  overlap = false: K5 has completed; CTAs stride over the
 // queue and take the entries of this batch's views.
-template <int N>
+template <int N, bool kRay>
 __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb, int overlap) {
     if (!overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ FbSmem sm;
@@ -972,7 +1017,8 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
                 if (i < n && Tb >= a.t_floor) {
                     const int h = sm.idx[i];
                     const float kap = sm.k[h];
-                    const float4 rgb = __ldg(recs + (size_t)sm.id[h] * rec_f4(N) + kRecConicRgb);
+                    const float4 rgb = hit_rgb<kRay>(recs + (size_t)sm.id[h] * rec_f4(N), a.sh, a.sh_degree,
+                                                     sm.id[h], ray);
                     const float w = Tb * kap;
                     wr = fmaf(w, rgb.y, wr);
                     wg = fmaf(w, rgb.z, wg);
@@ -1035,7 +1081,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
                         bh = sm.t[w]; bl = sm.l[w]; bid = sm.id[w]; bk = sm.k[w];
                     }
                 if (bid == 0xffffffffu) break;
-                const float4 rgb = __ldg(recs + (size_t)bid * rec_f4(N) + kRecConicRgb);
+                const float4 rgb = hit_rgb<kRay>(recs + (size_t)bid * rec_f4(N), a.sh, a.sh_degree, bid, ray);
                 const float w = T * bk;
                 cr = fmaf(w, rgb.y, cr);
                 cg = fmaf(w, rgb.z, cg);
@@ -1108,49 +1154,63 @@ __global__ void __launch_bounds__(1024) k_tile_order(RenderArgs a, CamBatch cb, 
 }  // namespace
 
 namespace {
-template <int N>
+template <int N, bool kRay>
 int render_grid_n(int tiles) {
     static int resident = 0;   // persistent grid: every CTA that fits, all SMs
     if (!resident) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_render<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<N>));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N>, kThreads, sizeof(Smem<N>));
+        cudaFuncSetAttribute(k_render<N, kRay>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<N>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N, kRay>, kThreads, sizeof(Smem<N>));
         resident = std::max(1, sms) * std::max(1, per_sm);
     }
     return std::min(tiles, resident);
 }
 
-template <int N>
+template <int N, bool kRay>
 cudaError_t launch_render_n(const RenderArgs &a, const CamBatch &cams, int tiles, cudaStream_t st) {
     static bool attr_set = false;
     const int smem = (int)sizeof(Smem<N>);
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_render<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    k_render<N><<<render_grid_n<N>(tiles), kThreads, smem, st>>>(a, cams);
+    k_render<N, kRay><<<render_grid_n<N, kRay>(tiles), kThreads, smem, st>>>(a, cams);
     return cudaGetLastError();
 }
 
-template <int N>
+template <int N, bool kRay>
 cudaError_t launch_fallback_n(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
     static int resident = 0;   // every CTA that fits, all SMs (the queue loop strides by the grid)
     if (!resident) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback<N>, kFbThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback<N, kRay>, kFbThreads, 0);
         resident = std::max(1, sms) * std::max(1, per_sm);
     }
     const int overlap = n_batches == 1 ? 1 : 0;
     for (int i = 0; i < n_batches; ++i) {
-        cudaError_t e = launch_hi(k_fallback<N>, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i], overlap);
+        cudaError_t e = launch_hi(k_fallback<N, kRay>, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i], overlap);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_render_w(const RenderArgs &a, const CamBatch &cams, int tiles, cudaStream_t st) {
+    return a.colour_ray ? launch_render_n<N, true>(a, cams, tiles, st) : launch_render_n<N, false>(a, cams, tiles, st);
+}
+template <int N>
+int render_grid_w(bool ray, int tiles) {
+    return ray ? render_grid_n<N, true>(tiles) : render_grid_n<N, false>(tiles);
+}
+template <int N>
+cudaError_t launch_fallback_w(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
+    return a.colour_ray ? launch_fallback_n<N, true>(a, cams, n_batches, st)
+                        : launch_fallback_n<N, false>(a, cams, n_batches, st);
 }
 }  // namespace
 
@@ -1162,20 +1222,20 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
         if (e != cudaSuccess) return e;
     }
     switch (a.n_hidden) {
-        case 4: return launch_render_n<4>(a, cams, tiles, st);
-        case 8: return launch_render_n<8>(a, cams, tiles, st);
-        case 16: return launch_render_n<16>(a, cams, tiles, st);
-        case 32: return launch_render_n<32>(a, cams, tiles, st);
+        case 4: return launch_render_w<4>(a, cams, tiles, st);
+        case 8: return launch_render_w<8>(a, cams, tiles, st);
+        case 16: return launch_render_w<16>(a, cams, tiles, st);
+        case 32: return launch_render_w<32>(a, cams, tiles, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int render_grid(int n_hidden, int tiles) {
+int render_grid(int n_hidden, bool colour_ray, int tiles) {
     switch (n_hidden) {
-        case 4: return render_grid_n<4>(tiles);
-        case 16: return render_grid_n<16>(tiles);
-        case 32: return render_grid_n<32>(tiles);
-        default: return render_grid_n<8>(tiles);
+        case 4: return render_grid_w<4>(colour_ray, tiles);
+        case 16: return render_grid_w<16>(colour_ray, tiles);
+        case 32: return render_grid_w<32>(colour_ray, tiles);
+        default: return render_grid_w<8>(colour_ray, tiles);
     }
 }
 
@@ -1186,10 +1246,10 @@ cudaError_t launch_tile_order(const RenderArgs &a, const CamBatch &cams, uint32_
 
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
     switch (a.n_hidden) {
-        case 4: return launch_fallback_n<4>(a, cams, n_batches, st);
-        case 8: return launch_fallback_n<8>(a, cams, n_batches, st);
-        case 16: return launch_fallback_n<16>(a, cams, n_batches, st);
-        case 32: return launch_fallback_n<32>(a, cams, n_batches, st);
+        case 4: return launch_fallback_w<4>(a, cams, n_batches, st);
+        case 8: return launch_fallback_w<8>(a, cams, n_batches, st);
+        case 16: return launch_fallback_w<16>(a, cams, n_batches, st);
+        case 32: return launch_fallback_w<32>(a, cams, n_batches, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -170,6 +170,9 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
 
 struct RenderArgs {
     int32_t n_hidden;              // N_sigma (hidden_supported): selects the kernel instantiation
+    int32_t colour_ray;            // 1: SH colour at each pixel's ray direction (SNP_COLOUR_RAY)
+    const float *sh;               // scene SH coefficients [n][16][3] (per-ray colour)
+    int32_t sh_degree;
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;
@@ -200,6 +203,6 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
 // CTAs leave, take overflowed pixels as K5 queues them and end once every K5 CTA has
 // exited.  With several batches it runs after all of them.
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
-int render_grid(int n_hidden, int tiles);   // K5's persistent grid for `tiles` work units
+int render_grid(int n_hidden, bool colour_ray, int tiles);   // K5's persistent grid for `tiles` work units
 
 }  // namespace snp

@@ -23,6 +23,8 @@ STATUS = {0: "SNP_OK", 1: "SNP_ERR_INVALID_ARGUMENT", 2: "SNP_ERR_OUT_OF_MEMORY"
 SNP_MEM_HOST = 0
 SNP_MEM_DEVICE = 1
 SNP_MEM_HOST_ASYNC = 2   # snp_render output only: copy enqueued on the stream, no synchronisation
+SNP_COLOUR_PRIMITIVE = 0  # colour_mode: SH at normalize(mu - C) per primitive and view (default)
+SNP_COLOUR_RAY = 1        # colour_mode: SH at each pixel's ray direction
 
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
@@ -50,7 +52,7 @@ class Camera(C.Structure):
 class RenderOpts(C.Structure):
     _fields_ = [("background", C.c_float * 3), ("transmittance_floor", C.c_float),
                 ("tile_row_begin", C.c_int32), ("tile_row_stride", C.c_int32),
-                ("out_memory", C.c_int32), ("sync_check", C.c_int32)]
+                ("out_memory", C.c_int32), ("sync_check", C.c_int32), ("colour_mode", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -168,9 +170,10 @@ def make_cameras(cams):
 
 
 def make_opts(background=(0.0, 0.0, 0.0), transmittance_floor=1e-4, tile_row_begin=0, tile_row_stride=1,
-              out_memory=SNP_MEM_DEVICE, sync_check=1):
+              out_memory=SNP_MEM_DEVICE, sync_check=1, colour_mode=0):
     return RenderOpts((C.c_float * 3)(*[float(b) for b in background]), float(transmittance_floor),
-                      int(tile_row_begin), int(tile_row_stride), int(out_memory), int(sync_check))
+                      int(tile_row_begin), int(tile_row_stride), int(out_memory), int(sync_check),
+                      int(colour_mode))
 
 
 def project(h, cams, stream=None):

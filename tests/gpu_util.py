@@ -15,7 +15,7 @@ def torch_scene(scene):
 
 
 def gpu_render(scene, cams, bg=(0.0, 0.0, 0.0), t_floor=1e-4, stripe=(0, 1), pending_limit=0,
-               device_scene=True, host_out=False, binning=False, sync_check=1, repeat=1):
+               device_scene=True, host_out=False, binning=False, sync_check=1, repeat=1, colour_mode=0):
     import torch
     from paper_2510_08491_b200 import snp
     src = torch_scene(scene) if device_scene else scene
@@ -25,8 +25,8 @@ def gpu_render(scene, cams, bg=(0.0, 0.0, 0.0), t_floor=1e-4, stripe=(0, 1), pen
             snp.set_pending_limit(h, pending_limit)
         V, H, W = len(cams), int(cams[0].height), int(cams[0].width)
         mem = snp.SNP_MEM_HOST if host_out else snp.SNP_MEM_DEVICE
-        first = snp.make_opts(bg, t_floor, stripe[0], stripe[1], mem, 1)   # sizes the key buffer
-        opts = snp.make_opts(bg, t_floor, stripe[0], stripe[1], mem, sync_check)
+        first = snp.make_opts(bg, t_floor, stripe[0], stripe[1], mem, 1, colour_mode)   # sizes the key buffer
+        opts = snp.make_opts(bg, t_floor, stripe[0], stripe[1], mem, sync_check, colour_mode)
         if host_out:
             out = np.full((V, H, W, 4), np.nan, np.float32)
         else:

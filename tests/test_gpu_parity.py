@@ -425,3 +425,29 @@ def test_hidden_widths(orc, n_hidden):
     out_o, fl2, _ = orc.render_pixels(scene2, cams2[0], px, py, bg2)
     c = compare(res["img"][0][py, px], out_o, fl2)
     assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
+
+
+@pytest.mark.parametrize("n_hidden", [8, 16])
+def test_colour_per_ray(orc, n_hidden):
+    """SNP_COLOUR_RAY: SH colour at each pixel's ray direction, in K5's
+    blend and in K6 (forced pending overflow), against the oracle's per-ray mode; a C1
+    frame at every SH degree and sampled pixels of the full C3 view."""
+    from paper_2510_08491_b200 import snp
+    _, cams, bg = synth.make_config("C1")
+    scene = synth.make_scene(51, 400, n_hidden=n_hidden)
+    for deg in (3, 1, 0):
+        scene.sh_degree = deg
+        img_o, fl, _ = orc.render_frame(scene, cams[0], bg, colour_per_ray=True)
+        for limit in (0, 2):
+            res = gpu_render(scene, cams, bg, pending_limit=limit, colour_mode=snp.SNP_COLOUR_RAY)
+            c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+            assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.01 * c["n"], (deg, limit, c)
+    prim = gpu_render(scene, cams, bg)["img"][0]       # degree 0: the two modes coincide
+    assert np.abs(prim - res["img"][0]).max() <= 1e-6
+    if n_hidden == 8:
+        scene3, cams3, bg3 = synth.make_config("C3")
+        res = gpu_render(scene3, cams3, bg3, colour_mode=snp.SNP_COLOUR_RAY)
+        px, py = sample_pixels(cams3[0], 1500, 3, seed=5)
+        out_o, fl3, _ = orc.render_pixels(scene3, cams3[0], px, py, bg3, colour_per_ray=True)
+        c = compare(res["img"][0][py, px], out_o, fl3)
+        assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
