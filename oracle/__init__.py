@@ -48,14 +48,15 @@ def build(force: bool = False) -> str:
 class _Scene(C.Structure):
     _fields_ = [("n", C.c_int64), ("n_hidden", C.c_int32), ("sh_degree", C.c_int32),
                 ("omega", C.c_double)] + [(f, C.c_void_p) for f in
-                                          ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh")]
+                                          ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh",
+                                           "w_t")]
 
 
 class _Camera(C.Structure):
     _fields_ = [("R_wc", C.c_double * 9), ("C_w", C.c_double * 3), ("fx", C.c_double),
                 ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
                 ("width", C.c_int32), ("height", C.c_int32), ("t_near", C.c_double),
-                ("t_far", C.c_double)]
+                ("t_far", C.c_double), ("xi_t", C.c_double)]
 
 
 def lib():
@@ -105,8 +106,12 @@ class _SceneRef:
     def __init__(self, scene):
         self.arrs = [_f32(getattr(scene, f)) for f in
                      ("centers", "rotations", "scales", "w1", "b1", "w2", "b2", "sh")]
+        w_t = getattr(scene, "w_t", None)   # temporal weights [n, N] (R24) or None
+        if w_t is not None:
+            self.arrs.append(_f32(w_t))
         self.s = _Scene(scene.n, int(scene.w1.shape[1]), int(scene.sh_degree), float(scene.omega),
-                        *[a.ctypes.data for a in self.arrs])
+                        *[a.ctypes.data for a in self.arrs[:8]],
+                        self.arrs[8].ctypes.data if w_t is not None else None)
 
 
 def _camera(cam) -> _Camera:
@@ -121,6 +126,7 @@ def _camera(cam) -> _Camera:
     c.fx, c.fy, c.cx, c.cy = f32(cam.fx), f32(cam.fy), f32(cam.cx), f32(cam.cy)
     c.width, c.height = int(cam.width), int(cam.height)
     c.t_near, c.t_far = f32(cam.t_near), f32(cam.t_far)
+    c.xi_t = f32(getattr(cam, "xi_t", 0.0))
     return c
 
 

@@ -52,6 +52,7 @@ typedef struct {
     const float *w2;         /* [n][N] */
     const float *b2;         /* [n] */
     const float *sh;         /* [n][16][3] */
+    const float *w_t;        /* [n][N] temporal weights W_t, or NULL (static scene) */
 } orc_scene;
 
 typedef struct {
@@ -60,6 +61,7 @@ typedef struct {
     double fx, fy, cx, cy;
     int32_t width, height;
     double t_near, t_far;
+    double xi_t;     /* timestamp xi_t in [0, 1] of this view (temporal scenes, R24) */
 } orc_camera;
 
 /* ------------------------------------------------------------------ geometry */
@@ -270,7 +272,11 @@ static int cmp_hit(const void *pa, const void *pb)
     return (a->id < b->id) ? -1 : (a->id > b->id);
 }
 
-static void load_prim(const orc_scene *sc, int64_t i, const double o[3], orc_prim *p)
+/* Temporal scenes ("augmenting the network's input dimensions", appendix
+ * "Dynamic scenes" f(x, xi_t) = W2 cos(W1 x + xi_t W_t + b1) + b2; reading R24): time
+ * is a fourth network input, so at the view's timestamp the phase of unit k is
+ * omega (W1_k . x^ + xi_t W_t,k + b1_k), i.e. b1_k + xi_t W_t,k takes the place of b1_k. */
+static void load_prim(const orc_scene *sc, int64_t i, const double o[3], double xi_t, orc_prim *p)
 {
     int N = sc->n_hidden;
     double q[4];
@@ -286,6 +292,7 @@ static void load_prim(const orc_scene *sc, int64_t i, const double o[3], orc_pri
     for (int k = 0; k < 3 * N; ++k) p->W1[k] = sc->w1[(int64_t)3 * N * i + k];
     for (int k = 0; k < N; ++k) {
         p->b1[k] = sc->b1[(int64_t)N * i + k];
+        if (sc->w_t) p->b1[k] += xi_t * (double)sc->w_t[(int64_t)N * i + k];
         p->W2[k] = sc->w2[(int64_t)N * i + k];
     }
     p->b2 = sc->b2[i];
@@ -339,7 +346,7 @@ int orc_render_pixels_ex(const orc_scene *sc, const orc_camera *cam, const doubl
     double *geo = (double *)malloc(sizeof(double) * 4 * (size_t)(n > 0 ? n : 1));
     if (!prims || !geo) { free(prims); free(geo); return -2; }
     for (int64_t i = 0; i < n; ++i) {
-        load_prim(sc, i, cam->C_w, &prims[i]);
+        load_prim(sc, i, cam->C_w, cam->xi_t, &prims[i]);
         /* compact copy of (mu, smax) so the reject loop streams 32 B per primitive */
         geo[4 * i + 0] = prims[i].mu[0];
         geo[4 * i + 1] = prims[i].mu[1];

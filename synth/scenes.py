@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import dataclasses
 import struct
-from typing import List, Tuple
+from typing import Optional, List, Tuple
 
 import numpy as np
 
@@ -41,6 +41,7 @@ class Scene:
     sh: np.ndarray         # [n,16,3] f32, coefficient-major, RGB innermost
     omega: float = OMEGA
     sh_degree: int = 3
+    w_t: Optional[np.ndarray] = None   # [n,N] f32 temporal weights W_t (appendix "Dynamic scenes"), or None
 
     @property
     def n(self) -> int:
@@ -85,6 +86,7 @@ class Camera:
     height: int
     t_near: float = 0.01   # S:295 defaults
     t_far: float = 1e4
+    xi_t: float = 0.0      # timestamp of this view (temporal scenes only)
 
 
 def empty_scene(n_hidden: int = N_HIDDEN) -> Scene:
