@@ -151,6 +151,18 @@ snp_status snp_update_scene(snp_scene s, const snp_scene_desc *desc, void *cuda_
  * `cams` is host memory, read before return. */
 snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, void *cuda_stream);
 
+/* Temporal scenes (appendix "Dynamic scenes"; R24): time is
+ * a fourth input of each primitive's network, so at a view's timestamp xi_t the phase of
+ * hidden unit k is omega (W1_k . x^ + xi_t W_t,k + b1_k).  snp_set_temporal attaches the
+ * temporal weights w_t [n][N] (host or device memory as `memory` says, copied; validated
+ * finite, SNP_ERR_INVALID_ARGUMENT otherwise) -- NULL detaches them (static scene).
+ * snp_project_at is snp_project with one timestamp per view (xi_t: host [n_views], read
+ * before return; NULL = all 0).  The time-dependent colour model of the appendix is not
+ * specified closely enough to implement: pass the colour at the view's time as SH. */
+snp_status snp_set_temporal(snp_scene s, const float *w_t, int32_t memory, void *cuda_stream);
+snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, const float *xi_t,
+                          void *cuda_stream);
+
 /* K2-K4: keys (view | tile | depth) in primitive order, stable LSD radix sort,
  * per-(view, tile) ranges.  Uses opts->tile_row_begin/stride and sync_check. */
 snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_stream);

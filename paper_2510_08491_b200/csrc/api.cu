@@ -72,6 +72,8 @@ struct snp_scene_s {
     DevBuf<short4> rects;
     DevBuf<uint32_t> depth;
     DevBuf<float4> records;
+    DevBuf<float> w_t;               // temporal weights [n][N] (temporal scenes only)
+    bool temporal = false;
     // binning
     int32_t row_begin = 0, row_stride = 1, stripe_rows = 0;
     DevBuf<uint64_t> keys0, keys1;
@@ -129,6 +131,7 @@ void fill_args(snp_scene s, ProjectArgs &a) {
     a.omega = s->omega;
     a.centers = s->centers; a.rotations = s->rotations; a.scales = s->scales;
     a.w1 = s->w1; a.b1 = s->b1; a.w2 = s->w2; a.b2 = s->b2; a.sh = s->sh;
+    a.w_t = s->temporal ? s->w_t.p : nullptr;
     a.tiles_x = s->tiles_x; a.tiles_y = s->tiles_y;
     a.rects = s->rects.p; a.depth = s->depth.p; a.records = s->records.p;
     a.counters = s->counters.p;
@@ -267,6 +270,45 @@ snp_status snp_update_scene(snp_scene s, const snp_scene_desc *d, void *cuda_str
 }
 
 snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, void *cuda_stream) {
+    return snp_project_at(s, cams, n_views, nullptr, cuda_stream);
+}
+
+snp_status snp_set_temporal(snp_scene s, const float *w_t, int32_t memory, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (memory != SNP_MEM_HOST && memory != SNP_MEM_DEVICE)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "memory must be SNP_MEM_HOST or SNP_MEM_DEVICE");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if (s->join_pending) {   // K1b may still read the weights being replaced
+        SNP_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+        s->join_pending = false;
+    }
+    s->state = kCreated;   // the records change: project again
+    if (!w_t) {
+        s->temporal = false;
+        return SNP_OK;
+    }
+    const int64_t count = s->n * s->n_hidden;
+    SNP_CUDA(s->w_t.ensure((size_t)std::max<int64_t>(count, 4)));
+    SNP_CUDA(cudaMemcpyAsync(s->w_t.p, w_t, sizeof(float) * count,
+                             memory == SNP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    const int init[2] = {0, 0x7fffffff};
+    SNP_CUDA(cudaMemcpyAsync(s->flag.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+    SNP_CUDA(launch_validate_finite(s->w_t.p, count, s->flag.p, st));
+    SNP_CUDA(cudaMemcpyAsync(s->h_flag, s->flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    SNP_CUDA(cudaStreamSynchronize(st));
+    if (s->h_flag[0]) {
+        s->temporal = false;
+        return fail(SNP_ERR_INVALID_ARGUMENT,
+                    "non-finite temporal weight at primitive " + std::to_string(s->h_flag[1] / s->n_hidden));
+    }
+    s->temporal = true;
+    return SNP_OK;
+}
+
+snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, const float *xi_t,
+                          void *cuda_stream) {
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -281,6 +323,7 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
                   std::isfinite(c.cy) && c.t_near >= 0.f && c.t_far > c.t_near && std::isfinite(c.t_far);
         for (int k = 0; k < 9; ++k) ok = ok && std::isfinite(c.R_wc[k]);
         for (int k = 0; k < 3; ++k) ok = ok && std::isfinite(c.C_w[k]);
+        if (xi_t) ok = ok && std::isfinite(xi_t[v]);
         if (!ok) return fail(SNP_ERR_INVALID_ARGUMENT, "invalid camera " + std::to_string(v));
     }
     cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -311,6 +354,7 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
             dc.ify = 1.0 / (double)c.fy;
             dc.W = c.width; dc.H = c.height;
             dc.t_near = c.t_near; dc.t_far = c.t_far;
+            dc.xi_t = xi_t ? xi_t[v0 + k] : 0.f;
         }
         s->cams.push_back(cb);
     }
@@ -564,6 +608,7 @@ snp_status snp_destroy(snp_scene s) {
     s->rects.release();
     s->depth.release();
     s->records.release();
+    s->w_t.release();
     s->keys0.release();
     s->keys1.release();
     s->vals0.release();

@@ -197,6 +197,23 @@ __global__ void k_validate(ProjectArgs a, int *bad) {
 
 }  // namespace
 
+namespace {
+__global__ void k_validate_finite(const float *v, int64_t count, int *bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(v[i])) {
+            atomicOr(bad, 1);
+            atomicMin(bad + 1, (int)(i < 0x7fffffff ? i : 0x7fffffff));
+        }
+}
+}  // namespace
+
+cudaError_t launch_validate_finite(const float *v, int64_t count, int *d_bad, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+    k_validate_finite<<<(unsigned)blocks, 256, 0, st>>>(v, count, d_bad);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bin_geom(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
     if (a.n == 0) return cudaSuccess;
     k_bin_geom<<<(unsigned)((a.n + kGeomThreads - 1) / kGeomThreads), kGeomThreads, 0, st>>>(a, cams);

@@ -321,6 +321,13 @@ __device__ __forceinline__ void record_one(const ProjectArgs &a, const CamBatch 
             }
             const float4 tb = b1v[g];
             b1[0] = tb.x; b1[1] = tb.y; b1[2] = tb.z; b1[3] = tb.w;
+            if (a.w_t) {   // temporal scene: b1 + xi_t W_t at this view's timestamp (R24)
+                const float4 wt = __ldg(reinterpret_cast<const float4 *>(a.w_t + (size_t)N * i) + g);
+                b1[0] = fmaf(cam.xi_t, wt.x, b1[0]);
+                b1[1] = fmaf(cam.xi_t, wt.y, b1[1]);
+                b1[2] = fmaf(cam.xi_t, wt.z, b1[2]);
+                b1[3] = fmaf(cam.xi_t, wt.w, b1[3]);
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 rec[kRecUnits + 4 * g + k] = make_float4(scf * w1[3 * k], scf * w1[3 * k + 1], scf * w1[3 * k + 2],

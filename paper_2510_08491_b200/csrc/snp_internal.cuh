@@ -72,6 +72,7 @@ struct DevCam {
     int32_t W, H;
     float t_near, t_far;
     double ifx, ify;  // 1 / fx, 1 / fy (host-computed: no FP64 division per pixel ray)
+    float xi_t;       // timestamp of this view (temporal scenes, R24)
 };
 
 struct CamBatch {
@@ -110,6 +111,7 @@ struct ProjectArgs {
     int32_t sh_degree;
     float omega;
     const float *centers, *rotations, *scales, *w1, *b1, *w2, *b2, *sh;
+    const float *w_t;       // [n][N] temporal weights, or nullptr (static scene)
     int32_t tiles_x, tiles_y;
     short4 *rects;          // [V*n] tile rect or (-1,-1,-1,-1)
     uint32_t *depth;        // [V*n] fp32 bits of the depth lower bound
@@ -119,6 +121,7 @@ struct ProjectArgs {
 
 // ---- host-side launchers (each .cu owns its kernels) ----
 cudaError_t launch_validate(const ProjectArgs &a, int *d_bad, cudaStream_t st);
+cudaError_t launch_validate_finite(const float *v, int64_t count, int *d_bad, cudaStream_t st);
 // K1a: cull + tile rect + depth key (critical path).  K1b: render records of the
 // visible pairs (reads K1a's rects; may run concurrently with K2-K4).
 cudaError_t launch_bin_geom(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st);

@@ -28,7 +28,7 @@ SNP_COLOUR_RAY = 1        # colour_mode: SH at each pixel's ray direction
 
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
-           "snp_set_pending_limit", "snp_get_debug_counters")
+           "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at")
 
 
 class SnpError(RuntimeError):
@@ -87,6 +87,8 @@ def lib():
             L.snp_get_binning.argtypes = [vp, vp, vp, vp, vp, C.c_int64, C.POINTER(C.c_int64), vp, vp]
             L.snp_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
+            L.snp_set_temporal.argtypes = [vp, vp, C.c_int32, vp]
+            L.snp_project_at.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp, vp]
             L.snp_get_debug_counters.argtypes = [vp, vp, C.c_int32, vp]
             for f in EXPORTS:
                 if f not in ("snp_version", "snp_last_error"):
@@ -176,9 +178,34 @@ def make_opts(background=(0.0, 0.0, 0.0), transmittance_floor=1e-4, tile_row_beg
                       int(colour_mode))
 
 
-def project(h, cams, stream=None):
+def _times(xi_t, n):
+    if xi_t is None:
+        return None
+    t = np.ascontiguousarray(np.broadcast_to(np.asarray(xi_t, np.float32), (n,)))
+    return t
+
+
+def project(h, cams, stream=None, xi_t=None):
+    """K1 for the cameras; xi_t (temporal scenes): one timestamp per view, or None."""
     arr = cams if isinstance(cams, C.Array) else make_cameras(cams)
-    _check(lib().snp_project(h, arr, len(arr), _stream(stream)))
+    t = _times(xi_t, len(arr))
+    if t is None:
+        _check(lib().snp_project(h, arr, len(arr), _stream(stream)))
+    else:
+        _check(lib().snp_project_at(h, arr, len(arr), t.ctypes.data_as(C.c_void_p), _stream(stream)))
+
+
+def set_temporal(h, w_t, stream=None):
+    """Attach temporal weights w_t [n, N] (numpy = host, torch CUDA = device), or None."""
+    if w_t is None:
+        _check(lib().snp_set_temporal(h, None, SNP_MEM_HOST, _stream(stream)))
+        return
+    if _is_device(w_t):
+        w = w_t.contiguous().float()
+        _check(lib().snp_set_temporal(h, _ptr(w), SNP_MEM_DEVICE, _stream(stream)))
+    else:
+        w = np.ascontiguousarray(w_t, dtype=np.float32)
+        _check(lib().snp_set_temporal(h, w.ctypes.data_as(C.c_void_p), SNP_MEM_HOST, _stream(stream)))
 
 
 def bin_sort(h, opts, stream=None):
@@ -189,9 +216,14 @@ def render(h, opts, out, stream=None):
     _check(lib().snp_render(h, C.byref(opts), _ptr(out), _stream(stream)))
 
 
-def render_views(h, cams, opts, out, stream=None):
+def render_views(h, cams, opts, out, stream=None, xi_t=None):
     arr = cams if isinstance(cams, C.Array) else make_cameras(cams)
-    _check(lib().snp_render_views(h, arr, len(arr), C.byref(opts), _ptr(out), _stream(stream)))
+    if xi_t is None:
+        _check(lib().snp_render_views(h, arr, len(arr), C.byref(opts), _ptr(out), _stream(stream)))
+    else:
+        project(h, arr, stream, xi_t)
+        bin_sort(h, opts, stream)
+        render(h, opts, out, stream)
 
 
 def destroy(h):

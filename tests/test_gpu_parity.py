@@ -451,3 +451,40 @@ def test_colour_per_ray(orc, n_hidden):
         out_o, fl3, _ = orc.render_pixels(scene3, cams3[0], px, py, bg3, colour_per_ray=True)
         c = compare(res["img"][0][py, px], out_o, fl3)
         assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
+
+
+def test_temporal_views(orc):
+    """Temporal scenes: one timestamp per view folded into K1b's
+    records (omega (b1 + xi_t W_t)); a 3-view batch at xi_t = 0, 0.4, 1 against the
+    oracle, detaching the weights restores the static image, non-finite weights are
+    rejected with the primitive's index."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene, cams, bg = synth.make_config("C1")
+    rng = np.random.default_rng(17)
+    scene.w_t = rng.uniform(-1, 1, (scene.n, scene.n_hidden)).astype(np.float32)
+    c = cams[0]
+    cams = synth.orbit_cameras(3, 4.0, c.width, c.height, c.fx, elev_deg=(10, 35))
+    times = [0.0, 0.4, 1.0]
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        snp.set_temporal(h, scene.w_t)
+        out = torch.full((3, c.height, c.width, 4), float("nan"), device="cuda")
+        snp.render_views(h, cams, snp.make_opts(bg), out, xi_t=times)
+        img = out.cpu().numpy()
+        snp.set_temporal(h, None)
+        snp.render_views(h, cams, snp.make_opts(bg), out)
+        static = out.cpu().numpy()
+        bad = scene.w_t.copy()
+        bad[37, 2] = np.inf
+        with pytest.raises(snp.SnpError, match="primitive 37"):
+            snp.set_temporal(h, bad)
+    finally:
+        snp.destroy(h)
+    for v, t in enumerate(times):
+        cams[v].xi_t = t
+        img_o, fl, _ = orc.render_frame(scene, cams[v], bg)
+        cmp_ = compare(img[v].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+        assert cmp_["max_unflagged"] <= TOL and cmp_["n_flagged"] <= 0.01 * cmp_["n"], (v, cmp_)
+    assert np.array_equal(static[0], img[0]) and np.abs(static[2] - img[2]).max() > 1e-3

@@ -25,7 +25,7 @@ agg = collections.OrderedDict()
 for r in rows[1:]:
     k = r[ki].split("(")[0].split("::")[-1].strip()
     agg.setdefault(k, []).append(float(r[vi].replace(",", "")))
-frames = max(1, len(agg.get("k_render", [1])))
+frames = max(1, len(next((v for k, v in agg.items() if k.startswith("k_render")), [1])))
 shutil.copy(os.path.join(src, f"{tag}_launches.csv"), os.path.join(dst, f"{tag}_launches_c3.csv"))
 tot = sum(sum(v) for k, v in agg.items() if k != "k_validate") / frames
 out = [f"# Round {tag[1:]} -- kernel launch list of one C3 frame (ncu gpu__time_duration, --clock-control none)", "",
