@@ -18,7 +18,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
 # K1's FP64 binning geometry follows a fixed operation order without FMA
 # contraction so it is bit-exact with the binning definition.
 PER_FILE = {"project.cu": ["-fmad=false"]}
-SOURCES = ["api.cu", "project.cu", "records.cu", "binning.cu", "sort.cu", "render.cu"]
+SOURCES = ["api.cu", "project.cu", "records.cu", "binning.cu", "sort.cu", "render.cu", "backward.cu"]
 
 
 def nvcc() -> str:
@@ -37,7 +37,8 @@ def _stale(out, deps):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, "snp_internal.cuh"), os.path.join(ROOT, "include", "snp.h")]
+    headers = [os.path.join(CSRC, "snp_internal.cuh"), os.path.join(CSRC, "hit.cuh"),
+               os.path.join(ROOT, "include", "snp.h")]
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)

@@ -588,6 +588,45 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     return SNP_OK;
 }
 
+snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
+                               float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!opts || !grad_rgba || !grad_w1 || !grad_b1 || !grad_w2 || !grad_b2 || !grad_sh)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "opts or a gradient pointer is NULL");
+    if (s->state < kBinned) return fail(SNP_ERR_BAD_STATE, "snp_render_backward before snp_bin_sort");
+    if (s->row_begin != 0 || s->row_stride != 1)
+        return fail(SNP_ERR_UNSUPPORTED, "snp_render_backward needs the whole image (tile rows 0, 1)");
+    if (opts->colour_mode != SNP_COLOUR_PRIMITIVE && opts->colour_mode != SNP_COLOUR_RAY)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "colour_mode must be SNP_COLOUR_PRIMITIVE or SNP_COLOUR_RAY");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    RenderArgs a{};
+    a.n_hidden = s->n_hidden;
+    a.colour_ray = opts->colour_mode == SNP_COLOUR_RAY ? 1 : 0;
+    a.sh = s->sh;
+    a.sh_degree = s->sh_degree;
+    a.scales = s->scales;
+    a.tiles_x = s->tiles_x;
+    a.tiles_y = s->tiles_y;
+    a.tiles_per_view = s->tiles_x * s->tiles_y;
+    a.tile_bits = s->tile_bits;
+    a.row_begin = 0;
+    a.row_stride = 1;
+    a.stripe_rows = s->stripe_rows;
+    a.n = s->n;
+    a.records = s->records.p;
+    a.keys = s->sorted_idx ? s->keys1.p : s->keys0.p;
+    a.vals = s->sorted_idx ? s->vals1.p : s->vals0.p;
+    a.ranges = s->ranges.p;
+    for (int c = 0; c < 3; ++c) a.bg[c] = opts->background[c];
+    a.t_floor = opts->transmittance_floor;
+    a.counters = s->counters.p;
+    BackwardGrads g{grad_w1, grad_b1, grad_w2, grad_b2, grad_sh};
+    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, st));
+    return SNP_OK;
+}
+
 snp_status snp_render_views(snp_scene s, const snp_camera *cams, int32_t n_views, const snp_render_opts *opts,
                             float *out_rgba, void *cuda_stream) {
     snp_status r = snp_project(s, cams, n_views, cuda_stream);

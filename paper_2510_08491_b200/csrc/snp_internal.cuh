@@ -102,7 +102,7 @@ __host__ __device__ constexpr int rec_w2(int N) { return kRecUnits + N; }
 // by K2's last block.  No memset node in a project -> bin_sort -> render frame.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
                kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
-               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12,
+               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12, kCntBwdSkipped = 14,
                kNumCounters = 48 };   // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
@@ -176,6 +176,7 @@ struct RenderArgs {
     int32_t colour_ray;            // 1: SH colour at each pixel's ray direction (SNP_COLOUR_RAY)
     const float *sh;               // scene SH coefficients [n][16][3] (per-ray colour)
     int32_t sh_degree;
+    const float *scales;           // scene semi-axes [n][3] (backward: ||s||_inf)
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;
@@ -206,6 +207,14 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
 // CTAs leave, take overflowed pixels as K5 queues them and end once every K5 CTA has
 // exited.  With several batches it runs after all of them.
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
-int render_grid(int n_hidden, bool colour_ray, int tiles);   // K5's persistent grid for `tiles` work units
+int render_grid(int n_hidden, bool colour_ray, int tiles);
+// K7 (backward.cu): adds dL/d{W1, b1, W2, b2, SH} for grad = dL/d(out RGBA) of one camera
+// batch, re-deriving each pixel's forward (whole image; counters[kCntBwdSkipped] counts
+// pixels with more hits than the kernel holds)
+struct BackwardGrads {
+    float *w1, *b1, *w2, *b2, *sh;
+};
+cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
+                            float omega, cudaStream_t st);   // K5's persistent grid for `tiles` work units
 
 }  // namespace snp

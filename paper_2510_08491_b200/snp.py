@@ -28,7 +28,8 @@ SNP_COLOUR_RAY = 1        # colour_mode: SH at each pixel's ray direction
 
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
-           "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at")
+           "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at",
+           "snp_render_backward")
 
 
 class SnpError(RuntimeError):
@@ -88,6 +89,7 @@ def lib():
             L.snp_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
             L.snp_set_temporal.argtypes = [vp, vp, C.c_int32, vp]
+            L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp]
             L.snp_project_at.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp, vp]
             L.snp_get_debug_counters.argtypes = [vp, vp, C.c_int32, vp]
             for f in EXPORTS:
@@ -224,6 +226,13 @@ def render_views(h, cams, opts, out, stream=None, xi_t=None):
         project(h, arr, stream, xi_t)
         bin_sort(h, opts, stream)
         render(h, opts, out, stream)
+
+
+def render_backward(h, opts, grad_rgba, grads, stream=None):
+    """K7: adds dL/d{w1, b1, w2, b2, sh} (dict of CUDA tensors shaped like the scene's
+    arrays) for grad_rgba = dL/d(out RGBA) (CUDA tensor [V, H, W, 4])."""
+    _check(lib().snp_render_backward(h, C.byref(opts), _ptr(grad_rgba), _ptr(grads["w1"]), _ptr(grads["b1"]),
+                                     _ptr(grads["w2"]), _ptr(grads["b2"]), _ptr(grads["sh"]), _stream(stream)))
 
 
 def destroy(h):

@@ -488,3 +488,69 @@ def test_temporal_views(orc):
         cmp_ = compare(img[v].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
         assert cmp_["max_unflagged"] <= TOL and cmp_["n_flagged"] <= 0.01 * cmp_["n"], (v, cmp_)
     assert np.array_equal(static[0], img[0]) and np.abs(static[2] - img[2]).max() > 1e-3
+
+
+@pytest.mark.parametrize("colour_mode,n_hidden", [(0, 8), (1, 8), (0, 16)])
+def test_backward_mlp_and_sh_vs_finite_differences(orc, colour_mode, n_hidden):
+    """K7 (snp_render_backward, SURVEY §8(f) rank 1 first part): dL/d{W1, b1, W2, b2, SH}
+    for L = sum(G * out_rgba), against central differences of the fp64 oracle's forward
+    on sampled parameters of hit primitives (geometry fixed)."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene = synth.make_scene(61, 150, box=0.6, n_hidden=n_hidden)
+    # semi-transparent (no pixel reaches the T floor, whose stop rule makes L jump) and a
+    # density bounded away from 0 (b2 > sum |W2|: no I <= 0 kink of Eq. 9), so that L is
+    # smooth around the sampled parameters and finite differences see the derivative
+    scene.w2 *= np.float32(0.8 / n_hidden)
+    scene.b2[:] = (1.2 * np.abs(scene.w2).sum(1)).astype(np.float32)
+    cam = synth.orbit_cameras(1, 3.0, 64, 48, 60.0)[0]
+    bg = (0.1, 0.2, 0.3)
+    rng = np.random.default_rng(62 + colour_mode + n_hidden)
+    G = rng.normal(size=(1, 48, 64, 4)).astype(np.float32)
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        opts = snp.make_opts(bg, colour_mode=colour_mode)
+        out = torch.zeros((1, 48, 64, 4), device="cuda")
+        snp.render_views(h, [cam], opts, out)
+        grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in ("w1", "b1", "w2", "b2", "sh")}
+        snp.render_backward(h, opts, torch.from_numpy(G).cuda(), grads)
+        torch.cuda.synchronize()
+        assert snp.get_debug_counters(h, 48)[14] == 0
+        assert out[..., 3].max().item() < 0.999
+        g = {f: v.cpu().numpy().astype(np.float64) for f, v in grads.items()}
+    finally:
+        snp.destroy(h)
+    ray = colour_mode == 1
+
+    def loss(sc):
+        img, _, _ = orc.render_frame(sc, cam, bg, colour_per_ray=ray)
+        return float((img * G[0].astype(np.float64)).sum())
+
+    hit = np.nonzero(np.abs(g["b2"]) > 0)[0]
+    assert len(hit) > 20
+    checks = []
+    for f in ("w1", "b1", "w2", "b2", "sh"):
+        for _ in range(8):
+            i = int(rng.choice(hit))
+            idx = (i,) + tuple(int(rng.integers(0, s)) for s in getattr(scene, f).shape[1:])
+            if f == "sh":
+                idx = (i, int(rng.integers(0, 4)), int(rng.integers(0, 3)))   # low bands
+            arr = getattr(scene, f)
+            base = float(arr[idx])
+            step = np.float32(2e-3 * (abs(base) + 0.05))
+            vals = []
+            for sgn in (1, -1):
+                arr[idx] = np.float32(base + sgn * step)
+                vals.append(loss(scene))
+            arr[idx] = np.float32(base)
+            hp, hm = float(np.float32(base + step)) - base, base - float(np.float32(base - step))
+            fd = (vals[0] - vals[1]) / (hp + hm)
+            checks.append((f, idx, float(g[f][idx]), fd))
+    scale = max(abs(c[3]) for c in checks)
+    worst = max(abs(c[2] - c[3]) / (abs(c[3]) + 1e-3 * scale) for c in checks)
+    print("backward vs FD: worst relative error %.2e over %d parameters (scale %.3g)" % (worst, len(checks), scale))
+    for c in sorted(checks, key=lambda c: -abs(c[2] - c[3]) / (abs(c[3]) + 1e-3 * scale))[:6]:
+        print("   ", c)
+    bad = [c for c in checks if abs(c[2] - c[3]) > 2e-3 * abs(c[3]) + 2e-4 * scale]
+    assert not bad, (bad, scale)
