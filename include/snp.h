@@ -174,18 +174,21 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
  * host output: they are written as 0. */
 snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba, void *cuda_stream);
 
-/* Backward of snp_render (first part):
- * given grad_rgba = dL/d(out_rgba) [n_views][height][width][4] (device), ADDS
- * dL/d{w1, b1, w2, b2, sh} of every primitive into grad_w1 [n][N][3], grad_b1 [n][N],
- * grad_w2 [n][N], grad_b2 [n], grad_sh [n][16][3] (device; the caller zeroes them).  The
- * ellipsoid geometry (centers, rotations, scales) is held fixed: its gradients are not
- * computed.  Call after snp_bin_sort of the same frame, with the same opts as the
+/* Backward of snp_render: given
+ * grad_rgba = dL/d(out_rgba) [n_views][height][width][4] (device), ADDS the gradients
+ * of every primitive into grad_w1 [n][N][3], grad_b1 [n][N], grad_w2 [n][N], grad_b2 [n],
+ * grad_sh [n][16][3] and -- when grad_centers is not NULL -- grad_centers [n][3],
+ * grad_rotations [n][4], grad_scales [n][3] (device; the caller zeroes them; the three
+ * geometry pointers are all NULL or all set).  The per-ray hit order and the T < floor
+ * stop are piecewise constant and carry no gradient; the I <= 0 clamp of Eq. 9 has
+ * gradient 0.  Call after snp_bin_sort of the same frame, with the same opts as the
  * snp_render it differentiates (background, transmittance_floor, colour_mode); the
  * whole image only (tile_row_begin = 0, tile_row_stride = 1), else SNP_ERR_UNSUPPORTED.
  * Pixels with more than 256 hits are skipped (snp_get_debug_counters slot 14 counts
  * them). */
 snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
-                               float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, void *cuda_stream);
+                               float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
+                               float *grad_rotations, float *grad_scales, void *cuda_stream);
 
 /* Convenience: snp_project + snp_bin_sort + snp_render. */
 snp_status snp_render_views(snp_scene s, const snp_camera *cams, int32_t n_views,

@@ -589,12 +589,15 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
 }
 
 snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
-                               float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, void *cuda_stream) {
+                               float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
+                               float *grad_rotations, float *grad_scales, void *cuda_stream) {
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
     if (!opts || !grad_rgba || !grad_w1 || !grad_b1 || !grad_w2 || !grad_b2 || !grad_sh)
         return fail(SNP_ERR_INVALID_ARGUMENT, "opts or a gradient pointer is NULL");
+    if ((grad_centers == nullptr) != (grad_rotations == nullptr) || (grad_centers == nullptr) != (grad_scales == nullptr))
+        return fail(SNP_ERR_INVALID_ARGUMENT, "grad_centers, grad_rotations, grad_scales: all NULL or all set");
     if (s->state < kBinned) return fail(SNP_ERR_BAD_STATE, "snp_render_backward before snp_bin_sort");
     if (s->row_begin != 0 || s->row_stride != 1)
         return fail(SNP_ERR_UNSUPPORTED, "snp_render_backward needs the whole image (tile rows 0, 1)");
@@ -607,6 +610,7 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     a.sh = s->sh;
     a.sh_degree = s->sh_degree;
     a.scales = s->scales;
+    a.rotations = s->rotations;
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
     a.tiles_per_view = s->tiles_x * s->tiles_y;
@@ -622,7 +626,7 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     for (int c = 0; c < 3; ++c) a.bg[c] = opts->background[c];
     a.t_floor = opts->transmittance_floor;
     a.counters = s->counters.p;
-    BackwardGrads g{grad_w1, grad_b1, grad_w2, grad_b2, grad_sh};
+    BackwardGrads g{grad_w1, grad_b1, grad_w2, grad_b2, grad_sh, grad_centers, grad_rotations, grad_scales};
     for (const CamBatch &cb : s->cams) SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, st));
     return SNP_OK;
 }

@@ -1,6 +1,7 @@
-// backward.cu -- K7: backward of the forward render (first part):
-// dL/d{W1, b1, W2, b2, SH} of every primitive for a given dL/d(out RGBA), with the
-// ellipsoid geometry (mu, q, s) held fixed.
+// backward.cu -- K7: backward of the forward render:
+// dL/d{W1, b1, W2, b2, SH} and (optionally) dL/d{mu, q, s} of every primitive for a
+// given dL/d(out RGBA).  The per-ray hit order and the T-floor stop are piecewise
+// constant in the parameters and carry no gradient.
 //
 // One warp per pixel.  The warp re-derives its pixel's forward exactly as K6 does --
 // every hit of the tile list (conic pre-test + exact_hit), sorted by (t_in, id)
@@ -47,75 +48,192 @@ __device__ __forceinline__ float dsinc_f(float x) {
     return (__cosf(x) - __sinf(x) / x) / x;
 }
 
-// dL/dI of one (ray, record) hit into the MLP parameter gradients of primitive `prim`.
+// dL/dI (gI) of one (ray, record) hit into the gradients of primitive `prim`: the MLP
+// parameters always, the geometry (mu, q, s) when gr.mu is set.  The forward values are
+// recomputed exactly as exact_hit (hit.cuh) does; the geometry adjoints follow the
+// chain p = t_c d - m (m = mu - C, t_c = d.m), a = Wh d, b = Wh p (Wh = S^-1 R^T),
+// A = |a|^2, B = a.b, tau* = -B/A, b_perp = b + tau* a, Q = 1 - |b_perp|^2,
+// hc = sqrt(Q/A), [t0, t1] = tau* -/+ hc clipped to [t_near - t_c, t_far - t_c],
+// dt = t1 - t0, tau_m = (t0 + t1)/2, W1' = omega W1 / ||s||_inf.
 template <int N>
 __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const Ray &r, float gI, float omega,
-                                         float smax, uint32_t prim, float *g_w1, float *g_b1, float *g_w2,
-                                         float *g_b2) {
-    // the same intermediate values as exact_hit (hit.cuh)
+                                         uint32_t prim, const RenderArgs &ra, const BackwardGrads &gr) {
     const float4 mh = rec[kRecMh];
     const float4 ml = rec[kRecMl];
     const float4 w0 = rec[kRecWh0];
     const float4 w1 = rec[kRecWh1];
+    const float Wh[9] = {ml.w, w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const float d[3] = {r.dhx, r.dhy, r.dhz};
     const float tc = fmaf(r.dhz, mh.z, fmaf(r.dhy, mh.y, r.dhx * mh.x));
-    const float px = fmaf(tc, r.dhx, -mh.x) + fmaf(tc, r.dlx, -ml.x);
-    const float py = fmaf(tc, r.dhy, -mh.y) + fmaf(tc, r.dly, -ml.y);
-    const float pz = fmaf(tc, r.dhz, -mh.z) + fmaf(tc, r.dlz, -ml.z);
-    const float ax = fmaf(w0.y, r.dhz, fmaf(w0.x, r.dhy, ml.w * r.dhx));
-    const float ay = fmaf(w1.x, r.dhz, fmaf(w0.w, r.dhy, w0.z * r.dhx));
-    const float az = fmaf(w1.w, r.dhz, fmaf(w1.z, r.dhy, w1.y * r.dhx));
-    const float bx = fmaf(w0.y, pz, fmaf(w0.x, py, ml.w * px));
-    const float by = fmaf(w1.x, pz, fmaf(w0.w, py, w0.z * px));
-    const float bz = fmaf(w1.w, pz, fmaf(w1.z, py, w1.y * px));
-    const float A = fmaf(az, az, fmaf(ay, ay, ax * ax));
-    const float B = fmaf(az, bz, fmaf(ay, by, ax * bx));
+    const float p[3] = {fmaf(tc, r.dhx, -mh.x) + fmaf(tc, r.dlx, -ml.x),
+                        fmaf(tc, r.dhy, -mh.y) + fmaf(tc, r.dly, -ml.y),
+                        fmaf(tc, r.dhz, -mh.z) + fmaf(tc, r.dlz, -ml.z)};
+    float av[3], bv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        av[k] = fmaf(Wh[3 * k + 2], d[2], fmaf(Wh[3 * k + 1], d[1], Wh[3 * k] * d[0]));
+        bv[k] = fmaf(Wh[3 * k + 2], p[2], fmaf(Wh[3 * k + 1], p[1], Wh[3 * k] * p[0]));
+    }
+    const float A = fmaf(av[2], av[2], fmaf(av[1], av[1], av[0] * av[0]));
+    const float B = fmaf(av[2], bv[2], fmaf(av[1], bv[1], av[0] * bv[0]));
     const float iA = 1.0f / A;
     const float ts = -B * iA;
-    const float qx = fmaf(ts, ax, bx), qy = fmaf(ts, ay, by), qz = fmaf(ts, az, bz);
-    const float q1 = 1.0f - fmaf(qz, qz, fmaf(qy, qy, qx * qx));
-    if (!(q1 > 0.0f)) return;
-    const float hc = sqrtf(q1 * iA);
+    const float bp[3] = {fmaf(ts, av[0], bv[0]), fmaf(ts, av[1], bv[1]), fmaf(ts, av[2], bv[2])};
+    const float Q = 1.0f - fmaf(bp[2], bp[2], fmaf(bp[1], bp[1], bp[0] * bp[0]));
+    if (!(Q > 0.0f)) return;
+    const float hc = sqrtf(Q * iA);
     const float t0 = ts - hc, t1 = ts + hc;
     const float lo_lim = r.t_near - tc, hi_lim = r.t_far - tc;
-    const float tlo = t0 > lo_lim ? t0 : lo_lim;
-    const float thi = t1 < hi_lim ? t1 : hi_lim;
+    const bool clip_lo = !(t0 > lo_lim), clip_hi = !(t1 < hi_lim);
+    const float tlo = clip_lo ? lo_lim : t0;
+    const float thi = clip_hi ? hi_lim : t1;
     if (!(thi > tlo)) return;
     const float dt = thi - tlo, tm = 0.5f * (tlo + thi), hdt = 0.5f * dt;
+    const float *s3 = ra.scales + 3 * (size_t)prim;
+    const float sv[3] = {s3[0], s3[1], s3[2]};
+    const int imax = (sv[1] > sv[0]) ? ((sv[2] > sv[1]) ? 2 : 1) : ((sv[2] > sv[0]) ? 2 : 0);
+    const float smax = sv[imax];
     const uint32_t wbase = (uint32_t)N * prim;
-    float gb2 = 0.f;
-    gb2 = gI * dt;
-    atomicAdd(g_b2 + prim, gb2);
     const float s1 = omega / smax;
+    float sumc = mh.w;                    // sum_k W2_k cos(phi_k) S_k + b2
+    float gdt = 0.f, gtm = 0.f, gsmax = 0.f;
+    float gp[3] = {0.f, 0.f, 0.f};        // dI/dp through the phases
     for (int gq = 0; gq < N / 4; ++gq) {
-    const float4 w4 = rec[rec_w2(N) + gq];
-    const float w2s[4] = {w4.x, w4.y, w4.z, w4.w};
+        const float4 w4 = rec[rec_w2(N) + gq];
+        const float w2s[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-    for (int uu = 0; uu < 4; ++uu) {
-        const int k = 4 * gq + uu;
-        const float4 u = rec[kRecUnits + k];
-        const float w2 = w2s[uu];
-        const float h = fmaf(u.z, r.dhz, fmaf(u.y, r.dhy, u.x * r.dhx));
-        const float g = fmaf(u.z, pz, fmaf(u.y, py, fmaf(u.x, px, u.w)));
-        const float phi = fmaf(h, tm, g);
-        float sn, cs;
-        sincosf(phi, &sn, &cs);
-        const float x = h * hdt;
-        const float S = fabsf(x) < 0.25f ? fmaf(x * x, fmaf(x * x, 8.3333333e-03f, -1.6666667e-01f), 1.0f)
-                                         : sinf(x) / x;
-        const float Sp = dsinc_f(x);
-        atomicAdd(g_w2 + wbase + k, gI * dt * cs * S);
-        const float a_sin = -gI * dt * w2 * sn * S;   // dL/dphi_k (through cos)
-        atomicAdd(g_b1 + wbase + k, omega * a_sin);
-        const float a_h = gI * dt * w2 * cs * Sp * hdt;   // dL/dh_k through the sinc
-        // dphi/dW1' = p + tm d, dh/dW1' = d
-        const float gx = a_sin * fmaf(tm, r.dhx, px) + a_h * r.dhx;
-        const float gy = a_sin * fmaf(tm, r.dhy, py) + a_h * r.dhy;
-        const float gz = a_sin * fmaf(tm, r.dhz, pz) + a_h * r.dhz;
-        atomicAdd(g_w1 + 3 * (wbase + k) + 0, s1 * gx);
-        atomicAdd(g_w1 + 3 * (wbase + k) + 1, s1 * gy);
-        atomicAdd(g_w1 + 3 * (wbase + k) + 2, s1 * gz);
+        for (int uu = 0; uu < 4; ++uu) {
+            const int k = 4 * gq + uu;
+            const float4 u = rec[kRecUnits + k];
+            const float w2 = w2s[uu];
+            const float h = fmaf(u.z, d[2], fmaf(u.y, d[1], u.x * d[0]));
+            const float g = fmaf(u.z, p[2], fmaf(u.y, p[1], fmaf(u.x, p[0], u.w)));
+            const float phi = fmaf(h, tm, g);
+            float sn, cs;
+            sincosf(phi, &sn, &cs);
+            const float x = h * hdt;
+            const float S = fabsf(x) < 0.25f ? fmaf(x * x, fmaf(x * x, 8.3333333e-03f, -1.6666667e-01f), 1.0f)
+                                             : sinf(x) / x;
+            const float Sp = dsinc_f(x);
+            sumc = fmaf(w2 * cs, S, sumc);
+            gdt = fmaf(w2 * cs * Sp, 0.5f * h, gdt);
+            gtm = fmaf(-w2 * sn * S, h, gtm);
+            const float coef = -dt * w2 * sn * S;            // dI/dphi_k
+            const float chs = dt * w2 * cs * Sp * hdt;        // dI/dh_k through the sinc
+            gp[0] = fmaf(coef, u.x, gp[0]);
+            gp[1] = fmaf(coef, u.y, gp[1]);
+            gp[2] = fmaf(coef, u.z, gp[2]);
+            // dI/dW1'_k = coef (p + tm d) + chs d
+            const float gw[3] = {fmaf(coef, fmaf(tm, d[0], p[0]), chs * d[0]),
+                                 fmaf(coef, fmaf(tm, d[1], p[1]), chs * d[1]),
+                                 fmaf(coef, fmaf(tm, d[2], p[2]), chs * d[2])};
+            gsmax -= (gw[0] * u.x + gw[1] * u.y + gw[2] * u.z) / smax;
+            atomicAdd(gr.w2 + wbase + k, gI * dt * cs * S);
+            atomicAdd(gr.b1 + wbase + k, gI * omega * coef);
+            atomicAdd(gr.w1 + 3 * (wbase + k) + 0, gI * s1 * gw[0]);
+            atomicAdd(gr.w1 + 3 * (wbase + k) + 1, gI * s1 * gw[1]);
+            atomicAdd(gr.w1 + 3 * (wbase + k) + 2, gI * s1 * gw[2]);
+        }
     }
+    atomicAdd(gr.b2 + prim, gI * dt);
+    if (!gr.mu) return;
+    // ---- geometry
+    const float G_dt = gI * fmaf(dt, gdt, sumc), G_tm = gI * dt * gtm;
+    const float G_tlo = -G_dt + 0.5f * G_tm, G_thi = G_dt + 0.5f * G_tm;
+    const float G_t0 = clip_lo ? 0.f : G_tlo, G_t1 = clip_hi ? 0.f : G_thi;
+    float G_tc = (clip_lo ? -G_tlo : 0.f) + (clip_hi ? -G_thi : 0.f);
+    float G_ts = G_t0 + G_t1;
+    const float G_hc = G_t1 - G_t0;
+    const float G_Q = G_hc * hc / (2.0f * Q);
+    float G_A = -G_hc * hc * 0.5f * iA;
+    float G_a[3], G_b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float gbp = -2.0f * bp[k] * G_Q;
+        G_b[k] = gbp;
+        G_a[k] = ts * gbp;
+        G_ts = fmaf(gbp, av[k], G_ts);
     }
+    const float G_B = -G_ts * iA;
+    G_A = fmaf(G_ts * B, iA * iA, G_A);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        G_a[k] = fmaf(2.0f * av[k], G_A, fmaf(bv[k], G_B, G_a[k]));
+        G_b[k] = fmaf(av[k], G_B, G_b[k]);
+    }
+    float Gp[3] = {gI * gp[0], gI * gp[1], gI * gp[2]};
+    float G_Wh[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            G_Wh[3 * k + j] = fmaf(G_a[k], d[j], G_b[k] * p[j]);
+            Gp[j] = fmaf(Wh[3 * k + j], G_b[k], Gp[j]);
+        }
+    G_tc = fmaf(Gp[2], d[2], fmaf(Gp[1], d[1], fmaf(Gp[0], d[0], G_tc)));
+    // m = mu - C: p = t_c d - m, t_c = d.m
+    atomicAdd(gr.mu + 3 * (size_t)prim + 0, fmaf(d[0], G_tc, -Gp[0]));
+    atomicAdd(gr.mu + 3 * (size_t)prim + 1, fmaf(d[1], G_tc, -Gp[1]));
+    atomicAdd(gr.mu + 3 * (size_t)prim + 2, fmaf(d[2], G_tc, -Gp[2]));
+    // Wh[k][j] = R[j][k] / s_k
+    float G_s[3], G_R[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            acc = fmaf(G_Wh[3 * k + j], Wh[3 * k + j], acc);
+            G_R[3 * j + k] = G_Wh[3 * k + j] / sv[k];
+        }
+        G_s[k] = -acc / sv[k];
+    }
+    G_s[imax] += gI * gsmax;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) atomicAdd(gr.s + 3 * (size_t)prim + k, G_s[k]);
+    // R(q^), q^ = q / |q| (w, x, y, z)
+    const float *q4 = ra.rotations + 4 * (size_t)prim;
+    const float qn = sqrtf(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
+    const float w = q4[0] / qn, x = q4[1] / qn, y = q4[2] / qn, z = q4[3] / qn;
+    const float gw_ = 2.0f * (-z * G_R[1] + y * G_R[2] + z * G_R[3] - x * G_R[5] - y * G_R[6] + x * G_R[7]);
+    const float gx_ = 2.0f * (y * G_R[1] + z * G_R[2] + y * G_R[3] - 2.0f * x * G_R[4] - w * G_R[5] + z * G_R[6] +
+                              w * G_R[7] - 2.0f * x * G_R[8]);
+    const float gy_ = 2.0f * (-2.0f * y * G_R[0] + x * G_R[1] + w * G_R[2] + x * G_R[3] + z * G_R[5] - w * G_R[6] +
+                              z * G_R[7] - 2.0f * y * G_R[8]);
+    const float gz_ = 2.0f * (-2.0f * z * G_R[0] - w * G_R[1] + x * G_R[2] + w * G_R[3] - 2.0f * z * G_R[4] +
+                              y * G_R[5] + x * G_R[6] + y * G_R[7]);
+    const float dotq = w * gw_ + x * gx_ + y * gy_ + z * gz_;
+    atomicAdd(gr.q + 4 * (size_t)prim + 0, (gw_ - w * dotq) / qn);
+    atomicAdd(gr.q + 4 * (size_t)prim + 1, (gx_ - x * dotq) / qn);
+    atomicAdd(gr.q + 4 * (size_t)prim + 2, (gy_ - y * dotq) / qn);
+    atomicAdd(gr.q + 4 * (size_t)prim + 3, (gz_ - z * dotq) / qn);
+}
+
+// d Y_lm / d dir for the basis of sh_basis_f (rows: coefficient, columns: x, y, z)
+__device__ __forceinline__ void sh_basis_grad(float x, float y, float z, float dY[16][3]) {
+    const float c1 = 0.4886025119029199f, c2 = 1.0925484305920792f, c3 = 0.31539156525252005f,
+                c4 = 0.5462742152960396f, c5 = 0.5900435899266435f, c6 = 2.890611442640554f,
+                c7 = 0.4570457994644658f, c8 = 0.3731763325901154f, c9 = 1.445305721320277f;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    const float t[16][3] = {{0.f, 0.f, 0.f},
+                            {0.f, -c1, 0.f},
+                            {0.f, 0.f, c1},
+                            {-c1, 0.f, 0.f},
+                            {c2 * y, c2 * x, 0.f},
+                            {0.f, -c2 * z, -c2 * y},
+                            {-2.f * c3 * x, -2.f * c3 * y, 4.f * c3 * z},
+                            {-c2 * z, 0.f, -c2 * x},
+                            {2.f * c4 * x, -2.f * c4 * y, 0.f},
+                            {-6.f * c5 * x * y, -3.f * c5 * (xx - yy), 0.f},
+                            {c6 * y * z, c6 * x * z, c6 * x * y},
+                            {2.f * c7 * x * y, -c7 * (4.f * zz - xx - 3.f * yy), -8.f * c7 * y * z},
+                            {-6.f * c8 * x * z, -6.f * c8 * y * z, c8 * (6.f * zz - 3.f * xx - 3.f * yy)},
+                            {-c7 * (4.f * zz - 3.f * xx - yy), 2.f * c7 * x * y, -8.f * c7 * x * z},
+                            {2.f * c9 * x * z, -2.f * c9 * y * z, c9 * (xx - yy)},
+                            {-3.f * c5 * (xx - yy), 6.f * c5 * x * y, 0.f}};
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dY[i][c] = t[i][c];
 }
 
 __device__ __forceinline__ void sh_basis_f(float x, float y, float z, float Y[16]) {
@@ -244,9 +362,7 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch 
             const int h = (int)sm.ord[wid][k];
             const uint32_t id = sm.id[wid][h];
             const float4 *rec = recs + (size_t)id * rec_f4(N);
-            const float *s3 = a.scales + 3 * (size_t)id;
-            const float smax = fmaxf(s3[0], fmaxf(s3[1], s3[2]));
-            hit_grad<N>(rec, ray, sm.gI[wid][k], omega, smax, id, gr.w1, gr.b1, gr.w2, gr.b2);
+            hit_grad<N>(rec, ray, sm.gI[wid][k], omega, id, a, gr);
             // SH colour: dc/dsh_lm = Y_lm(dir) (unclamped channels)
             float dxv, dyv, dzv;
             if (kRay) {
@@ -266,6 +382,28 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch 
                 if (g0 != 0.f) atomicAdd(gs + 3 * i + 0, Y[i] * g0);
                 if (g1 != 0.f) atomicAdd(gs + 3 * i + 1, Y[i] * g1);
                 if (g2 != 0.f) atomicAdd(gs + 3 * i + 2, Y[i] * g2);
+            }
+            if (!kRay && gr.mu && (g0 != 0.f || g1 != 0.f || g2 != 0.f)) {
+                // colour direction dir = (mu - C) / |mu - C|: dL/dmu = (I - dir dir^T) dL/ddir / |mu - C|
+                const float *shp = a.sh + 48 * (size_t)id;
+                float dY[16][3];
+                sh_basis_grad(dxv, dyv, dzv, dY);
+                float gd[3] = {0.f, 0.f, 0.f};
+                for (int i = 0; i < ncoef; ++i) {
+                    const float e = shp[3 * i] * g0 + shp[3 * i + 1] * g1 + shp[3 * i + 2] * g2;
+                    gd[0] = fmaf(dY[i][0], e, gd[0]);
+                    gd[1] = fmaf(dY[i][1], e, gd[1]);
+                    gd[2] = fmaf(dY[i][2], e, gd[2]);
+                }
+                const float4 mh = rec[kRecMh], ml = rec[kRecMl];
+                const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
+                const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
+                if (nrm > 0.f) {
+                    const float dd = dxv * gd[0] + dyv * gd[1] + dzv * gd[2];
+                    atomicAdd(gr.mu + 3 * (size_t)id + 0, (gd[0] - dxv * dd) / nrm);
+                    atomicAdd(gr.mu + 3 * (size_t)id + 1, (gd[1] - dyv * dd) / nrm);
+                    atomicAdd(gr.mu + 3 * (size_t)id + 2, (gd[2] - dzv * dd) / nrm);
+                }
             }
         }
         __syncwarp();

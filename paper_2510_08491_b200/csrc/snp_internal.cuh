@@ -176,7 +176,8 @@ struct RenderArgs {
     int32_t colour_ray;            // 1: SH colour at each pixel's ray direction (SNP_COLOUR_RAY)
     const float *sh;               // scene SH coefficients [n][16][3] (per-ray colour)
     int32_t sh_degree;
-    const float *scales;           // scene semi-axes [n][3] (backward: ||s||_inf)
+    const float *scales;           // scene semi-axes [n][3] (backward)
+    const float *rotations;        // scene quaternions [n][4] (backward)
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;
@@ -213,6 +214,7 @@ int render_grid(int n_hidden, bool colour_ray, int tiles);
 // pixels with more hits than the kernel holds)
 struct BackwardGrads {
     float *w1, *b1, *w2, *b2, *sh;
+    float *mu, *q, *s;             // geometry gradients, or all nullptr (not computed)
 };
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
                             float omega, cudaStream_t st);   // K5's persistent grid for `tiles` work units

@@ -89,7 +89,7 @@ def lib():
             L.snp_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
             L.snp_set_temporal.argtypes = [vp, vp, C.c_int32, vp]
-            L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp]
+            L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
             L.snp_project_at.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp, vp]
             L.snp_get_debug_counters.argtypes = [vp, vp, C.c_int32, vp]
             for f in EXPORTS:
@@ -229,10 +229,13 @@ def render_views(h, cams, opts, out, stream=None, xi_t=None):
 
 
 def render_backward(h, opts, grad_rgba, grads, stream=None):
-    """K7: adds dL/d{w1, b1, w2, b2, sh} (dict of CUDA tensors shaped like the scene's
-    arrays) for grad_rgba = dL/d(out RGBA) (CUDA tensor [V, H, W, 4])."""
+    """K7: adds dL/d{w1, b1, w2, b2, sh} and, when ``grads`` has "centers", "rotations" and
+    "scales", the geometry gradients (dict of CUDA tensors shaped like the scene's arrays)
+    for grad_rgba = dL/d(out RGBA) (CUDA tensor [V, H, W, 4])."""
     _check(lib().snp_render_backward(h, C.byref(opts), _ptr(grad_rgba), _ptr(grads["w1"]), _ptr(grads["b1"]),
-                                     _ptr(grads["w2"]), _ptr(grads["b2"]), _ptr(grads["sh"]), _stream(stream)))
+                                     _ptr(grads["w2"]), _ptr(grads["b2"]), _ptr(grads["sh"]),
+                                     _ptr(grads.get("centers")), _ptr(grads.get("rotations")),
+                                     _ptr(grads.get("scales")), _stream(stream)))
 
 
 def destroy(h):

@@ -513,7 +513,8 @@ def test_backward_mlp_and_sh_vs_finite_differences(orc, colour_mode, n_hidden):
         opts = snp.make_opts(bg, colour_mode=colour_mode)
         out = torch.zeros((1, 48, 64, 4), device="cuda")
         snp.render_views(h, [cam], opts, out)
-        grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in ("w1", "b1", "w2", "b2", "sh")}
+        grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda")
+                 for f in ("w1", "b1", "w2", "b2", "sh", "centers", "rotations", "scales")}
         snp.render_backward(h, opts, torch.from_numpy(G).cuda(), grads)
         torch.cuda.synchronize()
         assert snp.get_debug_counters(h, 48)[14] == 0
@@ -530,7 +531,9 @@ def test_backward_mlp_and_sh_vs_finite_differences(orc, colour_mode, n_hidden):
     hit = np.nonzero(np.abs(g["b2"]) > 0)[0]
     assert len(hit) > 20
     checks = []
-    for f in ("w1", "b1", "w2", "b2", "sh"):
+    geo = ("centers", "rotations", "scales")
+    skipped = []
+    for f in ("w1", "b1", "w2", "b2", "sh") + geo:
         for _ in range(8):
             i = int(rng.choice(hit))
             idx = (i,) + tuple(int(rng.integers(0, s)) for s in getattr(scene, f).shape[1:])
@@ -538,19 +541,34 @@ def test_backward_mlp_and_sh_vs_finite_differences(orc, colour_mode, n_hidden):
                 idx = (i, int(rng.integers(0, 4)), int(rng.integers(0, 3)))   # low bands
             arr = getattr(scene, f)
             base = float(arr[idx])
-            step = np.float32(2e-3 * (abs(base) + 0.05))
-            vals = []
-            for sgn in (1, -1):
-                arr[idx] = np.float32(base + sgn * step)
-                vals.append(loss(scene))
-            arr[idx] = np.float32(base)
-            hp, hm = float(np.float32(base + step)) - base, base - float(np.float32(base - step))
-            fd = (vals[0] - vals[1]) / (hp + hm)
-            checks.append((f, idx, float(g[f][idx]), fd))
-    scale = max(abs(c[3]) for c in checks)
-    worst = max(abs(c[2] - c[3]) / (abs(c[3]) + 1e-3 * scale) for c in checks)
-    print("backward vs FD: worst relative error %.2e over %d parameters (scale %.3g)" % (worst, len(checks), scale))
-    for c in sorted(checks, key=lambda c: -abs(c[2] - c[3]) / (abs(c[3]) + 1e-3 * scale))[:6]:
-        print("   ", c)
-    bad = [c for c in checks if abs(c[2] - c[3]) > 2e-3 * abs(c[3]) + 2e-4 * scale]
-    assert not bad, (bad, scale)
+            # geometry: steps far below the primitive size (the chord is sqrt-shaped at
+            # the silhouette); the fp64 oracle resolves them
+            step = np.float32(2e-3 * (abs(base) + 0.05)) if f not in geo else \
+                np.float32(2e-4 * float(scene.scales[i].min()))
+            fds = []
+            for st in ((step, step / 4) if f in geo else (step,)):
+                st = np.float32(st)
+                vals = []
+                for sgn in (1, -1):
+                    arr[idx] = np.float32(base + sgn * st)
+                    vals.append(loss(scene))
+                arr[idx] = np.float32(base)
+                hp, hm = float(np.float32(base + st)) - base, base - float(np.float32(base - st))
+                fds.append((vals[0] - vals[1]) / (hp + hm))
+            # a geometry parameter whose finite differences change with the step sits on a
+            # pixel where the chord's sqrt-shaped silhouette edge is within reach: skipped
+            if len(fds) == 2 and abs(fds[0] - fds[1]) > 1e-3 * max(abs(fds[0]), abs(fds[1]), 1e-3):
+                skipped.append((f, idx, float(g[f][idx]), fds))
+                continue
+            checks.append((f, idx, float(g[f][idx]), fds[-1]))
+    assert len(skipped) <= 6, skipped
+    for group, tol in (("mlp+sh", 2e-3), ("geometry", 5e-3)):
+        cs = [c for c in checks if (c[0] in geo) == (group == "geometry")]
+        scale = max(abs(c[3]) for c in cs)
+        worst = max(abs(c[2] - c[3]) / (abs(c[3]) + 1e-3 * scale) for c in cs)
+        print("backward vs FD (%s): worst relative error %.2e over %d parameters (scale %.3g; %d skipped)"
+              % (group, worst, len(cs), scale, len(skipped) if group == "geometry" else 0))
+        for c in sorted(cs, key=lambda c: -abs(c[2] - c[3]) / (abs(c[3]) + 1e-3 * scale))[:4]:
+            print("   ", c)
+        bad = [c for c in cs if abs(c[2] - c[3]) > tol * abs(c[3]) + 0.1 * tol * scale]
+        assert not bad, (group, bad, scale)

@@ -20,7 +20,8 @@ out = torch.empty((V, H, W, 4), device="cuda")
 opts = snp.make_opts(bg)
 snp.render_views(h, cams, opts, out)
 G = torch.randn((V, H, W, 4), device="cuda")
-grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in ("w1", "b1", "w2", "b2", "sh")}
+grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda")
+         for f in ("w1", "b1", "w2", "b2", "sh", "centers", "rotations", "scales")}
 ts = []
 for _ in range(args.iters):
     for v in grads.values():
