@@ -30,6 +30,7 @@ namespace {
 constexpr int kBwWarps = 8;
 constexpr int kBwThreads = kBwWarps * 32;
 constexpr int kBwHits = 256;
+constexpr int kBwQueue = 64;
 
 struct BwSmem {
     float th[kBwWarps][kBwHits], tl[kBwWarps][kBwHits], kap[kBwWarps][kBwHits];
@@ -39,6 +40,13 @@ struct BwSmem {
     float gI[kBwWarps][kBwHits];               // dL/dI per sorted hit
     float gc[kBwWarps][kBwHits][3];            // dL/dc per sorted hit (clamped channels: 0)
     int ncomp[kBwWarps];
+    // per-warp queue of composited hits awaiting their parameter gradients: the warp
+    // drains it 32 hits at a time (all lanes busy) across its successive pixels
+    float q_ray[kBwWarps][6][kBwQueue];        // pixel ray, hi + lo
+    uint32_t q_vl[kBwWarps][kBwQueue];         // camera index within the batch
+    uint32_t q_id[kBwWarps][kBwQueue];
+    float q_gI[kBwWarps][kBwQueue];
+    float q_gc[kBwWarps][3][kBwQueue];
 };
 
 __device__ __forceinline__ float dsinc_f(float x) {
@@ -256,6 +264,89 @@ __device__ __forceinline__ void sh_basis_f(float x, float y, float z, float Y[16
     Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
 }
 
+// Every parameter gradient of one composited hit (dL/dI = gI, dL/dc = gc).
+template <int N, bool kRay>
+__device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 *rec, const Ray &ray, uint32_t id,
+                                              float gI, const float gc[3], float omega, const BackwardGrads &gr) {
+    const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
+    hit_grad<N>(rec, ray, gI, omega, id, a, gr);
+    // SH colour: dc/dsh_lm = Y_lm(dir) (unclamped channels)
+    float dxv, dyv, dzv;
+    if (kRay) {
+        dxv = ray.dhx; dyv = ray.dhy; dzv = ray.dhz;
+    } else {   // dir = normalize(mu - C): the record's compensated camera-relative centre
+        const float4 mh = rec[kRecMh], ml = rec[kRecMl];
+        const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
+        const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
+        const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
+        dxv = nrm > 0.f ? vx * inv : 0.f; dyv = nrm > 0.f ? vy * inv : 0.f; dzv = nrm > 0.f ? vz * inv : 1.f;
+    }
+    float Y[16];
+    sh_basis_f(dxv, dyv, dzv, Y);
+    const float g0 = gc[0], g1 = gc[1], g2 = gc[2];
+    float *gs = gr.sh + 48 * (size_t)id;
+    for (int i = 0; i < ncoef; ++i) {
+        if (g0 != 0.f) atomicAdd(gs + 3 * i + 0, Y[i] * g0);
+        if (g1 != 0.f) atomicAdd(gs + 3 * i + 1, Y[i] * g1);
+        if (g2 != 0.f) atomicAdd(gs + 3 * i + 2, Y[i] * g2);
+    }
+    if (!kRay && gr.mu && (g0 != 0.f || g1 != 0.f || g2 != 0.f)) {
+        // colour direction dir = (mu - C) / |mu - C|: dL/dmu = (I - dir dir^T) dL/ddir / |mu - C|
+        const float *shp = a.sh + 48 * (size_t)id;
+        float dY[16][3];
+        sh_basis_grad(dxv, dyv, dzv, dY);
+        float gd[3] = {0.f, 0.f, 0.f};
+        for (int i = 0; i < ncoef; ++i) {
+            const float e = shp[3 * i] * g0 + shp[3 * i + 1] * g1 + shp[3 * i + 2] * g2;
+            gd[0] = fmaf(dY[i][0], e, gd[0]);
+            gd[1] = fmaf(dY[i][1], e, gd[1]);
+            gd[2] = fmaf(dY[i][2], e, gd[2]);
+        }
+        const float4 mh = rec[kRecMh], ml = rec[kRecMl];
+        const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
+        const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
+        if (nrm > 0.f) {
+            const float dd = dxv * gd[0] + dyv * gd[1] + dzv * gd[2];
+            atomicAdd(gr.mu + 3 * (size_t)id + 0, (gd[0] - dxv * dd) / nrm);
+            atomicAdd(gr.mu + 3 * (size_t)id + 1, (gd[1] - dyv * dd) / nrm);
+            atomicAdd(gr.mu + 3 * (size_t)id + 2, (gd[2] - dzv * dd) / nrm);
+        }
+    }
+}
+
+// Processes the first `cnt` (<= 32) entries of the warp's queue, one per lane, and moves
+// the rest to the front; returns the new queue length.
+template <int N, bool kRay>
+__device__ __forceinline__ int drain(BwSmem &sm, int wid, int lane, int qn, int cnt, const RenderArgs &a,
+                                     const CamBatch &cb, float omega, const BackwardGrads &gr) {
+    if (lane < cnt) {
+        Ray r;
+        r.dhx = sm.q_ray[wid][0][lane]; r.dhy = sm.q_ray[wid][1][lane]; r.dhz = sm.q_ray[wid][2][lane];
+        r.dlx = sm.q_ray[wid][3][lane]; r.dly = sm.q_ray[wid][4][lane]; r.dlz = sm.q_ray[wid][5][lane];
+        const uint32_t vl = sm.q_vl[wid][lane], id = sm.q_id[wid][lane];
+        r.t_near = cb.cams[vl].t_near;
+        r.t_far = cb.cams[vl].t_far;
+        const float gc[3] = {sm.q_gc[wid][0][lane], sm.q_gc[wid][1][lane], sm.q_gc[wid][2][lane]};
+        const float4 *rec = a.records + ((size_t)(cb.view0 + vl) * (size_t)a.n + id) * rec_f4(N);
+        hit_all_grads<N, kRay>(a, rec, r, id, sm.q_gI[wid][lane], gc, omega, gr);
+    }
+    __syncwarp();
+    const int rest = qn - cnt;
+    // (rest < kBwQueue - 32 + 32: every lane moves at most two entries)
+    for (int e = lane; e < rest; e += 32) {
+        const int from = cnt + e;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) sm.q_ray[wid][c][e] = sm.q_ray[wid][c][from];
+        sm.q_vl[wid][e] = sm.q_vl[wid][from];
+        sm.q_id[wid][e] = sm.q_id[wid][from];
+        sm.q_gI[wid][e] = sm.q_gI[wid][from];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sm.q_gc[wid][c][e] = sm.q_gc[wid][c][from];
+    }
+    __syncwarp();
+    return rest;
+}
+
 template <int N, bool kRay>
 __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch cb, const float4 *__restrict__ grad,
                                                          BackwardGrads gr, float omega) {
@@ -265,6 +356,7 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch 
     const uint32_t lt = (1u << lane) - 1u;
     const int W = cb.cams[0].W, H = cb.cams[0].H;
     const int64_t npix = (int64_t)cb.nv * W * H;
+    int qn = 0;   // entries in this warp's gradient queue
     for (int64_t pi = (int64_t)blockIdx.x * kBwWarps + wid; pi < npix; pi += (int64_t)gridDim.x * kBwWarps) {
         const int vloc = (int)(pi / ((int64_t)W * H));
         const int rem = (int)(pi - (int64_t)vloc * W * H);
@@ -355,59 +447,29 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch 
             sm.ncomp[wid] = last + 1;
         }
         __syncwarp();
-        // ---- parameter gradients of the composited hits
+        // ---- queue the composited hits; drain 32 at a time (all lanes busy)
         const int nc = sm.ncomp[wid];
-        const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
-        for (int k = lane; k < nc; k += 32) {
-            const int h = (int)sm.ord[wid][k];
-            const uint32_t id = sm.id[wid][h];
-            const float4 *rec = recs + (size_t)id * rec_f4(N);
-            hit_grad<N>(rec, ray, sm.gI[wid][k], omega, id, a, gr);
-            // SH colour: dc/dsh_lm = Y_lm(dir) (unclamped channels)
-            float dxv, dyv, dzv;
-            if (kRay) {
-                dxv = ray.dhx; dyv = ray.dhy; dzv = ray.dhz;
-            } else {   // dir = normalize(mu - C): the record's compensated camera-relative centre
-                const float4 mh = rec[kRecMh], ml = rec[kRecMl];
-                const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
-                const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
-                const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
-                dxv = nrm > 0.f ? vx * inv : 0.f; dyv = nrm > 0.f ? vy * inv : 0.f; dzv = nrm > 0.f ? vz * inv : 1.f;
+        for (int k0 = 0; k0 < nc;) {
+            const int m = min(nc - k0, kBwQueue - qn);
+            for (int e = lane; e < m; e += 32) {
+                const int k = k0 + e, slot = qn + e;
+                sm.q_ray[wid][0][slot] = ray.dhx; sm.q_ray[wid][1][slot] = ray.dhy; sm.q_ray[wid][2][slot] = ray.dhz;
+                sm.q_ray[wid][3][slot] = ray.dlx; sm.q_ray[wid][4][slot] = ray.dly; sm.q_ray[wid][5][slot] = ray.dlz;
+                sm.q_vl[wid][slot] = (uint32_t)vloc;
+                sm.q_id[wid][slot] = sm.id[wid][sm.ord[wid][k]];
+                sm.q_gI[wid][slot] = sm.gI[wid][k];
+                sm.q_gc[wid][0][slot] = sm.gc[wid][k][0];
+                sm.q_gc[wid][1][slot] = sm.gc[wid][k][1];
+                sm.q_gc[wid][2][slot] = sm.gc[wid][k][2];
             }
-            float Y[16];
-            sh_basis_f(dxv, dyv, dzv, Y);
-            const float g0 = sm.gc[wid][k][0], g1 = sm.gc[wid][k][1], g2 = sm.gc[wid][k][2];
-            float *gs = gr.sh + 48 * (size_t)id;
-            for (int i = 0; i < ncoef; ++i) {
-                if (g0 != 0.f) atomicAdd(gs + 3 * i + 0, Y[i] * g0);
-                if (g1 != 0.f) atomicAdd(gs + 3 * i + 1, Y[i] * g1);
-                if (g2 != 0.f) atomicAdd(gs + 3 * i + 2, Y[i] * g2);
-            }
-            if (!kRay && gr.mu && (g0 != 0.f || g1 != 0.f || g2 != 0.f)) {
-                // colour direction dir = (mu - C) / |mu - C|: dL/dmu = (I - dir dir^T) dL/ddir / |mu - C|
-                const float *shp = a.sh + 48 * (size_t)id;
-                float dY[16][3];
-                sh_basis_grad(dxv, dyv, dzv, dY);
-                float gd[3] = {0.f, 0.f, 0.f};
-                for (int i = 0; i < ncoef; ++i) {
-                    const float e = shp[3 * i] * g0 + shp[3 * i + 1] * g1 + shp[3 * i + 2] * g2;
-                    gd[0] = fmaf(dY[i][0], e, gd[0]);
-                    gd[1] = fmaf(dY[i][1], e, gd[1]);
-                    gd[2] = fmaf(dY[i][2], e, gd[2]);
-                }
-                const float4 mh = rec[kRecMh], ml = rec[kRecMl];
-                const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
-                const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
-                if (nrm > 0.f) {
-                    const float dd = dxv * gd[0] + dyv * gd[1] + dzv * gd[2];
-                    atomicAdd(gr.mu + 3 * (size_t)id + 0, (gd[0] - dxv * dd) / nrm);
-                    atomicAdd(gr.mu + 3 * (size_t)id + 1, (gd[1] - dyv * dd) / nrm);
-                    atomicAdd(gr.mu + 3 * (size_t)id + 2, (gd[2] - dzv * dd) / nrm);
-                }
-            }
+            __syncwarp();
+            qn += m;
+            k0 += m;
+            while (qn >= 32) qn = drain<N, kRay>(sm, wid, lane, qn, 32, a, cb, omega, gr);
         }
         __syncwarp();
     }
+    if (qn > 0) drain<N, kRay>(sm, wid, lane, qn, qn, a, cb, omega, gr);
 }
 
 template <int N, bool kRay>
