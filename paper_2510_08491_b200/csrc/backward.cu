@@ -412,40 +412,75 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch 
             sm.ord[wid][rnk] = (uint32_t)i;
         }
         __syncwarp();
-        // ---- forward transmittance, stop, and the back-to-front adjoints (one lane)
-        if (lane == 0) {
-            float T = 1.f;
-            int last = cnt - 1;
-            for (int k = 0; k < cnt; ++k) {
-                sm.T[wid][k] = T;
-                T *= 1.0f - sm.kap[wid][sm.ord[wid][k]];
-                if (T < a.t_floor) {
-                    last = k;
-                    break;
-                }
-            }
-            const float Tend = T;
-            float U[3] = {Tend * a.bg[0], Tend * a.bg[1], Tend * a.bg[2]};
-            for (int k = last; k >= 0; --k) {
-                const int h = (int)sm.ord[wid][k];
-                const float kp = sm.kap[wid][h];
-                const uint32_t id = sm.id[wid][h];
-                const float4 c4 = hit_rgb<kRay>(recs + (size_t)id * rec_f4(N), a.sh, a.sh_degree, id, ray);
-                const float c[3] = {c4.y, c4.z, c4.w};
-                const float Tk = sm.T[wid][k];
-                const float om = fmaxf(1.0f - kp, 1e-20f);
-                const float gr_[3] = {G.x, G.y, G.z};
-                float dk = G.w * Tend / om;
+        // ---- forward transmittance and stop: chunked warp product-scan of (1 - kappa)
+        float carryT = 1.f, Tend = 1.f;
+        int last = cnt - 1;
+        for (int k0 = 0; k0 < cnt; k0 += 32) {
+            const int k = k0 + lane;
+            const float om = k < cnt ? 1.0f - sm.kap[wid][sm.ord[wid][k]] : 1.0f;
+            float incl = om;
 #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    dk = fmaf(gr_[ch], Tk * c[ch] - U[ch] / om, dk);
-                    sm.gc[wid][k][ch] = c[ch] > 0.f ? Tk * kp * gr_[ch] : 0.f;
-                    U[ch] = fmaf(Tk * kp, c[ch], U[ch]);
-                }
-                sm.gI[wid][k] = kp > 0.f ? dk * (1.0f - kp) : 0.f;
+            for (int o = 1; o < 32; o <<= 1) {
+                const float y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl *= y;
             }
-            sm.ncomp[wid] = last + 1;
+            float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 1.0f;
+            const float Tafter = carryT * incl;
+            if (k < cnt) sm.T[wid][k] = carryT * excl;
+            const uint32_t sb = __ballot_sync(0xffffffffu, k < cnt && Tafter < a.t_floor);
+            if (sb) {   // stop after the first hit that takes T below the floor (Eq. 4)
+                last = k0 + __ffs(sb) - 1;
+                Tend = __shfl_sync(0xffffffffu, Tafter, __ffs(sb) - 1);
+                break;
+            }
+            carryT = __shfl_sync(0xffffffffu, Tafter, 31);
+            Tend = carryT;
         }
+        // ---- back-to-front adjoints: chunked warp suffix sums of T_k kappa_k c_k
+        {
+            float U0 = Tend * a.bg[0], U1 = Tend * a.bg[1], U2 = Tend * a.bg[2];
+            const float gr_[3] = {G.x, G.y, G.z};
+            for (int c0 = (last / 32) * 32; c0 >= 0; c0 -= 32) {
+                const int k = c0 + lane;
+                const bool valid = k <= last;
+                float kp = 0.f, Tk = 0.f, c[3] = {0.f, 0.f, 0.f};
+                if (valid) {
+                    const int h = (int)sm.ord[wid][k];
+                    kp = sm.kap[wid][h];
+                    const uint32_t id = sm.id[wid][h];
+                    const float4 c4 = hit_rgb<kRay>(recs + (size_t)id * rec_f4(N), a.sh, a.sh_degree, id, ray);
+                    c[0] = c4.y; c[1] = c4.z; c[2] = c4.w;
+                    Tk = sm.T[wid][k];
+                }
+                const float w[3] = {Tk * kp * c[0], Tk * kp * c[1], Tk * kp * c[2]};
+                // exclusive suffix sums within the chunk (lanes above this one)
+                float sfx[3] = {w[0], w[1], w[2]};
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float y = __shfl_down_sync(0xffffffffu, sfx[ch], o);
+                        if (lane + o < 32) sfx[ch] += y;
+                    }
+                }
+                const float Uk[3] = {U0 + sfx[0] - w[0], U1 + sfx[1] - w[1], U2 + sfx[2] - w[2]};
+                if (valid) {
+                    const float om = fmaxf(1.0f - kp, 1e-20f);
+                    float dk = G.w * Tend / om;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        dk = fmaf(gr_[ch], Tk * c[ch] - Uk[ch] / om, dk);
+                        sm.gc[wid][k][ch] = c[ch] > 0.f ? Tk * kp * gr_[ch] : 0.f;
+                    }
+                    sm.gI[wid][k] = kp > 0.f ? dk * (1.0f - kp) : 0.f;
+                }
+                U0 += __shfl_sync(0xffffffffu, sfx[0], 0);
+                U1 += __shfl_sync(0xffffffffu, sfx[1], 0);
+                U2 += __shfl_sync(0xffffffffu, sfx[2], 0);
+            }
+        }
+        if (lane == 0) sm.ncomp[wid] = last + 1;
         __syncwarp();
         // ---- queue the composited hits; drain 32 at a time (all lanes busy)
         const int nc = sm.ncomp[wid];
