@@ -190,6 +190,28 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
                                float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
                                float *grad_rotations, float *grad_scales, void *cuda_stream);
 
+/* Training step.  The paper trains with
+ * 3DGS's loss plus a std(s) regulariser and Adam.
+ * snp_loss_l1: L = sum |out_rgb - target_rgb| / (3 n_pixels) over device out_rgba
+ *   [n_pixels][4] and target_rgb [n_pixels][3]; writes grad_rgba = dL/d(out_rgba) (alpha
+ *   channel 0) and ADDS L to the device float *loss.  (3DGS's D-SSIM term is out of scope.)
+ * snp_scale_regularizer: R = weight * mean_i std(s_i) (population std of the semi-axes);
+ *   ADDS dR/ds to grad_scales [n][3] and R to *loss (device).
+ * snp_adam_step: one Adam step (bias-corrected) on every parameter array of the scene, in
+ *   place: grads[8] and lr[8] follow snp_scene_desc's array order (centers, rotations,
+ *   scales, w1, b1, w2, b2, sh); the semi-axes are stepped in log space (dL/dlog s =
+ *   s dL/ds), so they stay positive; the moments live in the scene (zero at the first
+ *   call); step >= 1 counts calls.  Later stages must be re-run (snp_project first). */
+snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n_pixels, float *grad_rgba, float *loss,
+                       void *cuda_stream);
+snp_status snp_scale_regularizer(snp_scene s, float weight, float *grad_scales, float *loss, void *cuda_stream);
+snp_status snp_adam_step(snp_scene s, const float *const *grads, const float *lr, float beta1, float beta2, float eps,
+                         int32_t step, void *cuda_stream);
+/* Copies the scene's current parameters (e.g. after training steps) into dst[8]
+ * (snp_scene_desc order and layouts; host or device memory as `memory` says).  Host
+ * copies synchronise the stream. */
+snp_status snp_get_params(snp_scene s, float *const *dst, int32_t memory, void *cuda_stream);
+
 /* Convenience: snp_project + snp_bin_sort + snp_render. */
 snp_status snp_render_views(snp_scene s, const snp_camera *cams, int32_t n_views,
                             const snp_render_opts *opts, float *out_rgba, void *cuda_stream);

@@ -18,7 +18,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
 # K1's FP64 binning geometry follows a fixed operation order without FMA
 # contraction so it is bit-exact with the binning definition.
 PER_FILE = {"project.cu": ["-fmad=false"]}
-SOURCES = ["api.cu", "project.cu", "records.cu", "binning.cu", "sort.cu", "render.cu", "backward.cu"]
+SOURCES = ["api.cu", "project.cu", "records.cu", "binning.cu", "sort.cu", "render.cu", "backward.cu", "train.cu"]
 
 
 def nvcc() -> str:

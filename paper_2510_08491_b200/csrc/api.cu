@@ -73,6 +73,9 @@ struct snp_scene_s {
     DevBuf<uint32_t> depth;
     DevBuf<float4> records;
     DevBuf<float> w_t;               // temporal weights [n][N] (temporal scenes only)
+    size_t param_off[8] = {};        // byte offsets of the 8 parameter arrays in `params`
+    int64_t param_count[8] = {};     // floats per array
+    DevBuf<float> adam_m, adam_v;    // Adam moments, same layout as `params` (training only)
     bool temporal = false;
     // binning
     int32_t row_begin = 0, row_stride = 1, stripe_rows = 0;
@@ -237,6 +240,10 @@ snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stre
     }
     float **dst[8] = {&s->centers, &s->rotations, &s->scales, &s->w1, &s->b1, &s->w2, &s->b2, &s->sh};
     for (int k = 0; k < 8; ++k) *dst[k] = reinterpret_cast<float *>(reinterpret_cast<char *>(s->params.p) + off[k]);
+    for (int k = 0; k < 8; ++k) {
+        s->param_off[k] = off[k];
+        s->param_count[k] = per[k] * n;
+    }
     r = upload_and_validate(s, d, st);
     if (r != SNP_OK) {
         std::string msg = g_err;
@@ -631,6 +638,77 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     return SNP_OK;
 }
 
+snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n_pixels, float *grad_rgba, float *loss,
+                       void *cuda_stream) {
+    g_err.clear();
+    if (n_pixels < 0) return fail(SNP_ERR_INVALID_ARGUMENT, "n_pixels < 0");
+    if (n_pixels > 0 && (!out_rgba || !target_rgb || !grad_rgba || !loss))
+        return fail(SNP_ERR_INVALID_ARGUMENT, "a pointer is NULL");
+    SNP_CUDA(launch_l1(out_rgba, target_rgb, n_pixels, grad_rgba, loss, (cudaStream_t)cuda_stream));
+    return SNP_OK;
+}
+
+snp_status snp_scale_regularizer(snp_scene s, float weight, float *grad_scales, float *loss, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!grad_scales || !loss) return fail(SNP_ERR_INVALID_ARGUMENT, "a pointer is NULL");
+    if (!(weight >= 0.f) || !std::isfinite(weight)) return fail(SNP_ERR_INVALID_ARGUMENT, "weight must be >= 0");
+    SNP_CUDA(launch_scale_reg(s->scales, s->n, weight, grad_scales, loss, (cudaStream_t)cuda_stream));
+    return SNP_OK;
+}
+
+snp_status snp_adam_step(snp_scene s, const float *const *grads, const float *lr, float beta1, float beta2, float eps,
+                         int32_t step, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!grads || !lr) return fail(SNP_ERR_INVALID_ARGUMENT, "grads or lr is NULL");
+    if (step < 1) return fail(SNP_ERR_INVALID_ARGUMENT, "step must be >= 1");
+    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f))
+        return fail(SNP_ERR_INVALID_ARGUMENT, "need 0 <= beta1, beta2 < 1 and eps > 0");
+    for (int k = 0; k < 8; ++k)
+        if (!grads[k] || !(lr[k] >= 0.f)) return fail(SNP_ERR_INVALID_ARGUMENT, "a gradient is NULL or lr < 0");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if (s->join_pending) {   // K1b may still read the parameters being updated
+        SNP_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+        s->join_pending = false;
+    }
+    if (!s->adam_m.p || s->adam_m.cap < s->params.cap) {
+        SNP_CUDA(s->adam_m.ensure(s->params.cap));
+        SNP_CUDA(s->adam_v.ensure(s->params.cap));
+        SNP_CUDA(cudaMemsetAsync(s->adam_m.p, 0, sizeof(float) * s->adam_m.cap, st));
+        SNP_CUDA(cudaMemsetAsync(s->adam_v.p, 0, sizeof(float) * s->adam_v.cap, st));
+    }
+    float *dst[8] = {s->centers, s->rotations, s->scales, s->w1, s->b1, s->w2, s->b2, s->sh};
+    for (int k = 0; k < 8; ++k) {
+        const size_t o = s->param_off[k] / sizeof(float);
+        // the semi-axes (k = 2) stay positive: their step is taken on log s
+        SNP_CUDA(launch_adam(dst[k], grads[k], s->adam_m.p + o, s->adam_v.p + o, s->param_count[k], lr[k], beta1,
+                             beta2, eps, step, k == 2, st));
+    }
+    s->state = kCreated;   // parameters changed: project again
+    return SNP_OK;
+}
+
+snp_status snp_get_params(snp_scene s, float *const *dst, int32_t memory, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!dst) return fail(SNP_ERR_INVALID_ARGUMENT, "dst is NULL");
+    if (memory != SNP_MEM_HOST && memory != SNP_MEM_DEVICE)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "memory must be SNP_MEM_HOST or SNP_MEM_DEVICE");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const float *src[8] = {s->centers, s->rotations, s->scales, s->w1, s->b1, s->w2, s->b2, s->sh};
+    for (int k = 0; k < 8; ++k) {
+        if (!dst[k]) return fail(SNP_ERR_INVALID_ARGUMENT, "a destination is NULL");
+        SNP_CUDA(cudaMemcpyAsync(dst[k], src[k], sizeof(float) * s->param_count[k],
+                                 memory == SNP_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
+    }
+    if (memory == SNP_MEM_HOST) SNP_CUDA(cudaStreamSynchronize(st));
+    return SNP_OK;
+}
+
 snp_status snp_render_views(snp_scene s, const snp_camera *cams, int32_t n_views, const snp_render_opts *opts,
                             float *out_rgba, void *cuda_stream) {
     snp_status r = snp_project(s, cams, n_views, cuda_stream);
@@ -652,6 +730,8 @@ snp_status snp_destroy(snp_scene s) {
     s->depth.release();
     s->records.release();
     s->w_t.release();
+    s->adam_m.release();
+    s->adam_v.release();
     s->keys0.release();
     s->keys1.release();
     s->vals0.release();

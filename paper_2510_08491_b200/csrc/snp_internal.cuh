@@ -217,6 +217,12 @@ struct BackwardGrads {
     float *mu, *q, *s;             // geometry gradients, or all nullptr (not computed)
 };
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, cudaStream_t st);   // K5's persistent grid for `tiles` work units
+                            float omega, cudaStream_t st);
+// train.cu: L1 loss + gradient, std(s) regulariser, Adam
+cudaError_t launch_l1(const float *out_rgba, const float *target_rgb, int64_t n, float *grad_rgba, float *loss,
+                      cudaStream_t st);
+cudaError_t launch_scale_reg(const float *s, int64_t n, float w, float *grad_s, float *loss, cudaStream_t st);
+cudaError_t launch_adam(float *p, const float *g, float *m, float *v, int64_t count, float lr, float b1, float b2,
+                        float eps, int step, bool log_space, cudaStream_t st);   // K5's persistent grid for `tiles` work units
 
 }  // namespace snp

@@ -29,7 +29,7 @@ SNP_COLOUR_RAY = 1        # colour_mode: SH at each pixel's ray direction
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
            "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at",
-           "snp_render_backward")
+           "snp_render_backward", "snp_loss_l1", "snp_scale_regularizer", "snp_adam_step", "snp_get_params")
 
 
 class SnpError(RuntimeError):
@@ -90,6 +90,11 @@ def lib():
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
             L.snp_set_temporal.argtypes = [vp, vp, C.c_int32, vp]
             L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+            L.snp_loss_l1.argtypes = [vp, vp, C.c_int64, vp, vp, vp]
+            L.snp_get_params.argtypes = [vp, C.POINTER(vp), C.c_int32, vp]
+            L.snp_scale_regularizer.argtypes = [vp, C.c_float, vp, vp, vp]
+            L.snp_adam_step.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_float), C.c_float, C.c_float, C.c_float,
+                                        C.c_int32, vp]
             L.snp_project_at.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp, vp]
             L.snp_get_debug_counters.argtypes = [vp, vp, C.c_int32, vp]
             for f in EXPORTS:
@@ -236,6 +241,39 @@ def render_backward(h, opts, grad_rgba, grads, stream=None):
                                      _ptr(grads["w2"]), _ptr(grads["b2"]), _ptr(grads["sh"]),
                                      _ptr(grads.get("centers")), _ptr(grads.get("rotations")),
                                      _ptr(grads.get("scales")), _stream(stream)))
+
+
+# P:735 learning rates (MLP 1e-3, means 1.6e-4, scales 5e-3, quaternions 1e-3, SH 2.5e-3)
+PAPER_LR = {"centers": 1.6e-4, "rotations": 1e-3, "scales": 5e-3, "w1": 1e-3, "b1": 1e-3, "w2": 1e-3, "b2": 1e-3,
+            "sh": 2.5e-3}
+
+
+def loss_l1(out_rgba, target_rgb, grad_rgba, loss, stream=None):
+    """L1 photometric loss: writes dL/d(out) into grad_rgba and adds L to loss (CUDA
+    tensors: out [..., 4], target [..., 3], loss a 1-element float tensor)."""
+    n = out_rgba.numel() // 4
+    _check(lib().snp_loss_l1(_ptr(out_rgba), _ptr(target_rgb), n, _ptr(grad_rgba), _ptr(loss), _stream(stream)))
+
+
+def scale_regularizer(h, weight, grad_scales, loss, stream=None):
+    _check(lib().snp_scale_regularizer(h, float(weight), _ptr(grad_scales), _ptr(loss), _stream(stream)))
+
+
+def adam_step(h, grads, step, lr=None, beta1=0.9, beta2=0.999, eps=1e-15, stream=None):
+    """One Adam step on the scene's parameters (grads: dict of CUDA tensors by FIELDS)."""
+    lr = dict(PAPER_LR, **(lr or {}))
+    ptrs = (C.c_void_p * 8)(*[_ptr(grads[f]) for f in FIELDS])
+    lrs = (C.c_float * 8)(*[float(lr[f]) for f in FIELDS])
+    _check(lib().snp_adam_step(h, ptrs, lrs, float(beta1), float(beta2), float(eps), int(step), _stream(stream)))
+
+
+def copy_params(h, dst, stream=None):
+    """Copies the scene's current parameters into dst (dict by FIELDS of CUDA tensors or
+    numpy arrays, all on the same side)."""
+    first = dst[FIELDS[0]]
+    mem = SNP_MEM_DEVICE if _is_device(first) else SNP_MEM_HOST
+    ptrs = (C.c_void_p * 8)(*[_ptr(dst[f]) for f in FIELDS])
+    _check(lib().snp_get_params(h, ptrs, mem, _stream(stream)))
 
 
 def destroy(h):

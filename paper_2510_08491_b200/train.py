@@ -1,0 +1,65 @@
+"""Data-parallel training step over camera views: every rank
+renders its own views, takes the L1 loss (+ optional std(s) regulariser) and K7's
+gradients, ONE all-reduce averages the flat gradient buffer over the ranks (NCCL over
+NVLink on a multi-GPU node; gloo in the CPU tests), and every rank applies the same Adam
+step to its replica of the parameters.  All arithmetic runs in libsnp's kernels; this
+module only owns buffers and the collective."""
+from __future__ import annotations
+
+import numpy as np
+
+from . import snp
+
+
+def flat_grads(scene, device):
+    """One contiguous float32 buffer with a view per parameter array (FIELDS order), so
+    that the gradient exchange is a single all-reduce."""
+    import torch
+    shapes = [tuple(np.asarray(getattr(scene, f)).shape) for f in snp.FIELDS]
+    sizes = [int(np.prod(s)) for s in shapes]
+    flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
+    views, o = {}, 0
+    for f, s, n in zip(snp.FIELDS, shapes, sizes):
+        views[f] = flat[o:o + n].view(s)
+        o += n
+    return flat, views
+
+
+def allreduce_mean(flat, group=None):
+    """Sums the flat gradient buffer over the ranks and divides by the world size."""
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return flat
+    dist.all_reduce(flat, group=group)
+    flat.div_(dist.get_world_size(group))
+    return flat
+
+
+class Trainer:
+    """Owns the per-rank buffers of one scene handle: image, dL/d(image), flat gradients,
+    the loss scalar and the Adam step counter."""
+
+    def __init__(self, h, scene, n_views, height, width, device, lr=None, reg_weight=0.0, opts=None):
+        import torch
+        self.h, self.lr, self.reg = h, lr, float(reg_weight)
+        self.opts = opts if opts is not None else snp.make_opts()
+        self.out = torch.zeros((n_views, height, width, 4), device=device)
+        self.gout = torch.zeros_like(self.out)
+        self.flat, self.grads = flat_grads(scene, device)
+        self.loss = torch.zeros(1, device=device)
+        self.step_count = 0
+
+    def step(self, cams, target_rgb, group=None):
+        """One training step on this rank's views; returns this rank's loss (a device
+        scalar, read by the caller when it wants it)."""
+        self.flat.zero_()
+        self.loss.zero_()
+        snp.render_views(self.h, cams, self.opts, self.out)
+        snp.loss_l1(self.out, target_rgb, self.gout, self.loss)
+        snp.render_backward(self.h, self.opts, self.gout, self.grads)
+        if self.reg > 0.0:
+            snp.scale_regularizer(self.h, self.reg, self.grads["scales"], self.loss)
+        allreduce_mean(self.flat, group)
+        self.step_count += 1
+        snp.adam_step(self.h, self.grads, self.step_count, self.lr)
+        return self.loss

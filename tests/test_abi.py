@@ -22,7 +22,7 @@ def snp():
 
 def test_exports_match_header(snp):
     hdr = open(os.path.join(ROOT, "include", "snp.h")).read()
-    declared = set(re.findall(r"\b(snp_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(snp_[a-z0-9_]+)\s*\(", hdr))
     assert declared == set(snp.EXPORTS), declared ^ set(snp.EXPORTS)
     L = snp.lib()
     for name in declared:

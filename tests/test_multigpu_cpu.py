@@ -85,3 +85,42 @@ def test_merge_stripes():
     m = mg.merge_stripes(fr, H)
     for y in range(H):
         assert m[0, y, 0, 0].item() == (y // 16) % 3
+
+
+def _train_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from paper_2510_08491_b200 import train
+        flat, views = train.flat_grads(synth.make_scene(5, 9), "cpu")
+        for k, f in enumerate(views):            # rank-dependent per-field gradients
+            views[f].fill_(float((rank + 1) * (k + 1)))
+        train.allreduce_mean(flat)
+        q.put((rank, {f: views[f].flatten()[0].item() for f in views}, flat.numel()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gradient_allreduce():
+    """the training step's single gradient exchange -- one flat
+    buffer (views per parameter array) averaged over the ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_train_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r = q.get(timeout=120)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 9
+    assert res[0][2] == n * (3 + 4 + 3 + 24 + 8 + 8 + 1 + 48)
+    for rank in (0, 1):
+        for k, (f, v) in enumerate(res[rank][1].items()):
+            assert v == pytest.approx(1.5 * (k + 1)), (rank, f, v)   # mean of 1x and 2x
