@@ -162,6 +162,9 @@ snp_status snp_project(snp_scene s, const snp_camera *cams, int32_t n_views, voi
 snp_status snp_set_temporal(snp_scene s, const float *w_t, int32_t memory, void *cuda_stream);
 snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, const float *xi_t,
                           void *cuda_stream);
+/* Training temporal scenes: snp_render_backward also ADDS dL/dW_t into grad_w_t (device
+ * [n][N], caller-owned and zeroed; NULL = not computed) while temporal weights are set. */
+snp_status snp_set_temporal_grad(snp_scene s, float *grad_w_t);
 
 /* K2-K4: keys (view | tile | depth) in primitive order, stable LSD radix sort,
  * per-(view, tile) ranges.  Uses opts->tile_row_begin/stride and sync_check. */

@@ -76,6 +76,7 @@ struct snp_scene_s {
     size_t param_off[8] = {};        // byte offsets of the 8 parameter arrays in `params`
     int64_t param_count[8] = {};     // floats per array
     DevBuf<float> adam_m, adam_v;    // Adam moments, same layout as `params` (training only)
+    float *grad_w_t = nullptr;       // where snp_render_backward adds dL/dW_t (caller-owned, device)
     bool temporal = false;
     // binning
     int32_t row_begin = 0, row_stride = 1, stripe_rows = 0;
@@ -311,6 +312,14 @@ snp_status snp_set_temporal(snp_scene s, const float *w_t, int32_t memory, void 
                     "non-finite temporal weight at primitive " + std::to_string(s->h_flag[1] / s->n_hidden));
     }
     s->temporal = true;
+    return SNP_OK;
+}
+
+snp_status snp_set_temporal_grad(snp_scene s, float *grad_w_t) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    s->grad_w_t = grad_w_t;
     return SNP_OK;
 }
 
@@ -633,7 +642,8 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     for (int c = 0; c < 3; ++c) a.bg[c] = opts->background[c];
     a.t_floor = opts->transmittance_floor;
     a.counters = s->counters.p;
-    BackwardGrads g{grad_w1, grad_b1, grad_w2, grad_b2, grad_sh, grad_centers, grad_rotations, grad_scales};
+    BackwardGrads g{grad_w1, grad_b1, grad_w2, grad_b2, grad_sh, grad_centers, grad_rotations, grad_scales,
+                    s->temporal ? s->grad_w_t : nullptr};
     for (const CamBatch &cb : s->cams) SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, st));
     return SNP_OK;
 }

@@ -65,7 +65,7 @@ __device__ __forceinline__ float dsinc_f(float x) {
 // dt = t1 - t0, tau_m = (t0 + t1)/2, W1' = omega W1 / ||s||_inf.
 template <int N>
 __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const Ray &r, float gI, float omega,
-                                         uint32_t prim, const RenderArgs &ra, const BackwardGrads &gr) {
+                                         uint32_t prim, const RenderArgs &ra, const BackwardGrads &gr, float xi_t) {
     const float4 mh = rec[kRecMh];
     const float4 ml = rec[kRecMl];
     const float4 w0 = rec[kRecWh0];
@@ -138,6 +138,8 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
             gsmax -= (gw[0] * u.x + gw[1] * u.y + gw[2] * u.z) / smax;
             atomicAdd(gr.w2 + wbase + k, gI * dt * cs * S);
             atomicAdd(gr.b1 + wbase + k, gI * omega * coef);
+            // temporal scene: the record's phase offset is omega (b1 + xi_t W_t) (R24)
+            if (gr.wt) atomicAdd(gr.wt + wbase + k, gI * omega * coef * xi_t);
             atomicAdd(gr.w1 + 3 * (wbase + k) + 0, gI * s1 * gw[0]);
             atomicAdd(gr.w1 + 3 * (wbase + k) + 1, gI * s1 * gw[1]);
             atomicAdd(gr.w1 + 3 * (wbase + k) + 2, gI * s1 * gw[2]);
@@ -267,9 +269,10 @@ __device__ __forceinline__ void sh_basis_f(float x, float y, float z, float Y[16
 // Every parameter gradient of one composited hit (dL/dI = gI, dL/dc = gc).
 template <int N, bool kRay>
 __device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 *rec, const Ray &ray, uint32_t id,
-                                              float gI, const float gc[3], float omega, const BackwardGrads &gr) {
+                                              float gI, const float gc[3], float omega, const BackwardGrads &gr,
+                                              float xi_t) {
     const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
-    hit_grad<N>(rec, ray, gI, omega, id, a, gr);
+    hit_grad<N>(rec, ray, gI, omega, id, a, gr, xi_t);
     // SH colour: dc/dsh_lm = Y_lm(dir) (unclamped channels)
     float dxv, dyv, dzv;
     if (kRay) {
@@ -328,7 +331,7 @@ __device__ __forceinline__ int drain(BwSmem &sm, int wid, int lane, int qn, int 
         r.t_far = cb.cams[vl].t_far;
         const float gc[3] = {sm.q_gc[wid][0][lane], sm.q_gc[wid][1][lane], sm.q_gc[wid][2][lane]};
         const float4 *rec = a.records + ((size_t)(cb.view0 + vl) * (size_t)a.n + id) * rec_f4(N);
-        hit_all_grads<N, kRay>(a, rec, r, id, sm.q_gI[wid][lane], gc, omega, gr);
+        hit_all_grads<N, kRay>(a, rec, r, id, sm.q_gI[wid][lane], gc, omega, gr, cb.cams[vl].xi_t);
     }
     __syncwarp();
     const int rest = qn - cnt;

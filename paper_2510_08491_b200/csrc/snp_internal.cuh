@@ -215,6 +215,7 @@ int render_grid(int n_hidden, bool colour_ray, int tiles);
 struct BackwardGrads {
     float *w1, *b1, *w2, *b2, *sh;
     float *mu, *q, *s;             // geometry gradients, or all nullptr (not computed)
+    float *wt;                     // temporal weights' gradient [n][N], or nullptr
 };
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
                             float omega, cudaStream_t st);

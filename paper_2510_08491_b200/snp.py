@@ -29,7 +29,8 @@ SNP_COLOUR_RAY = 1        # colour_mode: SH at each pixel's ray direction
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
            "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at",
-           "snp_render_backward", "snp_loss_l1", "snp_scale_regularizer", "snp_adam_step", "snp_get_params")
+           "snp_render_backward", "snp_loss_l1", "snp_scale_regularizer", "snp_adam_step", "snp_get_params",
+           "snp_set_temporal_grad")
 
 
 class SnpError(RuntimeError):
@@ -92,6 +93,7 @@ def lib():
             L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
             L.snp_loss_l1.argtypes = [vp, vp, C.c_int64, vp, vp, vp]
             L.snp_get_params.argtypes = [vp, C.POINTER(vp), C.c_int32, vp]
+            L.snp_set_temporal_grad.argtypes = [vp, vp]
             L.snp_scale_regularizer.argtypes = [vp, C.c_float, vp, vp, vp]
             L.snp_adam_step.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_float), C.c_float, C.c_float, C.c_float,
                                         C.c_int32, vp]
@@ -200,6 +202,11 @@ def project(h, cams, stream=None, xi_t=None):
         _check(lib().snp_project(h, arr, len(arr), _stream(stream)))
     else:
         _check(lib().snp_project_at(h, arr, len(arr), t.ctypes.data_as(C.c_void_p), _stream(stream)))
+
+
+def set_temporal_grad(h, grad_w_t):
+    """Where snp_render_backward adds dL/dW_t (a zeroed CUDA tensor [n, N]) or None."""
+    _check(lib().snp_set_temporal_grad(h, _ptr(grad_w_t)))
 
 
 def set_temporal(h, w_t, stream=None):

@@ -648,3 +648,60 @@ def test_training_step_reduces_loss():
         snp.destroy(h)
     print("training losses", [round(l, 4) for l in losses[::8]], round(losses[-1], 4))
     assert np.all(np.isfinite(losses)) and losses[-1] < 0.6 * losses[0], losses
+
+
+def test_backward_temporal_weights_vs_finite_differences(orc):
+    """K7 on a temporal scene (R24): dL/dW_t = xi_t omega dI/d(omega b1) per hit, and b1's
+    gradient, against central differences of the oracle at a view timestamp xi_t = 0.6."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene = synth.make_scene(81, 150, box=0.6)
+    scene.w2 *= np.float32(0.1)
+    scene.b2[:] = (1.2 * np.abs(scene.w2).sum(1)).astype(np.float32)
+    rng = np.random.default_rng(82)
+    scene.w_t = rng.uniform(-1, 1, (scene.n, scene.n_hidden)).astype(np.float32)
+    cam = synth.orbit_cameras(1, 3.0, 64, 48, 60.0)[0]
+    cam.xi_t = 0.6
+    bg = (0.1, 0.2, 0.3)
+    G = rng.normal(size=(1, 48, 64, 4)).astype(np.float32)
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        snp.set_temporal(h, scene.w_t)
+        gwt = torch.zeros(scene.w_t.shape, device="cuda")
+        snp.set_temporal_grad(h, gwt)
+        opts = snp.make_opts(bg)
+        out = torch.zeros((1, 48, 64, 4), device="cuda")
+        snp.render_views(h, [cam], opts, out, xi_t=[0.6])
+        grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in ("w1", "b1", "w2", "b2", "sh")}
+        snp.render_backward(h, opts, torch.from_numpy(G).cuda(), grads)
+        torch.cuda.synchronize()
+        g = {"w_t": gwt.cpu().numpy().astype(np.float64), "b1": grads["b1"].cpu().numpy().astype(np.float64)}
+    finally:
+        snp.destroy(h)
+
+    def loss(sc):
+        img, _, _ = orc.render_frame(sc, cam, bg)
+        return float((img * G[0].astype(np.float64)).sum())
+
+    hit = np.nonzero(np.abs(grads["b2"].cpu().numpy()) > 0)[0]
+    checks = []
+    for f in ("w_t", "b1"):
+        arr = getattr(scene, f)
+        for _ in range(10):
+            idx = (int(rng.choice(hit)), int(rng.integers(0, scene.n_hidden)))
+            base = float(arr[idx])
+            step = np.float32(2e-3 * (abs(base) + 0.05))
+            vals = []
+            for sgn in (1, -1):
+                arr[idx] = np.float32(base + sgn * step)
+                vals.append(loss(scene))
+            arr[idx] = np.float32(base)
+            hp, hm = float(np.float32(base + step)) - base, base - float(np.float32(base - step))
+            checks.append((f, idx, float(g[f][idx]), (vals[0] - vals[1]) / (hp + hm)))
+    scale = max(abs(c[3]) for c in checks)
+    bad = [c for c in checks if abs(c[2] - c[3]) > 2e-3 * abs(c[3]) + 2e-4 * scale]
+    assert not bad, (bad, scale)
+    for c in checks:       # dL/dW_t = xi_t dL/db1 for the same unit (one view)
+        if c[0] == "w_t":
+            assert abs(c[2] - 0.6 * g["b1"][c[1]]) <= 1e-5 * (abs(c[2]) + 1e-3)
