@@ -30,6 +30,9 @@ snp_status fail(snp_status st, const std::string &msg) {
     } while (0)
 
 enum State { kCreated = 0, kProjected = 1, kBinned = 2 };
+// K5 emits after every exact round when the tile lists average more keys than this
+// (DESIGN.md "K5 design" 7: C5 221 keys/tile -> eager; C3 90, C2 18 -> default)
+constexpr double kEagerKeysPerTile = 150.0;
 
 // Device buffer that only grows.
 template <typename T>
@@ -106,6 +109,11 @@ struct snp_scene_s {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool join_pending = false;
     bool render_dirty = false;       // a render has used the counters since the last binning
+    // K5's eager mid-batch emission: set by a synchronising snp_bin_sort when the tile
+    // lists are long (more than kEagerKeysPerTile keys per tile on average), where the
+    // pending lists overflow into K6 otherwise (a function of the binning only, so the
+    // same frame always renders the same way)
+    bool eager_emit = false;
 };
 
 namespace snp {
@@ -466,6 +474,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
         SNP_CUDA(cudaMemcpyAsync(s->h_counters + kCntDup, s->counters.p + kCntDup, sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, st));
         SNP_CUDA(cudaStreamSynchronize(st));
+        s->eager_emit = (double)s->h_counters[kCntDup] > kEagerKeysPerTile * (double)slots;
         const int64_t ndup = (int64_t)s->h_counters[kCntDup];
         s->known_ndup = ndup;
         if (ndup > s->key_capacity) {
@@ -561,6 +570,8 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     RenderArgs a{};
     a.n_hidden = s->n_hidden;
     a.colour_ray = opts->colour_mode == SNP_COLOUR_RAY ? 1 : 0;
+    a.eager_emit = s->eager_emit ? 1 : 0;
+    if (const char *ee = std::getenv("SNP_EAGER_EMIT")) a.eager_emit = std::atoi(ee) != 0;   // A/B override
     a.sh = s->sh;
     a.sh_degree = s->sh_degree;
     a.tiles_x = s->tiles_x;
@@ -587,7 +598,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     a.fallback_capacity = s->fallback_capacity;
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     a.counters = s->counters.p;
-    a.k5_grid = render_grid(s->n_hidden, a.colour_ray != 0, s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
+    a.k5_grid = render_grid(s->n_hidden, a.colour_ray != 0, a.eager_emit != 0, s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
         for (size_t k = 0; k < s->cams.size(); ++k) {

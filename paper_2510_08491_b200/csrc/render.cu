@@ -197,7 +197,7 @@ __device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimi
     ++pd.n;
 }
 
-template <int N, bool kRay>
+template <int N, bool kRay, bool kEager>
 __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
     constexpr int kStages = Cfg<N>::kStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -572,8 +572,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     ps.done = true;
                 }
                 // batch end: everything in later batches has t_in >= L of the next key;
-                // mid-batch: only when the pending list runs full
-                if (!ps.done && (batch_end || pd.n > plimit - 4)) {
+                // mid-batch: every hit not inserted yet comes from record jn or later, so
+                // L[jn] bounds it.  Default: only when the pending list runs nearly full;
+                // kEager: after every exact round -- shorter pending lists (fewer K6
+                // pixels), earlier termination; chosen per scene from the overflow rate
+                if (!ps.done && (batch_end || pd.n > (kEager ? 0 : plimit - 4))) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
                     ++ins_ecalls;
@@ -993,30 +996,31 @@ __global__ void __launch_bounds__(1024) k_tile_order(RenderArgs a, CamBatch cb, 
 }  // namespace
 
 namespace {
-template <int N, bool kRay>
+template <int N, bool kRay, bool kEager>
 int render_grid_n(int tiles) {
     static int resident = 0;   // persistent grid: every CTA that fits, all SMs
     if (!resident) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_render<N, kRay>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<N>));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N, kRay>, kThreads, sizeof(Smem<N>));
+        cudaFuncSetAttribute(k_render<N, kRay, kEager>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem<N>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N, kRay, kEager>, kThreads, sizeof(Smem<N>));
         resident = std::max(1, sms) * std::max(1, per_sm);
     }
     return std::min(tiles, resident);
 }
 
-template <int N, bool kRay>
+template <int N, bool kRay, bool kEager>
 cudaError_t launch_render_n(const RenderArgs &a, const CamBatch &cams, int tiles, cudaStream_t st) {
     static bool attr_set = false;
     const int smem = (int)sizeof(Smem<N>);
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay, kEager>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    k_render<N, kRay><<<render_grid_n<N, kRay>(tiles), kThreads, smem, st>>>(a, cams);
+    k_render<N, kRay, kEager><<<render_grid_n<N, kRay, kEager>(tiles), kThreads, smem, st>>>(a, cams);
     return cudaGetLastError();
 }
 
@@ -1040,11 +1044,16 @@ cudaError_t launch_fallback_n(const RenderArgs &a, const CamBatch *cams, int n_b
 
 template <int N>
 cudaError_t launch_render_w(const RenderArgs &a, const CamBatch &cams, int tiles, cudaStream_t st) {
-    return a.colour_ray ? launch_render_n<N, true>(a, cams, tiles, st) : launch_render_n<N, false>(a, cams, tiles, st);
+    if (a.eager_emit)
+        return a.colour_ray ? launch_render_n<N, true, true>(a, cams, tiles, st)
+                            : launch_render_n<N, false, true>(a, cams, tiles, st);
+    return a.colour_ray ? launch_render_n<N, true, false>(a, cams, tiles, st)
+                        : launch_render_n<N, false, false>(a, cams, tiles, st);
 }
 template <int N>
-int render_grid_w(bool ray, int tiles) {
-    return ray ? render_grid_n<N, true>(tiles) : render_grid_n<N, false>(tiles);
+int render_grid_w(bool ray, bool eager, int tiles) {
+    if (eager) return ray ? render_grid_n<N, true, true>(tiles) : render_grid_n<N, false, true>(tiles);
+    return ray ? render_grid_n<N, true, false>(tiles) : render_grid_n<N, false, false>(tiles);
 }
 template <int N>
 cudaError_t launch_fallback_w(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
@@ -1069,12 +1078,12 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
     }
 }
 
-int render_grid(int n_hidden, bool colour_ray, int tiles) {
+int render_grid(int n_hidden, bool colour_ray, bool eager, int tiles) {
     switch (n_hidden) {
-        case 4: return render_grid_w<4>(colour_ray, tiles);
-        case 16: return render_grid_w<16>(colour_ray, tiles);
-        case 32: return render_grid_w<32>(colour_ray, tiles);
-        default: return render_grid_w<8>(colour_ray, tiles);
+        case 4: return render_grid_w<4>(colour_ray, eager, tiles);
+        case 16: return render_grid_w<16>(colour_ray, eager, tiles);
+        case 32: return render_grid_w<32>(colour_ray, eager, tiles);
+        default: return render_grid_w<8>(colour_ray, eager, tiles);
     }
 }
 

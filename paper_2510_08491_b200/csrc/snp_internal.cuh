@@ -174,6 +174,7 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
 struct RenderArgs {
     int32_t n_hidden;              // N_sigma (hidden_supported): selects the kernel instantiation
     int32_t colour_ray;            // 1: SH colour at each pixel's ray direction (SNP_COLOUR_RAY)
+    int32_t eager_emit;            // K5 blends after every exact round (not only near-full lists)
     const float *sh;               // scene SH coefficients [n][16][3] (per-ray colour)
     int32_t sh_degree;
     const float *scales;           // scene semi-axes [n][3] (backward)
@@ -208,7 +209,7 @@ cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_
 // CTAs leave, take overflowed pixels as K5 queues them and end once every K5 CTA has
 // exited.  With several batches it runs after all of them.
 cudaError_t launch_fallback(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st);
-int render_grid(int n_hidden, bool colour_ray, int tiles);
+int render_grid(int n_hidden, bool colour_ray, bool eager, int tiles);
 // K7 (backward.cu): adds dL/d{W1, b1, W2, b2, SH} for grad = dL/d(out RGBA) of one camera
 // batch, re-deriving each pixel's forward (whole image; counters[kCntBwdSkipped] counts
 // pixels with more hits than the kernel holds)

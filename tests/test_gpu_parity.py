@@ -705,3 +705,25 @@ def test_backward_temporal_weights_vs_finite_differences(orc):
     for c in checks:       # dL/dW_t = xi_t dL/db1 for the same unit (one view)
         if c[0] == "w_t":
             assert abs(c[2] - 0.6 * g["b1"][c[1]]) <= 1e-5 * (abs(c[2]) + 1e-3)
+
+
+def test_eager_emission_rule(orc, monkeypatch):
+    """K5's eager mid-batch emission (kEager) is chosen from the binning alone (mean keys
+    per tile > 150): on for C5 (221), off for C3 (90); on C5 it hands fewer pixels to K6
+    than the forced default mode, on C3 nothing changes, and the C5 fallback pixels keep
+    parity."""
+    scene5, cams5, bg5 = synth.make_config("C5")
+    eager = gpu_render(scene5, cams5, bg5)
+    monkeypatch.setenv("SNP_EAGER_EMIT", "0")
+    forced = gpu_render(scene5, cams5, bg5)
+    monkeypatch.delenv("SNP_EAGER_EMIT")
+    assert eager["stats"]["overflow_pixels"] < 0.6 * forced["stats"]["overflow_pixels"]
+    scene3, cams3, bg3 = synth.make_config("C3")
+    a = gpu_render(scene3, cams3, bg3)
+    monkeypatch.setenv("SNP_EAGER_EMIT", "0")
+    b = gpu_render(scene3, cams3, bg3)
+    assert np.array_equal(a["img"], b["img"]) and a["stats"] == b["stats"]
+    px, py = sample_pixels(cams5[0], 600, 2, seed=11)
+    out_o, fl, _ = orc.render_pixels(scene5, cams5[0], px, py, bg5)
+    c = compare(eager["img"][0][py, px], out_o, fl)
+    assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
