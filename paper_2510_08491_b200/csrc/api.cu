@@ -79,6 +79,7 @@ struct snp_scene_s {
     size_t param_off[8] = {};        // byte offsets of the 8 parameter arrays in `params`
     int64_t param_count[8] = {};     // floats per array
     DevBuf<float> adam_m, adam_v;    // Adam moments, same layout as `params` (training only)
+    DevBuf<uint32_t> bw_queue;       // K7: pixels with more hits than its first pass holds
     float *grad_w_t = nullptr;       // where snp_render_backward adds dL/dW_t (caller-owned, device)
     bool temporal = false;
     // binning
@@ -638,6 +639,8 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     a.sh_degree = s->sh_degree;
     a.scales = s->scales;
     a.rotations = s->rotations;
+    SNP_CUDA(s->bw_queue.ensure((size_t)std::max<int64_t>(1, (int64_t)s->n_views * s->W * s->H)));
+    a.bw_queue = s->bw_queue.p;
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
     a.tiles_per_view = s->tiles_x * s->tiles_y;
@@ -752,6 +755,7 @@ snp_status snp_destroy(snp_scene s) {
     s->records.release();
     s->w_t.release();
     s->adam_m.release();
+    s->bw_queue.release();
     s->adam_v.release();
     s->keys0.release();
     s->keys1.release();

@@ -20,7 +20,8 @@
 //   dI/dW1_k = (omega / ||s||_inf) dt W2_k (-sin(phi_k) S_k (p + tau_m d) + cos(phi_k) S'_k (dt/2) d),
 //   S_k = sinc(h_k dt / 2), S' = d sinc / dx.
 // Gradients are accumulated with fp32 atomics.  Pixels with more than kBwHits hits are
-// skipped and counted in counters[kCntBwdSkipped].
+// redone by one-warp CTAs that hold kBwBigHits; beyond that they are skipped and counted
+// in counters[kCntBwdSkipped].
 #include "hit.cuh"
 #include "snp_internal.cuh"
 
@@ -31,7 +32,10 @@ constexpr int kBwWarps = 8;
 constexpr int kBwThreads = kBwWarps * 32;
 constexpr int kBwHits = 256;
 constexpr int kBwQueue = 64;
+// pixels with more than kBwHits hits are redone by one-warp CTAs holding kBwBigHits
+constexpr int kBwBigHits = 2048;
 
+template <int kBwWarps, int kBwHits>
 struct BwSmem {
     float th[kBwWarps][kBwHits], tl[kBwWarps][kBwHits], kap[kBwWarps][kBwHits];
     uint32_t id[kBwWarps][kBwHits];
@@ -319,8 +323,8 @@ __device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 
 
 // Processes the first `cnt` (<= 32) entries of the warp's queue, one per lane, and moves
 // the rest to the front; returns the new queue length.
-template <int N, bool kRay>
-__device__ __forceinline__ int drain(BwSmem &sm, int wid, int lane, int qn, int cnt, const RenderArgs &a,
+template <int N, bool kRay, class Sm>
+__device__ __forceinline__ int drain(Sm &sm, int wid, int lane, int qn, int cnt, const RenderArgs &a,
                                      const CamBatch &cb, float omega, const BackwardGrads &gr) {
     if (lane < cnt) {
         Ray r;
@@ -350,17 +354,21 @@ __device__ __forceinline__ int drain(BwSmem &sm, int wid, int lane, int qn, int 
     return rest;
 }
 
-template <int N, bool kRay>
-__global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch cb, const float4 *__restrict__ grad,
-                                                         BackwardGrads gr, float omega) {
+template <int N, bool kRay, int kBwWarps, int kBwHits>
+__global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBatch cb, const float4 *__restrict__ grad,
+                                                            BackwardGrads gr, float omega, const uint32_t *queue_in,
+                                                            uint32_t *queue_out) {
     extern __shared__ __align__(16) unsigned char bw_raw[];
-    BwSmem &sm = *reinterpret_cast<BwSmem *>(bw_raw);
+    using Sm = BwSmem<kBwWarps, kBwHits>;
+    Sm &sm = *reinterpret_cast<Sm *>(bw_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const int W = cb.cams[0].W, H = cb.cams[0].H;
-    const int64_t npix = (int64_t)cb.nv * W * H;
+    // queue_in: only the listed pixels (count in counters[kCntBwdQueue]); else every pixel
+    const int64_t npix = queue_in ? (int64_t)a.counters[kCntBwdQueue] : (int64_t)cb.nv * W * H;
     int qn = 0;   // entries in this warp's gradient queue
-    for (int64_t pi = (int64_t)blockIdx.x * kBwWarps + wid; pi < npix; pi += (int64_t)gridDim.x * kBwWarps) {
+    for (int64_t qi = (int64_t)blockIdx.x * kBwWarps + wid; qi < npix; qi += (int64_t)gridDim.x * kBwWarps) {
+        const int64_t pi = queue_in ? (int64_t)queue_in[qi] : qi;
         const int vloc = (int)(pi / ((int64_t)W * H));
         const int rem = (int)(pi - (int64_t)vloc * W * H);
         const int y = rem / W, x = rem - y * W;
@@ -400,8 +408,11 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch 
             }
             cnt += __popc(m);
         }
-        if (cnt > kBwHits) {
-            if (lane == 0) atomicAdd(a.counters + kCntBwdSkipped, 1ull);
+        if (cnt > kBwHits) {   // to the big-capacity pass, or (there) skipped and counted
+            if (lane == 0) {
+                if (queue_out) queue_out[atomicAdd(a.counters + kCntBwdQueue, 1ull)] = (uint32_t)pi;
+                else atomicAdd(a.counters + kCntBwdSkipped, 1ull);
+            }
             continue;
         }
         __syncwarp();
@@ -503,32 +514,44 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(RenderArgs a, CamBatch 
             __syncwarp();
             qn += m;
             k0 += m;
-            while (qn >= 32) qn = drain<N, kRay>(sm, wid, lane, qn, 32, a, cb, omega, gr);
+            while (qn >= 32) qn = drain<N, kRay, Sm>(sm, wid, lane, qn, 32, a, cb, omega, gr);
         }
         __syncwarp();
     }
-    if (qn > 0) drain<N, kRay>(sm, wid, lane, qn, qn, a, cb, omega, gr);
+    if (qn > 0) drain<N, kRay, Sm>(sm, wid, lane, qn, qn, a, cb, omega, gr);
+}
+
+template <int N, bool kRay, int kW, int kH>
+int backward_resident() {
+    static int resident = 0;
+    if (!resident) {
+        const int smem = (int)sizeof(BwSmem<kW, kH>);
+        cudaFuncSetAttribute(k_backward<N, kRay, kW, kH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward<N, kRay, kW, kH>, kW * 32, smem);
+        resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
+    }
+    return resident;
 }
 
 template <int N, bool kRay>
 cudaError_t launch_backward_n(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
                               float omega, cudaStream_t st) {
-    static int resident = 0;
-    const int smem = (int)sizeof(BwSmem);
-    if (!resident) {
-        cudaError_t e = cudaFuncSetAttribute(k_backward<N, kRay>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward<N, kRay>, kBwThreads, smem);
-        resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
-    }
     const int64_t npix = (int64_t)cb.nv * cb.cams[0].W * cb.cams[0].H;
+    if (npix == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.counters + kCntBwdQueue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    const int res = backward_resident<N, kRay, kBwWarps, kBwHits>();
     const int64_t want = (npix + kBwWarps - 1) / kBwWarps;
-    const unsigned grid = (unsigned)(want < resident ? want : resident);
-    if (grid == 0) return cudaSuccess;
-    k_backward<N, kRay><<<grid, kBwThreads, smem, st>>>(a, cb, reinterpret_cast<const float4 *>(grad), g, omega);
+    k_backward<N, kRay, kBwWarps, kBwHits><<<(unsigned)(want < res ? want : res), kBwThreads,
+                                              sizeof(BwSmem<kBwWarps, kBwHits>), st>>>(
+        a, cb, reinterpret_cast<const float4 *>(grad), g, omega, nullptr, a.bw_queue);
+    // pixels with more than kBwHits hits: one warp per CTA, kBwBigHits each
+    k_backward<N, kRay, 1, kBwBigHits><<<(unsigned)backward_resident<N, kRay, 1, kBwBigHits>(), 32,
+                                          sizeof(BwSmem<1, kBwBigHits>), st>>>(
+        a, cb, reinterpret_cast<const float4 *>(grad), g, omega, a.bw_queue, nullptr);
     return cudaGetLastError();
 }
 

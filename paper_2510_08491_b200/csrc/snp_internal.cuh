@@ -102,7 +102,7 @@ __host__ __device__ constexpr int rec_w2(int N) { return kRecUnits + N; }
 // by K2's last block.  No memset node in a project -> bin_sort -> render frame.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
                kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
-               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12, kCntBwdSkipped = 14,
+               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12, kCntBwdSkipped = 14, kCntBwdQueue = 15,
                kNumCounters = 48 };   // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
@@ -179,6 +179,7 @@ struct RenderArgs {
     int32_t sh_degree;
     const float *scales;           // scene semi-axes [n][3] (backward)
     const float *rotations;        // scene quaternions [n][4] (backward)
+    uint32_t *bw_queue;            // [V*H*W] K7's pixels for the big-capacity pass
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;

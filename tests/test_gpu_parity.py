@@ -727,3 +727,51 @@ def test_eager_emission_rule(orc, monkeypatch):
     out_o, fl, _ = orc.render_pixels(scene5, cams5[0], px, py, bg5)
     c = compare(eager["img"][0][py, px], out_o, fl)
     assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
+
+
+def test_backward_long_hit_lists(orc):
+    """K7's big-capacity pass: every pixel of the deep-overlap scene has 600 hits (more
+    than the first pass holds), none is skipped, and sampled W2/b2/centre gradients match
+    central differences of the oracle."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene = _deep_scene(600)
+    cam = synth.look_at((0, 0, 0), (1, 0, 0), 32, 24, 1600.0)
+    rng = np.random.default_rng(91)
+    G = rng.normal(size=(1, 24, 32, 4)).astype(np.float32)
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        opts = snp.make_opts()
+        out = torch.zeros((1, 24, 32, 4), device="cuda")
+        snp.render_views(h, [cam], opts, out)
+        grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in snp.FIELDS}
+        snp.render_backward(h, opts, torch.from_numpy(G).cuda(), grads)
+        torch.cuda.synchronize()
+        dc = snp.get_debug_counters(h, 48)
+        assert dc[15] == 32 * 24 and dc[14] == 0, (dc[14], dc[15])   # all redone, none skipped
+        g = {f: v.cpu().numpy().astype(np.float64) for f, v in grads.items()}
+    finally:
+        snp.destroy(h)
+
+    def loss(sc):
+        img, _, _ = orc.render_frame(sc, cam)
+        return float((img * G[0].astype(np.float64)).sum())
+
+    checks = []
+    for f, idx in (("w2", (100, 3)), ("w2", (433, 0)), ("b2", (7,)), ("b2", (590,)), ("centers", (250, 1)),
+                   ("scales", (321, 0))):
+        arr = getattr(scene, f)
+        base = float(arr[idx])
+        # steps relative to the (tiny) density parameters of this scene
+        step = np.float32(1e-3 * abs(base) + 1e-8) if f in ("w2", "b2") else np.float32(1e-4)
+        vals = []
+        for sgn in (1, -1):
+            arr[idx] = np.float32(base + sgn * step)
+            vals.append(loss(scene))
+        arr[idx] = np.float32(base)
+        hp, hm = float(np.float32(base + step)) - base, base - float(np.float32(base - step))
+        checks.append((f, idx, float(g[f][idx]), (vals[0] - vals[1]) / (hp + hm)))
+    scale = max(abs(c[3]) for c in checks)
+    bad = [c for c in checks if abs(c[2] - c[3]) > 5e-3 * abs(c[3]) + 1e-3 * scale]
+    assert not bad, (bad, checks)
