@@ -187,7 +187,7 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
  * gradient 0.  Call after snp_bin_sort of the same frame, with the same opts as the
  * snp_render it differentiates (background, transmittance_floor, colour_mode); the
  * whole image only (tile_row_begin = 0, tile_row_stride = 1), else SNP_ERR_UNSUPPORTED.
- * Pixels with more than 256 hits are skipped (snp_get_debug_counters slot 14 counts
+ * Pixels with more than 2048 hits are skipped (snp_get_debug_counters slot 14 counts
  * them). */
 snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
                                float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
