@@ -30,8 +30,8 @@ _lib = None
 FLAG_NEAR_TIE = 1
 FLAG_GRAZING = 2
 FLAG_TFLOOR = 4
-TIE_EPS = 1e-6      # DESIGN.md R23
-GRAZE_EPS = 3e-5    # DESIGN.md R23
+TIE_EPS = 1e-7      # DESIGN.md R23 = SURVEY A23: gap < 1e-7 max(1, t_in)
+GRAZE_EPS = 1e-5    # DESIGN.md R23 = SURVEY A23: |1 - q_min| < 1e-5
 T_FLOOR = 1e-4
 
 

@@ -323,12 +323,13 @@ int orc_validate(const orc_scene *sc)
  * OR of ORC_FLAG_*, stats[3*p] = (hit primitives, composited primitives,
  * index of the stopping hit or -1).
  *   near-tie: two consecutive hits in (t_in, id) order, up to and including the
- *             first hit after the stop, with |t_i - t_j| < tie_eps (1 + t_i)
+ *             first hit after the stop, with |t_i - t_j| < tie_eps max(1, t_i)
  *             (both clipped to t_near exactly is an exact tie -> not flagged)
- *   grazing:  a primitive with |1 - qmin| < graze_eps whose closest approach lies
- *             before the stopping depth
+ *   grazing:  a primitive with |1 - qmin| < graze_eps (a hit or a near miss) whose
+ *             closest approach lies before the stopping depth
  *   T-floor:  a transmittance after a composite with |T/floor - 1| < 1e-3
- * (R23: parity is scored on unflagged pixels; flagged counts are reported.)
+ * (R23 / SURVEY A23: tie_eps = 1e-7, graze_eps = 1e-5; parity is scored on
+ * unflagged pixels; flagged counts are reported.)
  */
 /* colour_per_ray = 0: each primitive's colour is its SH at dir = normalize(mu - o), once
  * per primitive and view (R14, the 3DGS convention).  colour_per_ray = 1 (SURVEY §8(f)
@@ -379,7 +380,9 @@ int orc_render_pixels_ex(const orc_scene *sc, const orc_camera *cam, const doubl
                 double tc = w[0] * d[0] + w[1] * d[1] + w[2] * d[2];
                 double ww = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
                 double dist2 = ww - tc * tc;
-                if (dist2 > G[3] * G[3] * (1.0 + 1e-6) + 1e-12 * ww) continue;
+                /* (q_min >= dist2 / smax^2: a primitive outside the widened sphere can
+                 * be neither a hit nor a near miss inside the grazing window) */
+                if (dist2 > G[3] * G[3] * (1.0 + 2.0 * graze_eps + 1e-6) + 1e-12 * ww) continue;
                 if (tc + G[3] < cam->t_near || tc - G[3] > cam->t_far) continue;
                 const orc_prim *P = &prims[i];
                 double ti, to, qmin;
@@ -432,7 +435,7 @@ int orc_render_pixels_ex(const orc_scene *sc, const orc_camera *cam, const doubl
             for (int64_t h = 0; h < last; ++h) {
                 double g = hits[h + 1].t_in - hits[h].t_in;
                 if (hits[h].clipped && hits[h + 1].clipped) continue;
-                if (g < tie_eps * (1.0 + fabs(hits[h].t_in))) fl |= ORC_FLAG_NEAR_TIE;
+                if (g < tie_eps * fmax(1.0, fabs(hits[h].t_in))) fl |= ORC_FLAG_NEAR_TIE;
             }
             double t_stop = (stop >= 0) ? hits[stop].t_in : INFINITY;
             for (int64_t j = 0; j < nnear; ++j)
