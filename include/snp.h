@@ -76,7 +76,8 @@ enum { SNP_COLOUR_PRIMITIVE = 0, SNP_COLOUR_RAY = 1 };
 /* One primitive = 99 fp32 parameters for N = 8 ("99 parameters in total";
  * P:751 "41 parameters from its 8-neuron MLP"). */
 typedef struct {
-    int64_t n;               /* number of primitives, >= 0 (0 renders background) */
+    int64_t n;               /* number of primitives, 0 <= n < 2^24 (0 renders background;
+                                larger n: SNP_ERR_UNSUPPORTED) */
     int32_t n_hidden;        /* N_sigma: 4, 8 (the paper's), 16 or 32; w1 is [n][N][3],
                                 b1 and w2 [n][N] */
     int32_t sh_degree;       /* 0..3; 3 = four bands, 16 coefficients */
@@ -237,9 +238,10 @@ snp_status snp_get_binning(snp_scene s, int32_t *rects, uint32_t *depth_keys, ui
 snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream);
 
 /* Debug readback of the raw device counters [0, n) (n <= 48; synchronises the
- * stream).  Slots >= 16 are only written by instrumented A/B builds (per-warp
- * clock64 accounting); the call clears them after reading.  Not part of the hot
- * path. */
+ * stream).  Slot 13 counts the grazing pairs K5 handed to K6 (FP64 roots, DESIGN.md
+ * R23) since the last readback; slots >= 16 are only written by instrumented A/B
+ * builds (per-warp clock64 accounting).  The call clears slot 13 and slots >= 16
+ * after reading.  Not part of the hot path. */
 snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *cuda_stream);
 
 /* Test hook: caps the per-pixel pending buffer of K5 at `k` entries (1..16) so

@@ -199,7 +199,7 @@ static snp_status check_desc(const snp_scene_desc *d) {
     if (!(d->omega > 0.f) || !std::isfinite(d->omega)) return fail(SNP_ERR_INVALID_ARGUMENT, "omega must be > 0");
     if (d->memory != SNP_MEM_HOST && d->memory != SNP_MEM_DEVICE)
         return fail(SNP_ERR_INVALID_ARGUMENT, "memory must be SNP_MEM_HOST or SNP_MEM_DEVICE");
-    if (d->n >= (int64_t)1 << 31) return fail(SNP_ERR_UNSUPPORTED, "n must be < 2^31");
+    if (d->n > kMaxPrims) return fail(SNP_ERR_UNSUPPORTED, "n must be < 2^24 (K5's pending entries pack the id in 24 bits)");
     const float *src[8] = {d->centers, d->rotations, d->scales, d->w1, d->b1, d->w2, d->b2, d->sh};
     if (d->n > 0)
         for (int k = 0; k < 8; ++k)
@@ -575,6 +575,9 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     if (const char *ee = std::getenv("SNP_EAGER_EMIT")) a.eager_emit = std::atoi(ee) != 0;   // A/B override
     a.sh = s->sh;
     a.sh_degree = s->sh_degree;
+    a.centers = s->centers;
+    a.scales = s->scales;
+    a.rotations = s->rotations;
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
     a.tiles_per_view = s->tiles_x * s->tiles_y;
@@ -637,6 +640,7 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     a.colour_ray = opts->colour_mode == SNP_COLOUR_RAY ? 1 : 0;
     a.sh = s->sh;
     a.sh_degree = s->sh_degree;
+    a.centers = s->centers;
     a.scales = s->scales;
     a.rotations = s->rotations;
     SNP_CUDA(s->bw_queue.ensure((size_t)std::max<int64_t>(1, (int64_t)s->n_views * s->W * s->H)));
@@ -845,6 +849,7 @@ snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *c
     for (int i = 0; i < n; ++i) out[i] = s->h_counters[i];
     // the instrumented slots accumulate until read: clear them for the next measurement
     SNP_CUDA(cudaMemsetAsync(s->counters.p + 16, 0, sizeof(unsigned long long) * (kNumCounters - 16), st));
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGraze, 0, sizeof(unsigned long long), st));
     SNP_CUDA(cudaStreamSynchronize(st));
     return SNP_OK;
 }

@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBat
         const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
         const float4 *recs = a.records + (size_t)view * (size_t)a.n * rec_f4(N);
         const Ray ray = make_ray(cam, x, y);
+        const Prec64 g64{a.centers, a.rotations, a.scales, cam.C[0], cam.C[1], cam.C[2]};
         const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
         // ---- every hit of the tile list
         int cnt = 0;
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBat
                 const float cc = rec[kRecConicRgb].x;
                 const float dx = pxf - c0.x, dy = pyf - c0.y;
                 const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
-                if (q <= 1.0f) hit = exact_hit<N>(rec, ray, th, tl, kap);
+                if (q <= 1.0f) hit = exact_hit<N, kGrazeInline>(rec, ray, th, tl, kap, &g64, id);
             }
             const uint32_t m = __ballot_sync(0xffffffffu, hit);
             const int pos = cnt + __popc(m & lt);

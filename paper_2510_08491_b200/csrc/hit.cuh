@@ -97,10 +97,76 @@ __device__ __forceinline__ float sinc_f(float x) {
     return fabsf(x) < 0.25f ? poly : s;
 }
 
-// Exact hit + kernel for one (ray, record) of N hidden units.  Returns false on a miss.
-template <int N>
+// ---- rare FP64 branch for grazing rays (R23)
+// The chord of a ray that grazes an ellipsoid is hc = sqrt(Q / |a|^2), Q = 1 - |b_perp|^2.
+// In fp32, Q carries an absolute error of a few 1e-7 (the record's fp32 whitening matrix,
+// the rounding of |b_perp|^2), i.e. a relative chord error ~ 2e-7 / Q, which a dense
+// primitive turns into a kappa error ~ I exp(-I) x 2e-7 / Q: 2e-4 at Q = 1e-4, I = 1.
+// Below kGrazeQ the roots are recomputed in FP64 from the primitive's own parameters
+// (mu, q, s), which bounds that error by ~4e-6 at the threshold and
+// ~1e-13 below it; the integral then runs in fp32 on the accurate segment as usual.
+constexpr float kGrazeQ = 4e-3f;
+// K5 (fp32 only): a hit whose kappa may be off by more than kGrazeK0 carries an error
+// exponent e; it is blended in fp32 only while T 2^e <= 2, i.e. while its share of the
+// pixel, T dkappa |c - behind| <= T kGrazeK0 2^e x 2 (colours <= 2), stays <= 6e-5
+constexpr float kGrazeK0 = 1.5e-5f;
+struct Prec64 {
+    const float *centers, *rotations, *scales;   // scene parameters [n][3], [n][4], [n][3]
+    float cx, cy, cz;                             // camera centre
+};
+
+// Segment [t0, t1] of ray C + t d inside the ellipsoid of primitive id, clipped to
+// [t_near, t_far], in FP64; returned relative to tc (the fp32 path's origin of tau).
+// Returns false on a miss.
+__device__ __forceinline__ bool roots_f64(const Prec64 &g, uint32_t id, const Ray &r, float tc, float &tlo_rel,
+                                       float &thi_rel, int &clipped, double &t_in) {
+    const double d[3] = {(double)r.dhx + (double)r.dlx, (double)r.dhy + (double)r.dly,
+                         (double)r.dhz + (double)r.dlz};
+    const float *q4 = g.rotations + 4 * (size_t)id;
+    const float *s3 = g.scales + 3 * (size_t)id;
+    const float *m3 = g.centers + 3 * (size_t)id;
+    double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
+    const double qn = 1.0 / sqrt(w * w + x * x + y * y + z * z);   // (R8: normalised on read)
+    w *= qn; x *= qn; y *= qn; z *= qn;
+    // columns of R(q) (w, x, y, z); Wh = diag(1/s) R^T has them as rows
+    const double R[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                         2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+                         2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
+    const double o[3] = {(double)g.cx - (double)m3[0], (double)g.cy - (double)m3[1], (double)g.cz - (double)m3[2]};
+    double a[3], b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double is = 1.0 / (double)s3[k];
+        a[k] = (R[k] * d[0] + R[3 + k] * d[1] + R[6 + k] * d[2]) * is;
+        b[k] = (R[k] * o[0] + R[3 + k] * o[1] + R[6 + k] * o[2]) * is;
+    }
+    const double A = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+    const double ts = -(a[0] * b[0] + a[1] * b[1] + a[2] * b[2]) / A;
+    const double p0 = b[0] + ts * a[0], p1 = b[1] + ts * a[1], p2 = b[2] + ts * a[2];
+    const double Q = 1.0 - (p0 * p0 + p1 * p1 + p2 * p2);
+    if (!(Q > 0.0)) return false;
+    const double hc = sqrt(Q / A);
+    const double t0 = ts - hc, t1 = ts + hc;
+    const double lo = t0 > (double)r.t_near ? t0 : (double)r.t_near;
+    const double hi = t1 < (double)r.t_far ? t1 : (double)r.t_far;
+    if (!(hi > lo)) return false;
+    clipped = !(t0 > (double)r.t_near);
+    t_in = lo;
+    tlo_rel = (float)(lo - (double)tc);
+    thi_rel = (float)(hi - (double)tc);
+    return true;
+}
+
+// Exact hit + kernel for one (ray, record) of N hidden units, primitive id.  Returns
+// false on a miss.  Grazing rays (|Q| < kGrazeQ): kGraze = kGrazeInline takes the FP64
+// branch in place (K6, K7); kGraze = kGrazeDefer (K5) stays in fp32 and reports, in
+// *graze / *gexp, how far the chord's rounding could move kappa: K5 blends the hit or
+// hands the pixel to K6 (no FP64 code or registers in K5's hot loop).
+enum { kGrazeInline = 0, kGrazeDefer = 1 };
+template <int N, int kGraze>
 __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const Ray &r, float &t_hi, float &t_lo,
-                                          float &kap) {
+                                          float &kap, const Prec64 *g, uint32_t id, bool *graze = nullptr,
+                                          int *gexp = nullptr) {
     const float4 mh = rec[kRecMh];
     const float4 ml = rec[kRecMl];
     const float4 w0 = rec[kRecWh0];
@@ -127,15 +193,26 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
     const float ts = -B * iA;
     const float qx = fmaf(ts, ax, bx), qy = fmaf(ts, ay, by), qz = fmaf(ts, az, bz);
     const float q1 = 1.0f - fmaf(qz, qz, fmaf(qy, qy, qx * qx));
-    if (!(q1 > 0.0f)) return false;
-    const float hq = q1 * iA;
-    const float hc = hq * rsqrtf(hq);   // half chord
-    const float t0 = ts - hc, t1 = ts + hc;
-    const float lo_lim = r.t_near - tc, hi_lim = r.t_far - tc;
-    const bool clipped = !(t0 > lo_lim);
-    const float tlo = clipped ? lo_lim : t0;
-    const float thi = t1 < hi_lim ? t1 : hi_lim;
-    if (!(thi > tlo)) return false;
+    float tlo, thi, hc = 0.f;
+    bool clipped;
+    double t_in64 = 0.0;
+    bool f64 = false;
+    if (kGraze == kGrazeInline && q1 < kGrazeQ && q1 > -kGrazeQ) {   // grazing (or a near miss): FP64 roots
+        int cl = 0;
+        if (!roots_f64(*g, id, r, tc, tlo, thi, cl, t_in64)) return false;
+        clipped = cl != 0;
+        f64 = true;
+    } else {
+        if (!(q1 > 0.0f)) return false;
+        const float hq = q1 * iA;
+        hc = hq * rsqrtf(hq);   // half chord
+        const float t0 = ts - hc, t1 = ts + hc;
+        const float lo_lim = r.t_near - tc, hi_lim = r.t_far - tc;
+        clipped = !(t0 > lo_lim);
+        tlo = clipped ? lo_lim : t0;
+        thi = t1 < hi_lim ? t1 : hi_lim;
+        if (!(thi > tlo)) return false;
+    }
     const float dt = thi - tlo;
     const float tm = 0.5f * (tlo + thi);
     const float hdt = 0.5f * dt;
@@ -156,14 +233,27 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
     }
     const float I = dt * (acc + mh.w);
     kap = 1.0f - __expf(-fmaxf(I, 0.0f));
+    if (kGraze == kGrazeDefer) {
+        // kappa's error from the fp32 chord: |dkappa| <= (1 - kappa) |I| |d dt| / dt with
+        // |d dt| <= 2 |d hc| = hc dQ / Q, dQ <= 3.6e-7 (measured maximum of the fp32 Q over
+        // grazing C3 rays, R23).  Reported as e = ceil(log2(dkappa / kGrazeK0))
+        // clamped to 1..7 when dkappa > kGrazeK0 (0: negligible); the pixel's emission
+        // then decides, knowing the transmittance in front of the hit (render.cu)
+        const float err = q1 < kGrazeQ ? (1.0f - kap) * fabsf(I) * hc * 3.6e-7f * rcp_fast(q1 * dt) : 0.0f;
+        *graze = err > kGrazeK0;
+        if (*graze) *gexp = min(7, max(1, (int)ceilf(__log2f(err * (1.0f / kGrazeK0)))));
+    }
     if (clipped) {
         t_hi = r.t_near;
         t_lo = 0.f;
+    } else if (f64) {
+        t_hi = (float)t_in64;
+        t_lo = (float)(t_in64 - (double)t_hi);
     } else {  // TwoSum(tc, t0): t_in = t_hi + t_lo exactly
-        const float s = tc + t0;
+        const float s = tc + tlo;
         const float bb = s - tc;
         t_hi = s;
-        t_lo = (tc - (s - bb)) + (t0 - bb);
+        t_lo = (tc - (s - bb)) + (tlo - bb);
     }
     return true;
 }

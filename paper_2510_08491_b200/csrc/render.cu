@@ -73,9 +73,10 @@ struct __align__(16) Smem {
     uint8_t qj[kWarps][kQueue];               // per-warp compaction queue of candidate pairs
     uint8_t ql[kWarps][kQueue];               //   (record slot j, owner lane), a ring from qhead
     float p_thi[kPend][kWarps * 32];          // pending hits, one column per pixel, kept sorted by
-                                              // (t_in, id) in a ring starting at the head: t_in
-                                              // (fp32: its 6e-8 rounding is far below the 1e-6
-                                              // near-tie flag of R23), kappa, primitive id
+                                              // (t_in, id) in a ring starting at the head: t_in's
+                                              // high part, kappa, and tin_code(t_in) << 24 | id, so
+                                              // that (p_thi, p_id) orders by the compensated t_in
+                                              // (hi + lo) then by id
     float p_kap[kPend][kWarps * 32];
     uint32_t p_id[kPend][kWarps * 32];
     uint32_t p_in[kWarps * 32];               // per owner pixel: lanes holding a hit for it this round
@@ -114,6 +115,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// t_in = t_hi + t_lo (TwoSum, |t_lo| <= ulp(t_hi)/2) as a 5-bit code of t_lo in units
+// of ulp(t_hi)/32, monotone in t_lo: among hits with equal t_hi, (code, id) orders by
+// t_in up to 2^-5 ulp (~4e-9 relative), far inside the 1e-7 near-tie window of R23,
+// and exact ties (both clipped to t_near: t_lo = 0) fall back to the id (R11).
+// Pending entry word: code << 27 | grazing exponent << 24 | primitive id (kMaxPrims).
+__device__ __forceinline__ uint32_t tin_code(float th, float tl) {
+    const int E = max((int)((__float_as_uint(th) >> 23) & 0xffu), 32);
+    const float sc = __uint_as_float((uint32_t)(282 - E) << 23);   // 2^(155 - E) = 32 / ulp(t_hi)
+    return (uint32_t)fminf(fmaxf(fmaf(tl, sc, 16.0f), 0.0f), 31.0f);
+}
+constexpr uint32_t kIdMask = (1u << 24) - 1u;   // kMaxPrims
+
 // The owner lane's view of its pixel's pending ring (the entries live in shared
 // memory, column tid; count, head and the largest entry are kept in registers).
 struct Pending {
@@ -144,7 +157,16 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
         const float t = sm.p_thi[h][tid];
         if (!(t < L)) break;
         const float kap = sm.p_kap[h][tid];
-        const uint32_t pid = sm.p_id[h][tid];
+        const uint32_t word = sm.p_id[h][tid];
+        const uint32_t pid = word & kIdMask;
+        const int gexp = (int)((word >> 24) & 7u);
+        // a grazing hit whose fp32 kappa could move this pixel by more than 6e-5 (hit.cuh,
+        // kGrazeK0): the pixel goes to K6, which evaluates it with FP64 roots
+        if (gexp && (gexp == 7 || ps.T * (float)(1 << gexp) > 2.0f)) {
+            ps.overflow = true;
+            ps.done = true;
+            break;
+        }
         const float4 rgb = hit_rgb<kRay>(recs + (size_t)pid * rec_f4(N), a.sh, a.sh_degree, pid, ray);
         const float w = ps.T * kap;
         ps.cr = fmaf(w, rgb.y, ps.cr);
@@ -468,10 +490,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 ro.dlz = __shfl_sync(0xffffffffu, ray.dlz, owner);
                 ro.t_near = cam->t_near;
                 ro.t_far = cam->t_far;
-                bool hit = false;
+                bool hit = false, graze = false;
+                int gexp = 0;
                 float th = 0.f, tl = 0.f, kap = 0.f;
-                if (valid) hit = exact_hit<N>(&sm.rec[slot][j][0], ro, th, tl, kap);
+                const uint32_t idj = sm.id[slot][j];
+                if (valid)
+                    hit = exact_hit<N, kGrazeDefer>(&sm.rec[slot][j][0], ro, th, tl, kap, nullptr, idj, &graze, &gexp);
                 n_hit += hit;
+                if (hit && graze) atomicAdd(a.counters + kCntGraze, 1ull);   // rare
 #ifdef SNP_INSTRUMENT
                 long long _i0 = clock64();
 #endif
@@ -479,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 // own sorted ring: each hitting lane adds its bit to the owner's mask; the
                 // owner then fetches its hits one per step by shuffle (no cross-lane
                 // writes to a ring, no dependent shared-memory round trips per step)
-                const uint32_t idn = hit ? sm.id[slot][j] : 0u;
+                const uint32_t idn = hit ? (tin_code(th, tl) << 27) | ((uint32_t)gexp << 24) | idj : 0u;
                 if (hit) atomicOr(&sm.p_in[wid * 32 + owner], 1u << lane);
                 __syncwarp();
                 uint32_t inc = sm.p_in[tid];
@@ -639,13 +665,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
 
 template <int N>
 __device__ __forceinline__ bool fb_hit(const float4 *rec, const Ray &ray, float pxf, float pyf, float &th,
-                                       float &tl, float &kap) {
+                                       float &tl, float &kap, const Prec64 &g64, uint32_t id) {
     const float4 c0 = rec[kRecConic];
     const float cc = rec[kRecConicRgb].x;
     const float dx = pxf - c0.x, dy = pyf - c0.y;
     const float q = fmaf(cc * dy, dy, dx * fmaf(c0.w, dy, c0.z * dx));
     if (!(q <= 1.0f)) return false;
-    return exact_hit<N>(rec, ray, th, tl, kap);
+    return exact_hit<N, kGrazeInline>(rec, ray, th, tl, kap, &g64, id);
 }
 
 // K6: exact per-pixel fallback, one CTA per overflowed pixel.  Phase A: the
@@ -734,6 +760,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
         const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
         const float4 *recs = a.records + (size_t)view * (size_t)a.n * rec_f4(N);
         const Ray ray = make_ray(cam, x, y);
+        const Prec64 g64{a.centers, a.rotations, a.scales, cam.C[0], cam.C[1], cam.C[2]};
         const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
         if (tid == 0) sm.count = 0;
         __syncthreads();
@@ -765,7 +792,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
 #pragma unroll
             for (int u = 0; u < kFbIlp; ++u) {
                 float th, tl, kap;
-                if (cand[u] && exact_hit<N>(recs + (size_t)ids[u] * rec_f4(N), ray, th, tl, kap)) {
+                if (cand[u] && exact_hit<N, kGrazeInline>(recs + (size_t)ids[u] * rec_f4(N), ray, th, tl, kap, &g64, ids[u])) {
                     const int pos = atomicAdd(&sm.count, 1);
                     if (pos < kFbHits) {
                         sm.t[pos] = th; sm.l[pos] = tl; sm.k[pos] = kap; sm.id[pos] = ids[u];
@@ -903,7 +930,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
                 for (uint32_t e = beg + tid; e < end; e += kFbThreads) {
                     const uint32_t id = a.vals[e];
                     float th, tl, kap;
-                    if (!fb_hit<N>(recs + (size_t)id * rec_f4(N), ray, pxf, pyf, th, tl, kap)) continue;
+                    if (!fb_hit<N>(recs + (size_t)id * rec_f4(N), ray, pxf, pyf, th, tl, kap, g64, id)) continue;
                     if (!first && !before(lh, ll, lid, th, tl, id)) continue;
                     if (before(th, tl, id, bh, bl, bid)) { bh = th; bl = tl; bid = id; bk = kap; }
                 }
@@ -996,40 +1023,42 @@ __global__ void __launch_bounds__(1024) k_tile_order(RenderArgs a, CamBatch cb, 
 }  // namespace
 
 namespace {
+constexpr int kMaxDevices = 64;
 template <int N, bool kRay, bool kEager>
 int render_grid_n(int tiles) {
-    static int resident = 0;   // persistent grid: every CTA that fits, all SMs
-    if (!resident) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+    // persistent grid: every CTA that fits, all SMs.  Cached per device (the shared-memory
+    // attribute and the occupancy are per-device properties; a process may drive several)
+    static int resident[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &res = resident[dev < kMaxDevices ? dev : 0];
+    if (!res) {
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_render<N, kRay, kEager>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(Smem<N>));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N, kRay, kEager>, kThreads, sizeof(Smem<N>));
-        resident = std::max(1, sms) * std::max(1, per_sm);
+        res = std::max(1, sms) * std::max(1, per_sm);
     }
-    return std::min(tiles, resident);
+    return std::min(tiles, res);
 }
 
 template <int N, bool kRay, bool kEager>
 cudaError_t launch_render_n(const RenderArgs &a, const CamBatch &cams, int tiles, cudaStream_t st) {
-    static bool attr_set = false;
     const int smem = (int)sizeof(Smem<N>);
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay, kEager>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    k_render<N, kRay, kEager><<<render_grid_n<N, kRay, kEager>(tiles), kThreads, smem, st>>>(a, cams);
+    const int grid = render_grid_n<N, kRay, kEager>(tiles);   // (sets the attribute on this device)
+    k_render<N, kRay, kEager><<<grid, kThreads, smem, st>>>(a, cams);
     return cudaGetLastError();
 }
 
 template <int N, bool kRay>
 cudaError_t launch_fallback_n(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
-    static int resident = 0;   // every CTA that fits, all SMs (the queue loop strides by the grid)
+    static int res[kMaxDevices] = {};   // every CTA that fits, all SMs (the queue loop strides by the grid)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &resident = res[dev < kMaxDevices ? dev : 0];
     if (!resident) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback<N, kRay>, kFbThreads, 0);
         resident = std::max(1, sms) * std::max(1, per_sm);

@@ -46,6 +46,9 @@ constexpr int kHidden = 8;                // N_sigma = 8, the paper's width (P:3
 // instantiated for these; N = 8 is the measured configuration.
 __host__ __device__ constexpr bool hidden_supported(int N) { return N == 4 || N == 8 || N == 16 || N == 32; }
 constexpr int kCamsPerLaunch = 32;        // cameras passed by value per launch
+// Largest scene: K5's pending entries carry the primitive id in 24 bits beside an
+// 8-bit code of t_in's low part (render.cu, tin_code).
+constexpr int64_t kMaxPrims = (1 << 24) - 1;
 // float4 per render record: 6 (conic, colour, centre, whitening) + N units + N/4 for W2
 // = 11 / 16 / 26 / 46 for N = 4 / 8 / 16 / 32 (256 B at N = 8)
 __host__ __device__ constexpr int rec_f4(int N) { return 6 + N + N / 4; }
@@ -102,7 +105,7 @@ __host__ __device__ constexpr int rec_w2(int N) { return kRecUnits + N; }
 // by K2's last block.  No memset node in a project -> bin_sort -> render frame.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
                kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
-               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12, kCntBwdSkipped = 14, kCntBwdQueue = 15,
+               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12, kCntGraze = 13, kCntBwdSkipped = 14, kCntBwdQueue = 15,
                kNumCounters = 48 };   // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
@@ -177,8 +180,9 @@ struct RenderArgs {
     int32_t eager_emit;            // K5 blends after every exact round (not only near-full lists)
     const float *sh;               // scene SH coefficients [n][16][3] (per-ray colour)
     int32_t sh_degree;
-    const float *scales;           // scene semi-axes [n][3] (backward)
-    const float *rotations;        // scene quaternions [n][4] (backward)
+    const float *centers;          // scene centres [n][3] (FP64 grazing branch)
+    const float *scales;           // scene semi-axes [n][3] (FP64 grazing branch, backward)
+    const float *rotations;        // scene quaternions [n][4] (FP64 grazing branch, backward)
     uint32_t *bw_queue;            // [V*H*W] K7's pixels for the big-capacity pass
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
