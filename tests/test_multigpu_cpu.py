@@ -124,3 +124,22 @@ def test_two_rank_gradient_allreduce():
     for rank in (0, 1):
         for k, (f, v) in enumerate(res[rank][1].items()):
             assert v == pytest.approx(1.5 * (k + 1)), (rank, f, v)   # mean of 1x and 2x
+
+
+def test_bench_launcher_two_ranks_gloo():
+    """bench.py --gpus 2 re-launches itself under torch.distributed.run (2 ranks); the C4
+    view-sharding and X2 protocol (multigpu.ShardedFrames, double-buffered gather to rank 0)
+    runs over gloo with a deterministic stand-in for the GPU render, and rank 0 finds the
+    gathered 64-view batch equal to the single-process one."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--selftest-cpu",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    assert lines[0]["n_gpus"] == 2 and lines[0]["bit_identical_to_single_gpu"] is True
