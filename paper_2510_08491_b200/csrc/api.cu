@@ -558,15 +558,15 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     }
     const int64_t fb_cap = std::min<int64_t>((int64_t)s->n_views * s->W * s->H, (int64_t)1 << 22);
     if (s->fallback_capacity < fb_cap) {
-        SNP_CUDA(s->fallback.ensure((size_t)fb_cap));
-        SNP_CUDA(cudaMemsetAsync(s->fallback.p, 0, sizeof(unsigned long long) * (size_t)fb_cap, st));
+        SNP_CUDA(s->fallback.ensure((size_t)(2 * fb_cap)));
+        SNP_CUDA(cudaMemsetAsync(s->fallback.p, 0, sizeof(unsigned long long) * (size_t)(2 * fb_cap), st));
         s->fallback_capacity = fb_cap;
     }
     // stats, fallback queue, tile queue: K4 cleared them for the first render of this
     // binning; a further render clears them with one memset (contiguous counters)
     if (s->render_dirty)
         SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
-                                 sizeof(unsigned long long) * (kCntK5Done - kCntTested + 1), st));
+                                 sizeof(unsigned long long) * (kCntRenderLast - kCntTested + 1), st));
     s->render_dirty = true;
     RenderArgs a{};
     a.n_hidden = s->n_hidden;

@@ -206,7 +206,7 @@ __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *co
     pdl_prologue();
     // the first render of this binning needs clean render counters, the next frame's K2
     // clean block states and digit histograms (no memset node)
-    if (blockIdx.x == 0 && threadIdx.x <= kCntK5Done - kCntTested)
+    if (blockIdx.x == 0 && threadIdx.x <= kCntRenderLast - kCntTested)
         const_cast<unsigned long long *>(counters)[kCntTested + threadIdx.x] = 0ull;
     if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<unsigned long long *>(counters)[kCntVisibleAcc] = 0ull;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < dup_blocks; j += (int64_t)gridDim.x * blockDim.x)

@@ -236,12 +236,18 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
     if (kGraze == kGrazeDefer) {
         // kappa's error from the fp32 chord: |dkappa| <= (1 - kappa) |I| |d dt| / dt with
         // |d dt| <= 2 |d hc| = hc dQ / Q, dQ <= 3.6e-7 (measured maximum of the fp32 Q over
-        // grazing C3 rays, R23).  Reported as e = ceil(log2(dkappa / kGrazeK0))
-        // clamped to 1..7 when dkappa > kGrazeK0 (0: negligible); the pixel's emission
-        // then decides, knowing the transmittance in front of the hit (render.cu)
-        const float err = q1 < kGrazeQ ? (1.0f - kap) * fabsf(I) * hc * 3.6e-7f * rcp_fast(q1 * dt) : 0.0f;
-        *graze = err > kGrazeK0;
-        if (*graze) *gexp = min(7, max(1, (int)ceilf(__log2f(err * (1.0f / kGrazeK0)))));
+        // grazing C3 rays, R23).  Reported as an exponent e >= ceil(log2(dkappa /
+        // kGrazeK0)) (from the float exponents: no division), clamped to 1..7, when dkappa may
+        // exceed kGrazeK0 (0: negligible); the pixel's emission then decides, knowing the
+        // transmittance in front of the hit (render.cu)
+        *graze = false;
+        if (q1 < kGrazeQ) {   // (rare)
+            const float num = (1.0f - kap) * fabsf(I) * hc * (3.6e-7f / kGrazeK0);
+            const float den = q1 * dt;
+            const int e = (int)(__float_as_uint(num) >> 23) - (int)(__float_as_uint(den) >> 23) + 1;
+            *graze = e > 0 && num > 0.0f;
+            *gexp = min(7, max(1, e));
+        }
     }
     if (clipped) {
         t_hi = r.t_near;

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     const long long ins_start = clock64();
 #endif
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
-    uint32_t n_cand = 0, n_hit = 0, n_comp = 0, n_ovf = 0;
+    uint32_t n_cand = 0, n_hit = 0, n_comp = 0, n_ovf = 0, n_graze = 0;
     unsigned long long n_tested = 0;
     // per-tile state
     int cur_seq = -1;
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 if (valid)
                     hit = exact_hit<N, kGrazeDefer>(&sm.rec[slot][j][0], ro, th, tl, kap, nullptr, idj, &graze, &gexp);
                 n_hit += hit;
-                if (hit && graze) atomicAdd(a.counters + kCntGraze, 1ull);   // rare
+                n_graze += hit && graze;
 #ifdef SNP_INSTRUMENT
                 long long _i0 = clock64();
 #endif
@@ -660,6 +660,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
         const uint32_t s = __reduce_add_sync(0xffffffffu, v[c]);   // per-warp totals fit 32 bits
         if (lane == 0 && s) atomicAdd(a.counters + kCntTested + c, (unsigned long long)s);
     }
+    {
+        const uint32_t s = __reduce_add_sync(0xffffffffu, n_graze);
+        if (lane == 0 && s) atomicAdd(a.counters + kCntGraze, (unsigned long long)s);
+    }
     warp_exit();
 }
 
@@ -712,46 +716,18 @@ __device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long 
 // exited and no entry is left.  overlap = false: K5 has completed; CTAs stride over the
 // queue and take the entries of this batch's views.
 template <int N, bool kRay>
-__global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb, int overlap) {
-    if (!overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
+__global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch cb) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ FbSmem sm;
-    __shared__ unsigned long long s_entry;
-    __shared__ int64_t s_q;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    int64_t nq = overlap ? 0 : (int64_t)a.counters[kCntFallbackQueue];
+    // the pixels K6w could not hold (second half of the queue buffer)
+    const unsigned long long *big = a.fallback + a.fallback_capacity;
+    int64_t nq = (int64_t)a.counters[kCntBigQueue];
     if (nq > a.fallback_capacity) nq = a.fallback_capacity;
-    for (int64_t it = blockIdx.x;; it += gridDim.x) {
-        if (tid == 0) {
-            unsigned long long v = 0;
-            int64_t q = it;
-            if (overlap) {
-                q = (int64_t)atomicAdd(a.counters + kCntFallbackClaim, 1ull);
-                while (q < a.fallback_capacity) {
-                    v = ld_vol64(a.fallback + q);
-                    if (v) break;
-                    if (ld_vol64(a.counters + kCntK5Done) == (unsigned long long)a.k5_grid) {
-                        v = ld_vol64(a.fallback + q);   // (pushed before K5's exit signal)
-                        break;
-                    }
-                    __nanosleep(200);
-                }
-            } else if (q < nq) {
-                v = a.fallback[q];
-            } else {
-                v = ~0ull;   // end
-            }
-            s_entry = v;
-            s_q = q;
-        }
-        __syncthreads();
-        const unsigned long long ent = s_entry;
-        const int64_t qi = s_q;
-        __syncthreads();
-        if (overlap ? ent == 0 : ent == ~0ull) break;
-        if (!(ent >> 63)) continue;
+    for (int64_t qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+        const unsigned long long ent = big[qi];
         const int64_t view = (int64_t)((ent >> 32) & 0x7fffffffull);
         if (view < cb.view0 || view >= cb.view0 + cb.nv) continue;
-        if (tid == 0) a.fallback[qi] = 0ull;   // consumed: the queue is all zero between renders
         const DevCam &cam = cb.cams[view - cb.view0];
         const uint32_t pix = (uint32_t)ent;
         const int x = (int)(pix % (uint32_t)cam.W), y = (int)(pix / (uint32_t)cam.W);
@@ -968,6 +944,155 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(RenderArgs a, CamBatch 
         }
         __syncthreads();
     }
+}
+
+// K6w: exact per-pixel fallback, one warp per overflowed pixel (the pixels K5 queues:
+// pending overflow or a grazing hit, R23).  Small enough (one warp, 7 KB of
+// shared memory) to run on the SMs beside K5's two CTAs: launched as K5's programmatic
+// dependent, its CTAs are resident while K5 runs and take pixels as K5 queues them, so
+// the fallback work overlaps K5 instead of following it.  Per pixel: every hit of the
+// tile list (conic pre-test, exact hit with the FP64 grazing branch), (t_in, id) order
+// by rank (R11), transmittance by a chunked warp product-scan with the stop rule
+// (Eq. 4, R13), colours summed over the warp.  A pixel with more than kFwHits
+// hits goes to the block-wide K6 (k_fallback) that runs after.
+constexpr int kFwHits = 384;
+struct FwSmem {
+    float th[kFwHits], tl[kFwHits], kap[kFwHits];
+    uint32_t id[kFwHits];
+    uint16_t ord[kFwHits];
+};
+
+template <int N, bool kRay>
+__global__ void __launch_bounds__(32) k_fallback_warp(RenderArgs a, CamBatch cb, int overlap) {
+    if (!overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ FwSmem sm;
+    const int lane = threadIdx.x;
+    const uint32_t lt = (1u << lane) - 1u;
+    int64_t nq = overlap ? 0 : (int64_t)a.counters[kCntFallbackQueue];
+    if (nq > a.fallback_capacity) nq = a.fallback_capacity;
+    for (int64_t it = blockIdx.x;; it += gridDim.x) {
+        unsigned long long ent = 0;
+        int64_t qi = it;
+        if (lane == 0) {
+            if (overlap) {
+                qi = (int64_t)atomicAdd(a.counters + kCntFallbackClaim, 1ull);
+                while (qi < a.fallback_capacity) {
+                    ent = ld_vol64(a.fallback + qi);
+                    if (ent) break;
+                    if (ld_vol64(a.counters + kCntK5Done) == (unsigned long long)a.k5_grid) {
+                        ent = ld_vol64(a.fallback + qi);   // (pushed before K5's exit signal)
+                        break;
+                    }
+                    __nanosleep(500);
+                }
+            } else {
+                ent = qi < nq ? a.fallback[qi] : ~0ull;
+            }
+        }
+        ent = __shfl_sync(0xffffffffu, ent, 0);
+        qi = __shfl_sync(0xffffffffu, qi, 0);
+        if (overlap ? ent == 0 : ent == ~0ull) break;
+        if (!(ent >> 63)) continue;
+        const int64_t view = (int64_t)((ent >> 32) & 0x7fffffffull);
+        if (view < cb.view0 || view >= cb.view0 + cb.nv) continue;
+        if (lane == 0) a.fallback[qi] = 0ull;   // consumed: the queue is all zero between renders
+        const DevCam &cam = cb.cams[view - cb.view0];
+        const uint32_t pix = (uint32_t)ent;
+        const int x = (int)(pix % (uint32_t)cam.W), y = (int)(pix / (uint32_t)cam.W);
+        const int tile = (y / kTile) * a.tiles_x + (x / kTile);
+        const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
+        const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
+        const float4 *recs = a.records + (size_t)view * (size_t)a.n * rec_f4(N);
+        const Ray ray = make_ray(cam, x, y);
+        const Prec64 g64{a.centers, a.rotations, a.scales, cam.C[0], cam.C[1], cam.C[2]};
+        const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
+        // ---- every hit of the tile list
+        int cnt = 0;
+        for (uint32_t e0 = beg; e0 < end; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            bool hit = false;
+            float th = 0.f, tl = 0.f, kap = 0.f;
+            uint32_t id = 0;
+            if (e < end) {
+                id = a.vals[e];
+                hit = fb_hit<N>(recs + (size_t)id * rec_f4(N), ray, pxf, pyf, th, tl, kap, g64, id);
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, hit);
+            const int pos = cnt + __popc(m & lt);
+            if (hit && pos < kFwHits) {
+                sm.th[pos] = th;
+                sm.tl[pos] = tl;
+                sm.kap[pos] = kap;
+                sm.id[pos] = id;
+            }
+            cnt += __popc(m);
+        }
+        if (cnt > kFwHits) {   // to the block-wide K6
+            if (lane == 0) {
+                const unsigned long long b = atomicAdd(a.counters + kCntBigQueue, 1ull);
+                if ((int64_t)b < a.fallback_capacity) a.fallback[a.fallback_capacity + b] = ent;
+            }
+            continue;
+        }
+        __syncwarp();
+        // ---- (t_in, id) order by rank
+        for (int i = lane; i < cnt; i += 32) {
+            const float ti = sm.th[i], li = sm.tl[i];
+            const uint32_t ii = sm.id[i];
+            int rnk = 0;
+            for (int j = 0; j < cnt; ++j) rnk += before(sm.th[j], sm.tl[j], sm.id[j], ti, li, ii) ? 1 : 0;
+            sm.ord[rnk] = (uint16_t)i;
+        }
+        __syncwarp();
+        // ---- composite: chunked warp product-scan of (1 - kappa), stop after the first hit
+        // that takes T below the floor
+        float carryT = 1.f, cr = 0.f, cg = 0.f, cbl = 0.f;
+        int ncomp = cnt;
+        for (int k0 = 0; k0 < cnt; k0 += 32) {
+            const int k = k0 + lane;
+            const bool valid = k < cnt;
+            const int h = valid ? (int)sm.ord[k] : 0;
+            const float kap = valid ? sm.kap[h] : 0.f;
+            float incl = 1.0f - kap;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float yv = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl *= yv;
+            }
+            float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 1.0f;
+            const float Tb = carryT * excl, Ta = carryT * incl;
+            const uint32_t sb = __ballot_sync(0xffffffffu, valid && Ta < a.t_floor);
+            const int stop = sb ? __ffs(sb) - 1 : 32;   // last composited lane of this chunk
+            if (valid && lane <= stop) {
+                const uint32_t id = sm.id[h];
+                const float4 c = hit_rgb<kRay>(recs + (size_t)id * rec_f4(N), a.sh, a.sh_degree, id, ray);
+                const float w = Tb * kap;
+                cr = fmaf(w, c.y, cr);
+                cg = fmaf(w, c.z, cg);
+                cbl = fmaf(w, c.w, cbl);
+            }
+            if (sb) {
+                carryT = __shfl_sync(0xffffffffu, Ta, stop);
+                ncomp = k0 + stop + 1;
+                break;
+            }
+            carryT = __shfl_sync(0xffffffffu, Ta, 31);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cr += __shfl_xor_sync(0xffffffffu, cr, o);
+            cg += __shfl_xor_sync(0xffffffffu, cg, o);
+            cbl += __shfl_xor_sync(0xffffffffu, cbl, o);
+        }
+        if (lane == 0) {
+            reinterpret_cast<float4 *>(a.out)[((size_t)view * cam.H + y) * cam.W + x] =
+                make_float4(fmaf(carryT, a.bg[0], cr), fmaf(carryT, a.bg[1], cg), fmaf(carryT, a.bg[2], cbl),
+                            1.f - carryT);
+            atomicAdd(a.counters + kCntComposited, (unsigned long long)ncomp);
+        }
+        __syncwarp();
+    }
     // (the grid completes only after K5: later work in the stream sees both)
     if (overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -1053,19 +1178,25 @@ cudaError_t launch_render_n(const RenderArgs &a, const CamBatch &cams, int tiles
 
 template <int N, bool kRay>
 cudaError_t launch_fallback_n(const RenderArgs &a, const CamBatch *cams, int n_batches, cudaStream_t st) {
-    static int res[kMaxDevices] = {};   // every CTA that fits, all SMs (the queue loop strides by the grid)
+    // K6w: 2 one-warp CTAs per SM (they fit beside K5's two CTAs); K6: every CTA that fits
+    static int fw[kMaxDevices] = {}, fb[kMaxDevices] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    int &resident = res[dev < kMaxDevices ? dev : 0];
-    if (!resident) {
+    const int d = dev < kMaxDevices ? dev : 0;
+    if (!fw[d]) {
         int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback<N, kRay>, kFbThreads, 0);
-        resident = std::max(1, sms) * std::max(1, per_sm);
+        fb[d] = std::max(1, sms) * std::max(1, per_sm);
+        fw[d] = 2 * std::max(1, sms);
     }
     const int overlap = n_batches == 1 ? 1 : 0;
     for (int i = 0; i < n_batches; ++i) {
-        cudaError_t e = launch_hi(k_fallback<N, kRay>, dim3(resident), dim3(kFbThreads), 0, st, a, cams[i], overlap);
+        cudaError_t e = launch_hi(k_fallback_warp<N, kRay>, dim3(fw[d]), dim3(32), 0, st, a, cams[i], overlap);
+        if (e != cudaSuccess) return e;
+    }
+    for (int i = 0; i < n_batches; ++i) {
+        cudaError_t e = launch_hi(k_fallback<N, kRay>, dim3(fb[d]), dim3(kFbThreads), 0, st, a, cams[i]);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();

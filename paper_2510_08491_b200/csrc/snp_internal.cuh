@@ -99,14 +99,16 @@ enum RecordSlot { kRecConic = 0, kRecConicRgb = 1, kRecMh = 2, kRecMl = 3, kRecW
 __host__ __device__ constexpr int rec_w2(int N) { return kRecUnits + N; }
 
 // Device-side counters (one 64-bit slot each), see snp_stats.
-// The render counters kCntTested..kCntK5Done are contiguous: K4 clears them for the
+// The render counters kCntTested..kCntRenderLast are contiguous: K4 clears them for the
 // first render after a binning (a further render of the same binning clears them with
 // one memset).  kCntVisibleAcc is K1a's accumulator, moved to kCntVisible (and cleared)
 // by K2's last block.  No memset node in a project -> bin_sort -> render frame.
 enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3, kCntCandidate = 4, kCntHit = 5,
                kCntComposited = 6, kCntOverflow = 7, kCntFallbackQueue = 8, kCntTileQueue = 9,
-               kCntFallbackClaim = 10, kCntK5Done = 11, kCntVisibleAcc = 12, kCntGraze = 13, kCntBwdSkipped = 14, kCntBwdQueue = 15,
-               kNumCounters = 48 };   // 16..47: instrumented (A/B) builds only, cleared by the debug readback
+               kCntFallbackClaim = 10, kCntK5Done = 11, kCntBigQueue = 12, kCntRenderLast = kCntBigQueue,
+               kCntVisibleAcc = 13, kCntBwdSkipped = 14, kCntBwdQueue = 15,
+               kCntGraze = 48,          // cumulative until the debug readback
+               kNumCounters = 56 };     // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
     int64_t n;
@@ -197,8 +199,10 @@ struct RenderArgs {
     int32_t pending_limit;
     int32_t debug_flags;           // SNP_DEBUG env bits (1: no sub-tile culling); 0 in production
     float *out;                    // [V][H][W][4]
-    unsigned long long *fallback;  // [capacity] overflowed pixels: 1 << 63 | view << 32 | pixel; 0 = empty
-                                   // (K6 clears every entry it consumes: all zero between renders)
+    unsigned long long *fallback;  // [2 x capacity] overflowed pixels: 1 << 63 | view << 32 | pixel; 0 = empty
+                                   // (K6w clears every entry it consumes: all zero between renders); the
+                                   // second half lists the pixels with more hits than K6w holds (count in
+                                   // counters[kCntBigQueue]) for the block-wide K6
     int64_t fallback_capacity;
     const uint32_t *tile_order;    // K5 claims tiles in this order (heaviest list first)
     int32_t k5_grid;               // K5's CTA count (K6 overlapping K5 waits for that many exits)

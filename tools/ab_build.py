@@ -22,4 +22,6 @@ for src in B.SOURCES:
 lib = os.path.join(ROOT, "abtest", f"libsnp_{name}.so")
 subprocess.run([B.nvcc()] + B.ARCH + ["-shared", "-o", lib] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"],
                check=True)
+import shutil
+shutil.rmtree(out_dir)   # (objects are not needed once linked; keeps the gpurun snapshot small)
 print(lib)
