@@ -237,11 +237,12 @@ snp_status snp_get_binning(snp_scene s, int32_t *rects, uint32_t *depth_keys, ui
 /* Counters of the last project/bin_sort/render (synchronises the stream). */
 snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream);
 
-/* Debug readback of the raw device counters [0, n) (n <= 48; synchronises the
- * stream).  Slot 13 counts the grazing pairs K5 handed to K6 (FP64 roots, DESIGN.md
- * R23) since the last readback; slots >= 16 are only written by instrumented A/B
- * builds (per-warp clock64 accounting).  The call clears slot 13 and slots >= 16
- * after reading.  Not part of the hot path. */
+/* Debug readback of the raw device counters [0, n) (n <= 56; synchronises the
+ * stream).  Slot 12 is the number of pixels the last render handed to the block-wide
+ * K6 (more hits than K6w holds); slot 48 counts the grazing hits K5 evaluated with a
+ * kappa error bound above 1.5e-5 (R23) since the last readback; slots 16..47
+ * are only written by instrumented A/B builds (per-warp clock64 accounting).  The
+ * call clears slots >= 16 after reading.  Not part of the hot path. */
 snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *cuda_stream);
 
 /* Test hook: caps the per-pixel pending buffer of K5 at `k` entries (1..16) so

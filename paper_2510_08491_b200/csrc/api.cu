@@ -849,7 +849,6 @@ snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *c
     for (int i = 0; i < n; ++i) out[i] = s->h_counters[i];
     // the instrumented slots accumulate until read: clear them for the next measurement
     SNP_CUDA(cudaMemsetAsync(s->counters.p + 16, 0, sizeof(unsigned long long) * (kNumCounters - 16), st));
-    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGraze, 0, sizeof(unsigned long long), st));
     SNP_CUDA(cudaStreamSynchronize(st));
     return SNP_OK;
 }

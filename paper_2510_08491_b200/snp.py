@@ -292,7 +292,7 @@ def set_pending_limit(h, k):
     _check(lib().snp_set_pending_limit(h, int(k)))
 
 
-def get_debug_counters(h, n=48, stream=None):
+def get_debug_counters(h, n=56, stream=None):
     out = np.zeros(n, np.uint64)
     _check(lib().snp_get_debug_counters(h, out.ctypes.data, int(n), _stream(stream)))
     return out
