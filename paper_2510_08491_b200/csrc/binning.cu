@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
         const uint64_t view = (uint64_t)(o / a.n);
         const uint32_t prim = (uint32_t)(o - (int64_t)view * a.n);
         const uint64_t tile = (uint64_t)row * (uint64_t)a.tiles_x + (uint64_t)(s_x0[lo] + c);
+        SNP_CHECK(lo >= i0 && lo < i0 + 32 * kScanItems && row < a.tiles_y && s_x0[lo] + c < a.tiles_x);
         const uint64_t key = (view << view_shift) | (tile << kDepthBits) | (uint64_t)s_dep[lo];
         const uint64_t g = gbase + e;
         if (g < (uint64_t)a.capacity) {
@@ -219,6 +220,7 @@ __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *co
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t vt = keys[i] >> kDepthBits;
         const uint64_t slot = (vt >> tile_bits) * (uint64_t)tiles + (vt & tmask);
+        SNP_CHECK((vt & tmask) < (uint64_t)tiles);
         if (i == 0 || (keys[i - 1] >> kDepthBits) != vt) ranges[2 * slot] = (uint32_t)i;
         if (i == n - 1 || (keys[i + 1] >> kDepthBits) != vt) ranges[2 * slot + 1] = (uint32_t)(i + 1);
     }

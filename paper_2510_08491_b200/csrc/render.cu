@@ -159,6 +159,7 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
         const float kap = sm.p_kap[h][tid];
         const uint32_t word = sm.p_id[h][tid];
         const uint32_t pid = word & kIdMask;
+        SNP_CHECK(h >= 0 && h < kPend && n <= kPend && (int64_t)pid < a.n);
         const int gexp = (int)((word >> 24) & 7u);
         // a grazing hit whose fp32 kappa could move this pixel by more than 6e-5 (hit.cuh,
         // kGrazeK0): the pixel goes to K6, which evaluates it with FP64 roots
@@ -196,6 +197,7 @@ __device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimi
         return;
     }
     int k = pd.n;
+    SNP_CHECK(k >= 0 && k < kPend && pd.head >= 0 && pd.head < kPend);
     if (k == 0 || pd.tail_t < tn || (pd.tail_t == tn && pd.tail_id < in)) {
         pd.tail_t = tn;
         pd.tail_id = in;
@@ -318,8 +320,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 }
                 const uint32_t e0 = beg + (uint32_t)bt * kBatch;
                 const uint32_t cnt = end > e0 ? min((uint32_t)kBatch, end - e0) : 0u;
+                SNP_CHECK(slot < kStages && cnt <= (uint32_t)kBatch && end >= beg);
                 if ((uint32_t)lane < cnt) {
                     const uint32_t id = a.vals[e0 + lane];
+                    SNP_CHECK((int64_t)id < a.n);
                     sm.id[slot][lane] = id;
                     sm.L[slot][lane] = key_depth(a.keys[e0 + lane]);
                     bulk_g2s(&sm.rec[slot][lane][0], recs + (size_t)id * rec_f4(N), Cfg<N>::kRecBytes,
@@ -389,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             } else {
                 const float4 o = make_float4(fmaf(ps.T, a.bg[0], ps.cr), fmaf(ps.T, a.bg[1], ps.cg),
                                              fmaf(ps.T, a.bg[2], ps.cb), 1.0f - ps.T);
+                SNP_CHECK(x >= 0 && x < cam->W && y >= 0 && y < cam->H);
                 reinterpret_cast<float4 *>(a.out)[((size_t)view * cam->H + y) * cam->W + x] = o;
             }
         }
@@ -493,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 bool hit = false, graze = false;
                 int gexp = 0;
                 float th = 0.f, tl = 0.f, kap = 0.f;
+                SNP_CHECK(!valid || (j < cnt && owner < 32));
                 const uint32_t idj = sm.id[slot][j];
                 if (valid)
                     hit = exact_hit<N, kGrazeDefer>(&sm.rec[slot][j][0], ro, th, tl, kap, nullptr, idj, &graze, &gexp);
@@ -559,6 +565,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     const uint32_t cm1 = __ballot_sync(0xffffffffu, cand1);
                     const uint32_t cm2 = __ballot_sync(0xffffffffu, cand2);
                     const int n1 = __popc(cm1);
+                    SNP_CHECK(qcount + __popc(cm1) + __popc(cm2) <= kQueue);
                     if (cand1) {
                         const int pos = (qhead + qcount + __popc(cm1 & lt_mask)) & (kQueue - 1);
                         sm.qj[wid][pos] = (uint8_t)j1;
@@ -999,9 +1006,11 @@ __global__ void __launch_bounds__(32) k_fallback_warp(RenderArgs a, CamBatch cb,
         const DevCam &cam = cb.cams[view - cb.view0];
         const uint32_t pix = (uint32_t)ent;
         const int x = (int)(pix % (uint32_t)cam.W), y = (int)(pix / (uint32_t)cam.W);
+        SNP_CHECK(y < cam.H);
         const int tile = (y / kTile) * a.tiles_x + (x / kTile);
         const uint32_t beg = a.ranges[2 * (view * a.tiles_per_view + tile)];
         const uint32_t end = a.ranges[2 * (view * a.tiles_per_view + tile) + 1];
+        SNP_CHECK(beg <= end);
         const float4 *recs = a.records + (size_t)view * (size_t)a.n * rec_f4(N);
         const Ray ray = make_ray(cam, x, y);
         const Prec64 g64{a.centers, a.rotations, a.scales, cam.C[0], cam.C[1], cam.C[2]};
@@ -1041,6 +1050,7 @@ __global__ void __launch_bounds__(32) k_fallback_warp(RenderArgs a, CamBatch cb,
             const uint32_t ii = sm.id[i];
             int rnk = 0;
             for (int j = 0; j < cnt; ++j) rnk += before(sm.th[j], sm.tl[j], sm.id[j], ti, li, ii) ? 1 : 0;
+            SNP_CHECK(rnk >= 0 && rnk < cnt);
             sm.ord[rnk] = (uint16_t)i;
         }
         __syncwarp();

@@ -7,6 +7,17 @@
 
 #include "../../include/snp.h"
 
+// Device-side invariant checks, compiled in only for the checked A/B build
+// (tools/ab_build.py checked -DSNP_CHECKS): index bounds of every shared-memory ring,
+// queue and global array the kernels address, plus protocol invariants.  A failed
+// check traps with file/line.  (compute-sanitizer is not available on the GPU pool.)
+#ifdef SNP_CHECKS
+#include <assert.h>
+#define SNP_CHECK(cond) assert(cond)
+#else
+#define SNP_CHECK(cond) ((void)0)
+#endif
+
 namespace snp {
 
 // Launch with the device's greatest scheduling priority.  Used for the K2-K4 chain

@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         const uint64_t kk = s_keys[i];
         const uint32_t dd = (uint32_t)(kk >> shift) & 255u;
         const uint32_t dest = s_goff[dd] + s_excl[dd] + (uint32_t)i - s_bstart[dd];
+        SNP_CHECK((int64_t)dest < n);
         kout[dest] = kk;
         vout[dest] = s_vals[i];
     }

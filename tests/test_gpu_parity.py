@@ -837,3 +837,25 @@ def test_render_full_frame_C3(orc):
     print("C3 full frame", c, "flag kinds", np.bincount(fl.ravel(), minlength=8).tolist(), res["stats"])
     assert c["max_unflagged"] <= TOL, c
     assert c["n_flagged"] <= 1e-3 * c["n"], c
+
+
+def test_repeated_renders_bit_identical():
+    """Races in K5's rings, the K5 -> K6w queue or the sort would show as frame-to-frame
+    differences: 8 renders of the C3 frame and 3 of C5 (K6w busy) are bit-identical."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    for cfg, reps in (("C3", 8), ("C5", 3)):
+        scene, cams, bg = synth.make_config(cfg)
+        h = snp.create_scene(torch_scene(scene), 0)
+        try:
+            out = torch.empty((1, cams[0].height, cams[0].width, 4), device="cuda")
+            snp.render_views(h, cams, snp.make_opts(bg, sync_check=1), out)
+            ref = out.clone()
+            for _ in range(reps):
+                out.fill_(float("nan"))
+                snp.render_views(h, cams, snp.make_opts(bg, sync_check=0), out)
+                torch.cuda.synchronize()
+                assert torch.equal(out, ref), cfg
+        finally:
+            snp.destroy(h)
