@@ -125,6 +125,8 @@ typedef struct {
     uint64_t composited;       /* kernels blended into pixels */
     uint64_t overflow_pixels;  /* pixels re-rendered by the exact fallback K6 */
     uint64_t capacity_overflow;/* 1 if the last no-sync bin_sort overflowed the key buffer */
+    uint64_t backward_skipped; /* pixels the last snp_render_backward skipped (more than 16384
+                                  hits on the ray: no gradient from them); 0 otherwise */
 } snp_stats;
 
 /* Library version string. */
@@ -188,8 +190,9 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
  * gradient 0.  Call after snp_bin_sort of the same frame, with the same opts as the
  * snp_render it differentiates (background, transmittance_floor, colour_mode); the
  * whole image only (tile_row_begin = 0, tile_row_stride = 1), else SNP_ERR_UNSUPPORTED.
- * Pixels with more than 2048 hits are skipped (snp_get_debug_counters slot 14 counts
- * them). */
+ * Every pixel is differentiated up to 16384 hits per ray (beyond 2048 through a
+ * global-memory pass); pixels with more are skipped and counted in
+ * snp_stats.backward_skipped (reset by every call). */
 snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
                                float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
                                float *grad_rotations, float *grad_scales, void *cuda_stream);

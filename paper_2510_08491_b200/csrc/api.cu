@@ -79,7 +79,8 @@ struct snp_scene_s {
     size_t param_off[8] = {};        // byte offsets of the 8 parameter arrays in `params`
     int64_t param_count[8] = {};     // floats per array
     DevBuf<float> adam_m, adam_v;    // Adam moments, same layout as `params` (training only)
-    DevBuf<uint32_t> bw_queue;       // K7: pixels with more hits than its first pass holds
+    DevBuf<uint32_t> bw_queue;       // K7: pixels with more hits than its first (second) pass holds
+    DevBuf<unsigned char> bw_scratch;  // K7: hit arrays of the global-memory pass
     float *grad_w_t = nullptr;       // where snp_render_backward adds dL/dW_t (caller-owned, device)
     bool temporal = false;
     // binning
@@ -643,8 +644,10 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     a.centers = s->centers;
     a.scales = s->scales;
     a.rotations = s->rotations;
-    SNP_CUDA(s->bw_queue.ensure((size_t)std::max<int64_t>(1, (int64_t)s->n_views * s->W * s->H)));
+    SNP_CUDA(s->bw_queue.ensure((size_t)std::max<int64_t>(1, 2 * (int64_t)s->n_views * s->W * s->H)));
     a.bw_queue = s->bw_queue.p;
+    SNP_CUDA(s->bw_scratch.ensure(backward_scratch_bytes()));
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdSkipped, 0, sizeof(unsigned long long), st));
     a.tiles_x = s->tiles_x;
     a.tiles_y = s->tiles_y;
     a.tiles_per_view = s->tiles_x * s->tiles_y;
@@ -662,7 +665,7 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
     a.counters = s->counters.p;
     BackwardGrads g{grad_w1, grad_b1, grad_w2, grad_b2, grad_sh, grad_centers, grad_rotations, grad_scales,
                     s->temporal ? s->grad_w_t : nullptr};
-    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, st));
+    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, s->bw_scratch.p, st));
     return SNP_OK;
 }
 
@@ -760,6 +763,7 @@ snp_status snp_destroy(snp_scene s) {
     s->w_t.release();
     s->adam_m.release();
     s->bw_queue.release();
+    s->bw_scratch.release();
     s->adam_v.release();
     s->keys0.release();
     s->keys1.release();
@@ -834,6 +838,7 @@ snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream) {
     out->composited = c[kCntComposited];
     out->overflow_pixels = c[kCntOverflow];
     out->capacity_overflow = c[kCntCapOverflow];
+    out->backward_skipped = c[kCntBwdSkipped];
     return SNP_OK;
 }
 

@@ -20,8 +20,10 @@
 //   dI/dW1_k = (omega / ||s||_inf) dt W2_k (-sin(phi_k) S_k (p + tau_m d) + cos(phi_k) S'_k (dt/2) d),
 //   S_k = sinc(h_k dt / 2), S' = d sinc / dx.
 // Gradients are accumulated with fp32 atomics.  Pixels with more than kBwHits hits are
-// redone by one-warp CTAs that hold kBwBigHits; beyond that they are skipped and counted
-// in counters[kCntBwdSkipped].
+// redone by one-warp CTAs that hold kBwBigHits in shared memory, and pixels with more
+// than that by one-warp CTAs whose arrays live in a global scratch (kBwHugeHits each);
+// only beyond that (tile lists of more than 16384 hits per ray) is a pixel skipped,
+// counted in counters[kCntBwdSkipped] (reset by every call, reported by snp_get_stats).
 #include "hit.cuh"
 #include "snp_internal.cuh"
 
@@ -32,8 +34,11 @@ constexpr int kBwWarps = 8;
 constexpr int kBwThreads = kBwWarps * 32;
 constexpr int kBwHits = 256;
 constexpr int kBwQueue = 64;
-// pixels with more than kBwHits hits are redone by one-warp CTAs holding kBwBigHits
+// pixels with more than kBwHits hits are redone by one-warp CTAs holding kBwBigHits,
+// and beyond that by kBwHugeCtas one-warp CTAs with kBwHugeHits in global memory
 constexpr int kBwBigHits = 2048;
+constexpr int kBwHugeHits = 16384;
+constexpr int kBwHugeCtas = 64;
 
 template <int kBwWarps, int kBwHits>
 struct BwSmem {
@@ -354,18 +359,22 @@ __device__ __forceinline__ int drain(Sm &sm, int wid, int lane, int qn, int cnt,
     return rest;
 }
 
-template <int N, bool kRay, int kBwWarps, int kBwHits>
+// kGlobal: the per-warp arrays live in gscratch (one Sm per CTA) instead of shared memory.
+// queue_in: only the listed pixels (count in counters[cnt_in]); else every pixel.  Pixels
+// with more hits than kBwHits go to queue_out (count in counters[cnt_out]), or -- without
+// one -- are skipped and counted in counters[kCntBwdSkipped].
+template <int N, bool kRay, int kBwWarps, int kBwHits, bool kGlobal>
 __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBatch cb, const float4 *__restrict__ grad,
                                                             BackwardGrads gr, float omega, const uint32_t *queue_in,
-                                                            uint32_t *queue_out) {
+                                                            int cnt_in, uint32_t *queue_out, int cnt_out,
+                                                            void *gscratch) {
     extern __shared__ __align__(16) unsigned char bw_raw[];
     using Sm = BwSmem<kBwWarps, kBwHits>;
-    Sm &sm = *reinterpret_cast<Sm *>(bw_raw);
+    Sm &sm = kGlobal ? reinterpret_cast<Sm *>(gscratch)[blockIdx.x] : *reinterpret_cast<Sm *>(bw_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const int W = cb.cams[0].W, H = cb.cams[0].H;
-    // queue_in: only the listed pixels (count in counters[kCntBwdQueue]); else every pixel
-    const int64_t npix = queue_in ? (int64_t)a.counters[kCntBwdQueue] : (int64_t)cb.nv * W * H;
+    const int64_t npix = queue_in ? (int64_t)a.counters[cnt_in] : (int64_t)cb.nv * W * H;
     int qn = 0;   // entries in this warp's gradient queue
     for (int64_t qi = (int64_t)blockIdx.x * kBwWarps + wid; qi < npix; qi += (int64_t)gridDim.x * kBwWarps) {
         const int64_t pi = queue_in ? (int64_t)queue_in[qi] : qi;
@@ -411,7 +420,7 @@ __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBat
         }
         if (cnt > kBwHits) {   // to the big-capacity pass, or (there) skipped and counted
             if (lane == 0) {
-                if (queue_out) queue_out[atomicAdd(a.counters + kCntBwdQueue, 1ull)] = (uint32_t)pi;
+                if (queue_out) queue_out[atomicAdd(a.counters + cnt_out, 1ull)] = (uint32_t)pi;
                 else atomicAdd(a.counters + kCntBwdSkipped, 1ull);
             }
             continue;
@@ -524,14 +533,16 @@ __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBat
 
 template <int N, bool kRay, int kW, int kH>
 int backward_resident() {
-    static int resident = 0;
+    static int res[64] = {};   // per device (the attribute and the occupancy are per-device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &resident = res[dev < 64 ? dev : 0];
     if (!resident) {
         const int smem = (int)sizeof(BwSmem<kW, kH>);
-        cudaFuncSetAttribute(k_backward<N, kRay, kW, kH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+        cudaFuncSetAttribute(k_backward<N, kRay, kW, kH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward<N, kRay, kW, kH>, kW * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward<N, kRay, kW, kH, false>, kW * 32, smem);
         resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
     }
     return resident;
@@ -539,39 +550,46 @@ int backward_resident() {
 
 template <int N, bool kRay>
 cudaError_t launch_backward_n(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                              float omega, cudaStream_t st) {
+                              float omega, void *scratch, cudaStream_t st) {
     const int64_t npix = (int64_t)cb.nv * cb.cams[0].W * cb.cams[0].H;
     if (npix == 0) return cudaSuccess;
+    const float4 *g4 = reinterpret_cast<const float4 *>(grad);
     cudaError_t e = cudaMemsetAsync(a.counters + kCntBwdQueue, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.counters + kCntBwdQueue2, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     const int res = backward_resident<N, kRay, kBwWarps, kBwHits>();
     const int64_t want = (npix + kBwWarps - 1) / kBwWarps;
-    k_backward<N, kRay, kBwWarps, kBwHits><<<(unsigned)(want < res ? want : res), kBwThreads,
-                                              sizeof(BwSmem<kBwWarps, kBwHits>), st>>>(
-        a, cb, reinterpret_cast<const float4 *>(grad), g, omega, nullptr, a.bw_queue);
-    // pixels with more than kBwHits hits: one warp per CTA, kBwBigHits each
-    k_backward<N, kRay, 1, kBwBigHits><<<(unsigned)backward_resident<N, kRay, 1, kBwBigHits>(), 32,
-                                          sizeof(BwSmem<1, kBwBigHits>), st>>>(
-        a, cb, reinterpret_cast<const float4 *>(grad), g, omega, a.bw_queue, nullptr);
+    k_backward<N, kRay, kBwWarps, kBwHits, false><<<(unsigned)(want < res ? want : res), kBwThreads,
+                                                     sizeof(BwSmem<kBwWarps, kBwHits>), st>>>(
+        a, cb, g4, g, omega, nullptr, 0, a.bw_queue, kCntBwdQueue, nullptr);
+    // pixels with more than kBwHits hits: one warp per CTA, kBwBigHits each in shared memory
+    k_backward<N, kRay, 1, kBwBigHits, false><<<(unsigned)backward_resident<N, kRay, 1, kBwBigHits>(), 32,
+                                                 sizeof(BwSmem<1, kBwBigHits>), st>>>(
+        a, cb, g4, g, omega, a.bw_queue, kCntBwdQueue, a.bw_queue + npix, kCntBwdQueue2, nullptr);
+    // and beyond: kBwHugeHits each in the global scratch
+    k_backward<N, kRay, 1, kBwHugeHits, true><<<kBwHugeCtas, 32, 0, st>>>(
+        a, cb, g4, g, omega, a.bw_queue + npix, kCntBwdQueue2, nullptr, 0, scratch);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t launch_backward_w(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                              float omega, cudaStream_t st) {
-    return a.colour_ray ? launch_backward_n<N, true>(a, cb, grad, g, omega, st)
-                        : launch_backward_n<N, false>(a, cb, grad, g, omega, st);
+                              float omega, void *scratch, cudaStream_t st) {
+    return a.colour_ray ? launch_backward_n<N, true>(a, cb, grad, g, omega, scratch, st)
+                        : launch_backward_n<N, false>(a, cb, grad, g, omega, scratch, st);
 }
 
 }  // namespace
 
+size_t backward_scratch_bytes() { return (size_t)kBwHugeCtas * sizeof(BwSmem<1, kBwHugeHits>); }
+
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, cudaStream_t st) {
+                            float omega, void *scratch, cudaStream_t st) {
     switch (a.n_hidden) {
-        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, st);
-        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, st);
-        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, st);
-        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, st);
+        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, scratch, st);
+        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, scratch, st);
+        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, scratch, st);
+        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, scratch, st);
         default: return cudaErrorInvalidValue;
     }
 }

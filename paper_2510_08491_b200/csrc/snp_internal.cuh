@@ -119,6 +119,7 @@ enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3
                kCntFallbackClaim = 10, kCntK5Done = 11, kCntBigQueue = 12, kCntRenderLast = kCntBigQueue,
                kCntVisibleAcc = 13, kCntBwdSkipped = 14, kCntBwdQueue = 15,
                kCntGraze = 48,          // cumulative until the debug readback
+               kCntBwdQueue2 = 49,      // K7: pixels for the global-memory pass
                kNumCounters = 56 };     // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
@@ -196,7 +197,7 @@ struct RenderArgs {
     const float *centers;          // scene centres [n][3] (FP64 grazing branch)
     const float *scales;           // scene semi-axes [n][3] (FP64 grazing branch, backward)
     const float *rotations;        // scene quaternions [n][4] (FP64 grazing branch, backward)
-    uint32_t *bw_queue;            // [V*H*W] K7's pixels for the big-capacity pass
+    uint32_t *bw_queue;            // [2][V*H*W] K7's pixels for the big-capacity and global passes
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;
@@ -239,7 +240,8 @@ struct BackwardGrads {
     float *wt;                     // temporal weights' gradient [n][N], or nullptr
 };
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, cudaStream_t st);
+                            float omega, void *scratch, cudaStream_t st);
+size_t backward_scratch_bytes();   // K7's global-memory pass (pixels with > 2048 hits)
 // train.cu: L1 loss + gradient, std(s) regulariser, Adam
 cudaError_t launch_l1(const float *out_rgba, const float *target_rgb, int64_t n, float *grad_rgba, float *loss,
                       cudaStream_t st);

@@ -60,7 +60,7 @@ class RenderOpts(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(f, C.c_uint64) for f in ("n_visible", "n_dup", "key_capacity", "tested_pairs",
                                           "candidate_pairs", "hit_pairs", "composited",
-                                          "overflow_pixels", "capacity_overflow")]
+                                          "overflow_pixels", "capacity_overflow", "backward_skipped")]
 
 
 _lock = threading.Lock()

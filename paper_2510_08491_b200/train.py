@@ -39,9 +39,11 @@ class Trainer:
     """Owns the per-rank buffers of one scene handle: image, dL/d(image), flat gradients,
     the loss scalar and the Adam step counter."""
 
-    def __init__(self, h, scene, n_views, height, width, device, lr=None, reg_weight=0.0, opts=None):
+    def __init__(self, h, scene, n_views, height, width, device, lr=None, reg_weight=0.0, opts=None,
+                 check_every=50):
         import torch
         self.h, self.lr, self.reg = h, lr, float(reg_weight)
+        self.check_every = int(check_every)   # steps between checks of K7's skipped-pixel count
         self.opts = opts if opts is not None else snp.make_opts()
         self.out = torch.zeros((n_views, height, width, 4), device=device)
         self.gout = torch.zeros_like(self.out)
@@ -57,6 +59,10 @@ class Trainer:
         snp.render_views(self.h, cams, self.opts, self.out)
         snp.loss_l1(self.out, target_rgb, self.gout, self.loss)
         snp.render_backward(self.h, self.opts, self.gout, self.grads)
+        if self.check_every and self.step_count % self.check_every == 0:
+            skipped = snp.get_stats(self.h)["backward_skipped"]   # (synchronises)
+            if skipped:
+                raise RuntimeError(f"snp_render_backward skipped {skipped} pixels with more than 16384 hits")
         if self.reg > 0.0:
             snp.scale_regularizer(self.h, self.reg, self.grads["scales"], self.loss)
         allreduce_mean(self.flat, group)

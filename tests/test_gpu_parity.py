@@ -517,7 +517,7 @@ def test_backward_mlp_and_sh_vs_finite_differences(orc, colour_mode, n_hidden):
                  for f in ("w1", "b1", "w2", "b2", "sh", "centers", "rotations", "scales")}
         snp.render_backward(h, opts, torch.from_numpy(G).cuda(), grads)
         torch.cuda.synchronize()
-        assert snp.get_debug_counters(h, 48)[14] == 0
+        assert snp.get_stats(h)["backward_skipped"] == 0
         assert out[..., 3].max().item() < 0.999
         g = {f: v.cpu().numpy().astype(np.float64) for f, v in grads.items()}
     finally:
@@ -729,14 +729,16 @@ def test_eager_emission_rule(orc, monkeypatch):
     assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
 
 
-def test_backward_long_hit_lists(orc):
-    """K7's big-capacity pass: every pixel of the deep-overlap scene has 600 hits (more
-    than the first pass holds), none is skipped, and sampled W2/b2/centre gradients match
+@pytest.mark.parametrize("n_hits", [600, 2600])
+def test_backward_long_hit_lists(orc, n_hits):
+    """K7's big-capacity passes: every pixel of the deep-overlap scene has 600 hits (more
+    than the first pass holds: the 2048-hit shared-memory pass) or 2600 (more than that:
+    the global-memory pass), none is skipped, and sampled W2/b2/centre gradients match
     central differences of the oracle."""
     import torch
     from paper_2510_08491_b200 import snp
     from gpu_util import torch_scene
-    scene = _deep_scene(600)
+    scene = _deep_scene(n_hits)
     cam = synth.look_at((0, 0, 0), (1, 0, 0), 32, 24, 1600.0)
     rng = np.random.default_rng(91)
     G = rng.normal(size=(1, 24, 32, 4)).astype(np.float32)
@@ -748,8 +750,10 @@ def test_backward_long_hit_lists(orc):
         grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in snp.FIELDS}
         snp.render_backward(h, opts, torch.from_numpy(G).cuda(), grads)
         torch.cuda.synchronize()
-        dc = snp.get_debug_counters(h, 48)
-        assert dc[15] == 32 * 24 and dc[14] == 0, (dc[14], dc[15])   # all redone, none skipped
+        dc = snp.get_debug_counters(h, 56)
+        assert dc[15] == 32 * 24, dc[15]                              # all past the first pass
+        assert dc[49] == (32 * 24 if n_hits > 2048 else 0), dc[49]    # ... and the second
+        assert snp.get_stats(h)["backward_skipped"] == 0              # none skipped
         g = {f: v.cpu().numpy().astype(np.float64) for f, v in grads.items()}
     finally:
         snp.destroy(h)

@@ -31,7 +31,7 @@ for _ in range(args.iters):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1) * 1e3)
 st = snp.get_stats(h)
-skipped = int(snp.get_debug_counters(h, 48)[14])
+skipped = int(snp.get_stats(h)["backward_skipped"])
 print(args.config, "backward us median %.1f (forward render stage for comparison: see stage_bench)" % statistics.median(ts),
       "composited", st["composited"], "skipped pixels", skipped)
 snp.destroy(h)

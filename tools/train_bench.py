@@ -53,7 +53,7 @@ if rank == 0:
                       "views_per_s": round(1000.0 * len(cams) / ms, 1), "n_gpus": world,
                       "config": {"workload": args.config, "views_per_step": len(cams), "primitives": scene.n,
                                  "width": W, "height": H}, "loss": round(loss.item(), 5),
-                      "skipped_pixels": int(snp.get_debug_counters(h, 48)[14])}))
+                      "skipped_pixels": int(snp.get_stats(h)["backward_skipped"])}))
 snp.destroy(h)
 if world > 1:
     dist.destroy_process_group()
