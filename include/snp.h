@@ -201,7 +201,13 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
  * 3DGS's loss plus a std(s) regulariser and Adam.
  * snp_loss_l1: L = sum |out_rgb - target_rgb| / (3 n_pixels) over device out_rgba
  *   [n_pixels][4] and target_rgb [n_pixels][3]; writes grad_rgba = dL/d(out_rgba) (alpha
- *   channel 0) and ADDS L to the device float *loss.  (3DGS's D-SSIM term is out of scope.)
+ *   channel 0) and ADDS L to the device float *loss.
+ * snp_loss_3dgs: 3DGS's loss L = (1 - lambda) L1 + lambda (1 - SSIM) ("the same loss
+ *   function as 3DGS"; 3DGS uses lambda = 0.2), SSIM per channel over 11x11 Gaussian windows
+ *   (sigma 1.5, zero padding), C1 = 0.01^2, C2 = 0.03^2, averaged over views, pixels and
+ *   channels (R25); images [n_views][height][width] (out RGBA, target RGB, device);
+ *   writes grad_rgba = dL/d(out_rgba) (alpha 0), ADDS L to *loss.  Scratch buffers belong to
+ *   the scene handle s (48 floats per pixel). lambda outside [0, 1]: SNP_ERR_INVALID_ARGUMENT.
  * snp_scale_regularizer: R = weight * mean_i std(s_i) (population std of the semi-axes);
  *   ADDS dR/ds to grad_scales [n][3] and R to *loss (device).
  * snp_adam_step: one Adam step (bias-corrected) on every parameter array of the scene, in
@@ -211,6 +217,8 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
  *   call); step >= 1 counts calls.  Later stages must be re-run (snp_project first). */
 snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n_pixels, float *grad_rgba, float *loss,
                        void *cuda_stream);
+snp_status snp_loss_3dgs(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views, int32_t height,
+                         int32_t width, float lambda_dssim, float *grad_rgba, float *loss, void *cuda_stream);
 snp_status snp_scale_regularizer(snp_scene s, float weight, float *grad_scales, float *loss, void *cuda_stream);
 snp_status snp_adam_step(snp_scene s, const float *const *grads, const float *lr, float beta1, float beta2, float eps,
                          int32_t step, void *cuda_stream);

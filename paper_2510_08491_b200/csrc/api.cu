@@ -81,6 +81,7 @@ struct snp_scene_s {
     DevBuf<float> adam_m, adam_v;    // Adam moments, same layout as `params` (training only)
     DevBuf<uint32_t> bw_queue;       // K7: pixels with more hits than its first (second) pass holds
     DevBuf<unsigned char> bw_scratch;  // K7: hit arrays of the global-memory pass
+    DevBuf<float> loss_scratch;        // snp_loss_3dgs: moment / SSIM-derivative maps
     float *grad_w_t = nullptr;       // where snp_render_backward adds dL/dW_t (caller-owned, device)
     bool temporal = false;
     // binning
@@ -679,6 +680,23 @@ snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n
     return SNP_OK;
 }
 
+snp_status snp_loss_3dgs(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views, int32_t height,
+                         int32_t width, float lambda_dssim, float *grad_rgba, float *loss, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (n_views < 0 || height < 0 || width < 0) return fail(SNP_ERR_INVALID_ARGUMENT, "negative image size");
+    if (!(lambda_dssim >= 0.f && lambda_dssim <= 1.f))
+        return fail(SNP_ERR_INVALID_ARGUMENT, "lambda_dssim must be in [0, 1]");
+    const int64_t total = (int64_t)n_views * height * width;
+    if (total == 0) return SNP_OK;
+    if (!out_rgba || !target_rgb || !grad_rgba || !loss) return fail(SNP_ERR_INVALID_ARGUMENT, "a pointer is NULL");
+    SNP_CUDA(s->loss_scratch.ensure(loss_3dgs_scratch_floats(n_views, height, width)));
+    SNP_CUDA(launch_loss_3dgs(out_rgba, target_rgb, n_views, height, width, lambda_dssim, grad_rgba, loss,
+                              s->loss_scratch.p, (cudaStream_t)cuda_stream));
+    return SNP_OK;
+}
+
 snp_status snp_scale_regularizer(snp_scene s, float weight, float *grad_scales, float *loss, void *cuda_stream) {
     g_err.clear();
     snp_status r = check_scene(s);
@@ -764,6 +782,7 @@ snp_status snp_destroy(snp_scene s) {
     s->adam_m.release();
     s->bw_queue.release();
     s->bw_scratch.release();
+    s->loss_scratch.release();
     s->adam_v.release();
     s->keys0.release();
     s->keys1.release();

@@ -246,6 +246,9 @@ size_t backward_scratch_bytes();   // K7's global-memory pass (pixels with > 204
 cudaError_t launch_l1(const float *out_rgba, const float *target_rgb, int64_t n, float *grad_rgba, float *loss,
                       cudaStream_t st);
 cudaError_t launch_scale_reg(const float *s, int64_t n, float w, float *grad_s, float *loss, cudaStream_t st);
+size_t loss_3dgs_scratch_floats(int V, int H, int W);
+cudaError_t launch_loss_3dgs(const float *out_rgba, const float *target_rgb, int V, int H, int W, float lam,
+                             float *grad_rgba, float *loss, float *scratch, cudaStream_t st);
 cudaError_t launch_adam(float *p, const float *g, float *m, float *v, int64_t count, float lr, float b1, float b2,
                         float eps, int step, bool log_space, cudaStream_t st);   // K5's persistent grid for `tiles` work units
 

@@ -30,7 +30,7 @@ EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
            "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at",
            "snp_render_backward", "snp_loss_l1", "snp_scale_regularizer", "snp_adam_step", "snp_get_params",
-           "snp_set_temporal_grad")
+           "snp_set_temporal_grad", "snp_loss_3dgs")
 
 
 class SnpError(RuntimeError):
@@ -95,6 +95,7 @@ def lib():
             L.snp_get_params.argtypes = [vp, C.POINTER(vp), C.c_int32, vp]
             L.snp_set_temporal_grad.argtypes = [vp, vp]
             L.snp_scale_regularizer.argtypes = [vp, C.c_float, vp, vp, vp]
+            L.snp_loss_3dgs.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_float, vp, vp, vp]
             L.snp_adam_step.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_float), C.c_float, C.c_float, C.c_float,
                                         C.c_int32, vp]
             L.snp_project_at.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp, vp]
@@ -260,6 +261,14 @@ def loss_l1(out_rgba, target_rgb, grad_rgba, loss, stream=None):
     tensors: out [..., 4], target [..., 3], loss a 1-element float tensor)."""
     n = out_rgba.numel() // 4
     _check(lib().snp_loss_l1(_ptr(out_rgba), _ptr(target_rgb), n, _ptr(grad_rgba), _ptr(loss), _stream(stream)))
+
+
+def loss_3dgs(h, out_rgba, target_rgb, grad_rgba, loss, lambda_dssim=0.2, stream=None):
+    """3DGS's loss (1 - lambda) L1 + lambda (1 - SSIM): out [V, H, W, 4], target
+    [V, H, W, 3] CUDA tensors; writes dL/d(out) into grad_rgba, adds L to loss."""
+    V, H, W = int(out_rgba.shape[0]), int(out_rgba.shape[1]), int(out_rgba.shape[2])
+    _check(lib().snp_loss_3dgs(h, _ptr(out_rgba), _ptr(target_rgb), V, H, W, float(lambda_dssim), _ptr(grad_rgba),
+                               _ptr(loss), _stream(stream)))
 
 
 def scale_regularizer(h, weight, grad_scales, loss, stream=None):

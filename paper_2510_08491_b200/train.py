@@ -40,9 +40,12 @@ class Trainer:
     the loss scalar and the Adam step counter."""
 
     def __init__(self, h, scene, n_views, height, width, device, lr=None, reg_weight=0.0, opts=None,
-                 check_every=50):
+                 check_every=50, dssim_lambda=0.2):
         import torch
         self.h, self.lr, self.reg = h, lr, float(reg_weight)
+        # the paper's loss is 3DGS's (P:416): (1 - lambda) L1 + lambda D-SSIM, lambda = 0.2;
+        # dssim_lambda = 0 takes the plain L1 kernel
+        self.dssim_lambda = float(dssim_lambda)
         self.check_every = int(check_every)   # steps between checks of K7's skipped-pixel count
         self.opts = opts if opts is not None else snp.make_opts()
         self.out = torch.zeros((n_views, height, width, 4), device=device)
@@ -52,12 +55,15 @@ class Trainer:
         self.step_count = 0
 
     def step(self, cams, target_rgb, group=None):
-        """One training step on this rank's views; returns this rank's loss (a device
-        scalar, read by the caller when it wants it)."""
+        """One training step on this rank's views (target_rgb [n_views, H, W, 3]); returns
+        this rank's loss (a device scalar, read by the caller when it wants it)."""
         self.flat.zero_()
         self.loss.zero_()
         snp.render_views(self.h, cams, self.opts, self.out)
-        snp.loss_l1(self.out, target_rgb, self.gout, self.loss)
+        if self.dssim_lambda > 0.0:
+            snp.loss_3dgs(self.h, self.out, target_rgb, self.gout, self.loss, self.dssim_lambda)
+        else:
+            snp.loss_l1(self.out, target_rgb, self.gout, self.loss)
         snp.render_backward(self.h, self.opts, self.gout, self.grads)
         if self.check_every and self.step_count % self.check_every == 0:
             skipped = snp.get_stats(self.h)["backward_skipped"]   # (synchronises)

@@ -619,9 +619,92 @@ def test_adam_and_l1_kernels():
         assert np.allclose(got[f].cpu().numpy(), p, rtol=2e-5, atol=2e-6), f
 
 
-def test_training_step_reduces_loss():
-    """SURVEY §8(f) rank 4 on one GPU: render 4 views, L1 vs target images of a reference
-    scene, K7 gradients, Adam (P:735 rates, x5) -- the loss falls over 40 steps."""
+def _ssim_loss_torch(out, tgt, lam):
+    """3DGS's loss, written with torch CPU ops in float64 (the plain reference of the op):
+    (1 - lam) mean|x - y| + lam (1 - mean SSIM), SSIM from an 11x11 Gaussian window
+    (sigma 1.5) by conv2d with zero padding, C1 = 0.01^2, C2 = 0.03^2, per channel."""
+    import torch
+    import torch.nn.functional as F
+    x = out[..., :3].permute(0, 3, 1, 2)
+    y = tgt.permute(0, 3, 1, 2)
+    k = torch.arange(11, dtype=torch.float64) - 5
+    g1 = torch.exp(-k * k / (2 * 1.5 ** 2))
+    g1 = g1 / g1.sum()
+    win = (g1[:, None] * g1[None, :]).expand(3, 1, 11, 11).contiguous()
+    conv = lambda z: F.conv2d(z, win, padding=5, groups=3)  # noqa: E731
+    mx, my = conv(x), conv(y)
+    sxx, syy, sxy = conv(x * x) - mx * mx, conv(y * y) - my * my, conv(x * y) - mx * my
+    C1, C2 = 0.01 ** 2, 0.03 ** 2
+    ssim = ((2 * mx * my + C1) * (2 * sxy + C2)) / ((mx * mx + my * my + C1) * (sxx + syy + C2))
+    return (1 - lam) * (x - y).abs().mean() + lam * (1 - ssim.mean())
+
+
+@pytest.mark.parametrize("lam", [0.2, 0.0, 1.0])
+def test_loss_3dgs_against_torch(lam):
+    """snp_loss_3dgs (the 3DGS loss, R25) against the torch float64 definition:
+    loss and dL/d(out) by autograd, on 2 views of a ragged 37x29 image."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    rng = np.random.default_rng(77)
+    out = rng.uniform(0, 1, (2, 29, 37, 4)).astype(np.float32)
+    tgt = np.clip(out[..., :3] + rng.normal(0, 0.15, (2, 29, 37, 3)), 0, 1).astype(np.float32)
+    h = snp.create_scene(torch_scene(synth.make_scene(1, 4)), 0)
+    try:
+        g = torch.zeros((2, 29, 37, 4), device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        snp.loss_3dgs(h, torch.from_numpy(out).cuda(), torch.from_numpy(tgt).cuda(), g, loss, lam)
+        torch.cuda.synchronize()
+    finally:
+        snp.destroy(h)
+    xo = torch.from_numpy(out.astype(np.float64)).requires_grad_(True)
+    ref = _ssim_loss_torch(xo, torch.from_numpy(tgt.astype(np.float64)), lam)
+    ref.backward()
+    assert abs(loss.item() - ref.item()) < 2e-6 * max(1.0, abs(ref.item())), (loss.item(), ref.item())
+    gr = xo.grad.numpy()
+    gg = g.cpu().numpy()
+    scale = np.abs(gr).max()
+    assert np.abs(gg - gr).max() <= 2e-4 * scale, (np.abs(gg - gr).max(), scale)
+
+
+def test_scale_regularizer_kernel():
+    """snp_scale_regularizer (P:416's std(s) penalty): R = w mean_i std(s_i) and dR/ds
+    against the numpy definition and central differences of it."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene = synth.make_scene(73, 200)
+    scene.scales[7] = np.float32([0.3, 0.3, 0.3])        # std 0: zero gradient
+    w = 0.37
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        gs = torch.zeros((200, 3), device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        snp.scale_regularizer(h, w, gs, loss)
+        torch.cuda.synchronize()
+    finally:
+        snp.destroy(h)
+    s = scene.scales.astype(np.float64)
+
+    def R(s):
+        return w * np.std(s, axis=1).mean()
+    assert abs(loss.item() - R(s)) < 1e-6 * max(1.0, R(s))
+    g = gs.cpu().numpy()
+    assert np.all(g[7] == 0)
+    for i, j in ((0, 0), (3, 2), (150, 1), (199, 0)):
+        e = 1e-6
+        sp, sm = s.copy(), s.copy()
+        sp[i, j] += e
+        sm[i, j] -= e
+        fd = (R(sp) - R(sm)) / (2 * e)
+        assert abs(g[i, j] - fd) <= 1e-4 * abs(fd) + 1e-9, (i, j, g[i, j], fd)
+
+
+@pytest.mark.parametrize("dssim_lambda", [0.0, 0.2])
+def test_training_step_reduces_loss(dssim_lambda):
+    """SURVEY §8(f) rank 4 on one GPU: render 4 views, L1 or 3DGS's L1 + D-SSIM vs
+    target images of a reference scene, K7 gradients, Adam (P:735 rates, x5) -- the loss
+    falls over 40 steps."""
     import torch
     from paper_2510_08491_b200 import snp, train
     from gpu_util import torch_scene
@@ -642,7 +725,7 @@ def test_training_step_reduces_loss():
     h = snp.create_scene(torch_scene(init), 0)
     try:
         tr = train.Trainer(h, init, 4, 72, 96, "cuda", lr={f: 5 * v for f, v in snp.PAPER_LR.items()},
-                           opts=snp.make_opts(bg))
+                           opts=snp.make_opts(bg), dssim_lambda=dssim_lambda)
         losses = [tr.step(cams, target).item() for _ in range(40)]
     finally:
         snp.destroy(h)

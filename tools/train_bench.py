@@ -48,7 +48,7 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / args.steps
 ms = mg.max_over_ranks(ms, "cuda") if world > 1 else ms
 if rank == 0:
-    print(json.dumps({"metric": "training steps/s (forward + L1 + backward + all-reduce + Adam)",
+    print(json.dumps({"metric": "training steps/s (forward + 3DGS loss (L1 + D-SSIM, lambda 0.2) + backward + all-reduce + Adam)",
                       "value": round(1000.0 / ms, 3), "unit": "steps/s", "ms_per_step": round(ms, 2),
                       "views_per_s": round(1000.0 * len(cams) / ms, 1), "n_gpus": world,
                       "config": {"workload": args.config, "views_per_step": len(cams), "primitives": scene.n,
