@@ -196,6 +196,15 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
 snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
                                float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
                                float *grad_rotations, float *grad_scales, void *cuda_stream);
+/* As snp_render_backward, given fwd_rgba = the out_rgba (device) of the snp_render of the
+ * same binning and opts that the gradients refer to (NULL: rendered again internally).
+ * The backward re-runs K5's traversal in gradient mode (each composited hit yields dL/dI
+ * and dL/dc from fwd_rgba and its transmittance), then the per-hit parameter gradients;
+ * pixels K5 hands to its fallbacks are differentiated by the per-pixel K7. */
+snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, const float *fwd_rgba,
+                                  const float *grad_rgba, float *grad_w1, float *grad_b1, float *grad_w2,
+                                  float *grad_b2, float *grad_sh, float *grad_centers, float *grad_rotations,
+                                  float *grad_scales, void *cuda_stream);
 
 /* Training step.  The paper trains with
  * 3DGS's loss plus a std(s) regulariser and Adam.

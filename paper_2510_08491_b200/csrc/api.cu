@@ -82,6 +82,9 @@ struct snp_scene_s {
     DevBuf<uint32_t> bw_queue;       // K7: pixels with more hits than its first (second) pass holds
     DevBuf<unsigned char> bw_scratch;  // K7: hit arrays of the global-memory pass
     DevBuf<float> loss_scratch;        // snp_loss_3dgs: moment / SSIM-derivative maps
+    DevBuf<uint32_t> bw_skip;          // K7: composited hits K5's grad mode already emitted, per pixel
+    DevBuf<float> bw_fwd;              // K7: the forward image when the caller does not pass it
+    DevBuf<GradEntry> grad_entries;    // K5 grad mode -> K7f
     float *grad_w_t = nullptr;       // where snp_render_backward adds dL/dW_t (caller-owned, device)
     bool temporal = false;
     // binning
@@ -534,42 +537,8 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     return SNP_OK;
 }
 
-snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba, void *cuda_stream) {
-    g_err.clear();
-    snp_status r = check_scene(s);
-    if (r != SNP_OK) return r;
-    if (!opts || !out_rgba) return fail(SNP_ERR_INVALID_ARGUMENT, "opts or out_rgba is NULL");
-    if (s->state < kBinned) return fail(SNP_ERR_BAD_STATE, "snp_render before snp_bin_sort");
-    if (!(opts->transmittance_floor >= 0.f) || !(opts->transmittance_floor < 1.f))
-        return fail(SNP_ERR_INVALID_ARGUMENT, "transmittance_floor must be in [0, 1)");
-    if (opts->out_memory != SNP_MEM_HOST && opts->out_memory != SNP_MEM_DEVICE &&
-        opts->out_memory != SNP_MEM_HOST_ASYNC)
-        return fail(SNP_ERR_INVALID_ARGUMENT, "out_memory must be SNP_MEM_HOST, SNP_MEM_DEVICE or SNP_MEM_HOST_ASYNC");
-    if (opts->colour_mode != SNP_COLOUR_PRIMITIVE && opts->colour_mode != SNP_COLOUR_RAY)
-        return fail(SNP_ERR_INVALID_ARGUMENT, "colour_mode must be SNP_COLOUR_PRIMITIVE or SNP_COLOUR_RAY");
-    const bool host_out = opts->out_memory != SNP_MEM_DEVICE;
-    cudaStream_t st = (cudaStream_t)cuda_stream;
-    const size_t out_floats = (size_t)s->n_views * s->W * s->H * 4;
-    float *dout = out_rgba;
-    if (host_out) {
-        SNP_CUDA(s->host_out_staging.ensure(out_floats));
-        dout = s->host_out_staging.p;
-        // pixels outside the stripe come back as 0 (every pixel is written otherwise)
-        if (s->row_begin != 0 || s->row_stride != 1)
-            SNP_CUDA(cudaMemsetAsync(dout, 0, out_floats * sizeof(float), st));
-    }
-    const int64_t fb_cap = std::min<int64_t>((int64_t)s->n_views * s->W * s->H, (int64_t)1 << 22);
-    if (s->fallback_capacity < fb_cap) {
-        SNP_CUDA(s->fallback.ensure((size_t)(2 * fb_cap)));
-        SNP_CUDA(cudaMemsetAsync(s->fallback.p, 0, sizeof(unsigned long long) * (size_t)(2 * fb_cap), st));
-        s->fallback_capacity = fb_cap;
-    }
-    // stats, fallback queue, tile queue: K4 cleared them for the first render of this
-    // binning; a further render clears them with one memset (contiguous counters)
-    if (s->render_dirty)
-        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
-                                 sizeof(unsigned long long) * (kCntRenderLast - kCntTested + 1), st));
-    s->render_dirty = true;
+// Common render arguments of a binned scene (K5, K6w, K6, K7).
+static RenderArgs render_args(snp_scene s, const snp_render_opts *opts) {
     RenderArgs a{};
     a.n_hidden = s->n_hidden;
     a.colour_ray = opts->colour_mode == SNP_COLOUR_RAY ? 1 : 0;
@@ -599,12 +568,31 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
         const char *dbg = std::getenv("SNP_DEBUG");
         a.debug_flags = dbg ? std::atoi(dbg) : 0;
     }
+    a.counters = s->counters.p;
+    return a;
+}
+
+// K5 (+ K6w, K6) into a device image: the body of snp_render.
+static snp_status render_device(snp_scene s, const snp_render_opts *opts, float *dout, cudaStream_t st) {
+    const int64_t fb_cap = std::min<int64_t>((int64_t)s->n_views * s->W * s->H, (int64_t)1 << 22);
+    if (s->fallback_capacity < fb_cap) {
+        SNP_CUDA(s->fallback.ensure((size_t)(2 * fb_cap)));
+        SNP_CUDA(cudaMemsetAsync(s->fallback.p, 0, sizeof(unsigned long long) * (size_t)(2 * fb_cap), st));
+        s->fallback_capacity = fb_cap;
+    }
+    // stats, fallback queue, tile queue: K4 cleared them for the first render of this
+    // binning; a further render clears them with one memset (contiguous counters)
+    if (s->render_dirty)
+        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntTested, 0,
+                                 sizeof(unsigned long long) * (kCntRenderLast - kCntTested + 1), st));
+    s->render_dirty = true;
+    RenderArgs a = render_args(s, opts);
     a.out = dout;
     a.fallback = s->fallback.p;
     a.fallback_capacity = s->fallback_capacity;
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
-    a.counters = s->counters.p;
-    a.k5_grid = render_grid(s->n_hidden, a.colour_ray != 0, a.eager_emit != 0, s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
+    a.k5_grid = render_grid(s->n_hidden, a.colour_ray != 0, a.eager_emit != 0,
+                            s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
     if (s->stripe_rows > 0) {
         // (an empty scene has empty tile ranges: every pixel gets the background)
         for (size_t k = 0; k < s->cams.size(); ++k) {
@@ -614,6 +602,35 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
         // (SNP_DEBUG bit 2 skips K6: timing experiments only, overflowed pixels stay unwritten)
         if (s->n > 0 && !(a.debug_flags & 2)) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
     }
+    return SNP_OK;
+}
+
+snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba, void *cuda_stream) {
+    g_err.clear();
+    snp_status r = check_scene(s);
+    if (r != SNP_OK) return r;
+    if (!opts || !out_rgba) return fail(SNP_ERR_INVALID_ARGUMENT, "opts or out_rgba is NULL");
+    if (s->state < kBinned) return fail(SNP_ERR_BAD_STATE, "snp_render before snp_bin_sort");
+    if (!(opts->transmittance_floor >= 0.f) || !(opts->transmittance_floor < 1.f))
+        return fail(SNP_ERR_INVALID_ARGUMENT, "transmittance_floor must be in [0, 1)");
+    if (opts->out_memory != SNP_MEM_HOST && opts->out_memory != SNP_MEM_DEVICE &&
+        opts->out_memory != SNP_MEM_HOST_ASYNC)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "out_memory must be SNP_MEM_HOST, SNP_MEM_DEVICE or SNP_MEM_HOST_ASYNC");
+    if (opts->colour_mode != SNP_COLOUR_PRIMITIVE && opts->colour_mode != SNP_COLOUR_RAY)
+        return fail(SNP_ERR_INVALID_ARGUMENT, "colour_mode must be SNP_COLOUR_PRIMITIVE or SNP_COLOUR_RAY");
+    const bool host_out = opts->out_memory != SNP_MEM_DEVICE;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const size_t out_floats = (size_t)s->n_views * s->W * s->H * 4;
+    float *dout = out_rgba;
+    if (host_out) {
+        SNP_CUDA(s->host_out_staging.ensure(out_floats));
+        dout = s->host_out_staging.p;
+        // pixels outside the stripe come back as 0 (every pixel is written otherwise)
+        if (s->row_begin != 0 || s->row_stride != 1)
+            SNP_CUDA(cudaMemsetAsync(dout, 0, out_floats * sizeof(float), st));
+    }
+    r = render_device(s, opts, dout, st);
+    if (r != SNP_OK) return r;
     if (host_out) {
         SNP_CUDA(cudaMemcpyAsync(out_rgba, dout, out_floats * sizeof(float), cudaMemcpyDeviceToHost, st));
         if (opts->out_memory == SNP_MEM_HOST) SNP_CUDA(cudaStreamSynchronize(st));
@@ -621,9 +638,10 @@ snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba,
     return SNP_OK;
 }
 
-snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
-                               float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
-                               float *grad_rotations, float *grad_scales, void *cuda_stream) {
+snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, const float *fwd_rgba,
+                                  const float *grad_rgba, float *grad_w1, float *grad_b1, float *grad_w2,
+                                  float *grad_b2, float *grad_sh, float *grad_centers, float *grad_rotations,
+                                  float *grad_scales, void *cuda_stream) {
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -636,38 +654,68 @@ snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const f
         return fail(SNP_ERR_UNSUPPORTED, "snp_render_backward needs the whole image (tile rows 0, 1)");
     if (opts->colour_mode != SNP_COLOUR_PRIMITIVE && opts->colour_mode != SNP_COLOUR_RAY)
         return fail(SNP_ERR_INVALID_ARGUMENT, "colour_mode must be SNP_COLOUR_PRIMITIVE or SNP_COLOUR_RAY");
+    if (!(opts->transmittance_floor >= 0.f) || !(opts->transmittance_floor < 1.f))
+        return fail(SNP_ERR_INVALID_ARGUMENT, "transmittance_floor must be in [0, 1)");
     cudaStream_t st = (cudaStream_t)cuda_stream;
-    RenderArgs a{};
-    a.n_hidden = s->n_hidden;
-    a.colour_ray = opts->colour_mode == SNP_COLOUR_RAY ? 1 : 0;
-    a.sh = s->sh;
-    a.sh_degree = s->sh_degree;
-    a.centers = s->centers;
-    a.scales = s->scales;
-    a.rotations = s->rotations;
-    SNP_CUDA(s->bw_queue.ensure((size_t)std::max<int64_t>(1, 2 * (int64_t)s->n_views * s->W * s->H)));
-    a.bw_queue = s->bw_queue.p;
+    const int64_t npix_all = (int64_t)s->n_views * s->W * s->H;
+    const int64_t npix_batch = (int64_t)std::min<int>(s->n_views, kCamsPerLaunch) * s->W * s->H;
+    SNP_CUDA(s->bw_queue.ensure((size_t)std::max<int64_t>(1, 3 * npix_batch)));
+    SNP_CUDA(s->bw_skip.ensure((size_t)std::max<int64_t>(1, npix_batch)));
     SNP_CUDA(s->bw_scratch.ensure(backward_scratch_bytes()));
     SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdSkipped, 0, sizeof(unsigned long long), st));
-    a.tiles_x = s->tiles_x;
-    a.tiles_y = s->tiles_y;
-    a.tiles_per_view = s->tiles_x * s->tiles_y;
-    a.tile_bits = s->tile_bits;
-    a.row_begin = 0;
-    a.row_stride = 1;
-    a.stripe_rows = s->stripe_rows;
-    a.n = s->n;
-    a.records = s->records.p;
-    a.keys = s->sorted_idx ? s->keys1.p : s->keys0.p;
-    a.vals = s->sorted_idx ? s->vals1.p : s->vals0.p;
-    a.ranges = s->ranges.p;
-    for (int c = 0; c < 3; ++c) a.bg[c] = opts->background[c];
-    a.t_floor = opts->transmittance_floor;
-    a.counters = s->counters.p;
     BackwardGrads g{grad_w1, grad_b1, grad_w2, grad_b2, grad_sh, grad_centers, grad_rotations, grad_scales,
-                    s->temporal ? s->grad_w_t : nullptr};
-    for (const CamBatch &cb : s->cams) SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, s->bw_scratch.p, st));
+                    s->temporal ? s->grad_w_t : nullptr, false};
+    {
+        auto al = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
+        g.vec = al(grad_w1) && al(grad_b1) && al(grad_w2) && al(grad_sh) && al(grad_rotations) && al(g.wt);
+    }
+    const bool legacy = [] {   // A/B: the per-pixel K7 for every pixel (round-1 path)
+        const char *e = std::getenv("SNP_BWD_LEGACY");
+        return e && std::atoi(e) != 0;
+    }();
+    if (legacy) {
+        RenderArgs a = render_args(s, opts);
+        a.bw_queue = s->bw_queue.p;
+        for (const CamBatch &cb : s->cams)
+            SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, s->bw_scratch.p, false, st));
+        return SNP_OK;
+    }
+    // the forward result the gradients refer to (the caller's, or rendered here)
+    const float *fwd = fwd_rgba;
+    if (!fwd) {
+        SNP_CUDA(s->bw_fwd.ensure((size_t)std::max<int64_t>(1, npix_all * 4)));
+        r = render_device(s, opts, s->bw_fwd.p, st);
+        if (r != SNP_OK) return r;
+        fwd = s->bw_fwd.p;
+    }
+    // K5 in grad mode: one GradEntry per composited hit (12 per pixel of a camera batch
+    // before the path falls back to the per-pixel K7 for every pixel)
+    const int64_t cap = 12 * npix_batch;
+    SNP_CUDA(s->grad_entries.ensure((size_t)std::max<int64_t>(1, cap)));
+    RenderArgs a = render_args(s, opts);
+    a.bw_queue = s->bw_queue.p;
+    a.bw_skip = s->bw_skip.p;
+    a.grad_in = reinterpret_cast<const float4 *>(grad_rgba);
+    a.fwd = reinterpret_cast<const float4 *>(fwd);
+    a.grad_entries = s->grad_entries.p;
+    a.grad_cap = cap;
+    const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
+    for (size_t k = 0; k < s->cams.size(); ++k) {
+        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdQueue, 0, sizeof(unsigned long long), st));
+        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGradEntries, 0, 2 * sizeof(unsigned long long), st));
+        a.tile_order = s->tile_order.p + k * order_stride;
+        if (s->n > 0) SNP_CUDA(launch_render_grad(a, s->cams[k], st));
+        // K7f over the entries, then the per-pixel K7 for the pixels K5 queued
+        SNP_CUDA(launch_backward(a, s->cams[k], grad_rgba, g, s->omega, s->bw_scratch.p, true, st));
+    }
     return SNP_OK;
+}
+
+snp_status snp_render_backward(snp_scene s, const snp_render_opts *opts, const float *grad_rgba, float *grad_w1,
+                               float *grad_b1, float *grad_w2, float *grad_b2, float *grad_sh, float *grad_centers,
+                               float *grad_rotations, float *grad_scales, void *cuda_stream) {
+    return snp_render_backward_ex(s, opts, nullptr, grad_rgba, grad_w1, grad_b1, grad_w2, grad_b2, grad_sh,
+                                  grad_centers, grad_rotations, grad_scales, cuda_stream);
 }
 
 snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n_pixels, float *grad_rgba, float *loss,
@@ -783,6 +831,9 @@ snp_status snp_destroy(snp_scene s) {
     s->bw_queue.release();
     s->bw_scratch.release();
     s->loss_scratch.release();
+    s->bw_skip.release();
+    s->bw_fwd.release();
+    s->grad_entries.release();
     s->adam_v.release();
     s->keys0.release();
     s->keys1.release();

@@ -58,11 +58,25 @@ struct BwSmem {
     float q_gc[kBwWarps][3][kBwQueue];
 };
 
+// Four consecutive gradient entries: one 16-byte vector atomic (red.global.add.v4.f32,
+// sm_90+) when the arrays are 16-byte aligned (gr.vec), else four scalar atomics.
+__device__ __forceinline__ void add4(float *p, float a, float b, float c, float d, bool vec) {
+    if (vec) {
+        atomicAdd(reinterpret_cast<float4 *>(p), make_float4(a, b, c, d));
+    } else {
+        atomicAdd(p, a);
+        atomicAdd(p + 1, b);
+        atomicAdd(p + 2, c);
+        atomicAdd(p + 3, d);
+    }
+}
+
 __device__ __forceinline__ float dsinc_f(float x) {
     // d/dx sin(x)/x = (cos x - sinc x) / x; Taylor -x/3 + x^3/30 below |x| = 0.25
     const float x2 = x * x;
     if (fabsf(x) < 0.25f) return x * fmaf(x2, 1.0f / 30.0f, -1.0f / 3.0f);
-    return (__cosf(x) - __sinf(x) / x) / x;
+    const float ix = rcp_fast(x);
+    return (__cosf(x) - __sinf(x) * ix) * ix;
 }
 
 // dL/dI (gI) of one (ray, record) hit into the gradients of primitive `prim`: the MLP
@@ -118,6 +132,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     for (int gq = 0; gq < N / 4; ++gq) {
         const float4 w4 = rec[rec_w2(N) + gq];
         const float w2s[4] = {w4.x, w4.y, w4.z, w4.w};
+        float a_w2[4], a_b1[4], a_w1[12];   // this group's four units, added as vectors below
 #pragma unroll
         for (int uu = 0; uu < 4; ++uu) {
             const int k = 4 * gq + uu;
@@ -126,11 +141,11 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
             const float h = fmaf(u.z, d[2], fmaf(u.y, d[1], u.x * d[0]));
             const float g = fmaf(u.z, p[2], fmaf(u.y, p[1], fmaf(u.x, p[0], u.w)));
             const float phi = fmaf(h, tm, g);
+            // (MUFU sin/cos and the forward's sinc: the same approximations as exact_hit)
             float sn, cs;
-            sincosf(phi, &sn, &cs);
+            __sincosf(phi, &sn, &cs);
             const float x = h * hdt;
-            const float S = fabsf(x) < 0.25f ? fmaf(x * x, fmaf(x * x, 8.3333333e-03f, -1.6666667e-01f), 1.0f)
-                                             : sinf(x) / x;
+            const float S = sinc_f(x);
             const float Sp = dsinc_f(x);
             sumc = fmaf(w2 * cs, S, sumc);
             gdt = fmaf(w2 * cs * Sp, 0.5f * h, gdt);
@@ -145,14 +160,20 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
                                  fmaf(coef, fmaf(tm, d[1], p[1]), chs * d[1]),
                                  fmaf(coef, fmaf(tm, d[2], p[2]), chs * d[2])};
             gsmax -= (gw[0] * u.x + gw[1] * u.y + gw[2] * u.z) / smax;
-            atomicAdd(gr.w2 + wbase + k, gI * dt * cs * S);
-            atomicAdd(gr.b1 + wbase + k, gI * omega * coef);
-            // temporal scene: the record's phase offset is omega (b1 + xi_t W_t) (R24)
-            if (gr.wt) atomicAdd(gr.wt + wbase + k, gI * omega * coef * xi_t);
-            atomicAdd(gr.w1 + 3 * (wbase + k) + 0, gI * s1 * gw[0]);
-            atomicAdd(gr.w1 + 3 * (wbase + k) + 1, gI * s1 * gw[1]);
-            atomicAdd(gr.w1 + 3 * (wbase + k) + 2, gI * s1 * gw[2]);
+            a_w2[uu] = gI * dt * cs * S;
+            a_b1[uu] = gI * omega * coef;
+            a_w1[3 * uu + 0] = gI * s1 * gw[0];
+            a_w1[3 * uu + 1] = gI * s1 * gw[1];
+            a_w1[3 * uu + 2] = gI * s1 * gw[2];
         }
+        const uint32_t k0 = wbase + 4 * gq;
+        add4(gr.w2 + k0, a_w2[0], a_w2[1], a_w2[2], a_w2[3], gr.vec);
+        add4(gr.b1 + k0, a_b1[0], a_b1[1], a_b1[2], a_b1[3], gr.vec);
+        // temporal scene: the record's phase offset is omega (b1 + xi_t W_t) (R24)
+        if (gr.wt) add4(gr.wt + k0, xi_t * a_b1[0], xi_t * a_b1[1], xi_t * a_b1[2], xi_t * a_b1[3], gr.vec);
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+            add4(gr.w1 + 3 * k0 + 4 * v, a_w1[4 * v], a_w1[4 * v + 1], a_w1[4 * v + 2], a_w1[4 * v + 3], gr.vec);
     }
     atomicAdd(gr.b2 + prim, gI * dt);
     if (!gr.mu) return;
@@ -221,10 +242,8 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     const float gz_ = 2.0f * (-2.0f * z * G_R[0] - w * G_R[1] + x * G_R[2] + w * G_R[3] - 2.0f * z * G_R[4] +
                               y * G_R[5] + x * G_R[6] + y * G_R[7]);
     const float dotq = w * gw_ + x * gx_ + y * gy_ + z * gz_;
-    atomicAdd(gr.q + 4 * (size_t)prim + 0, (gw_ - w * dotq) / qn);
-    atomicAdd(gr.q + 4 * (size_t)prim + 1, (gx_ - x * dotq) / qn);
-    atomicAdd(gr.q + 4 * (size_t)prim + 2, (gy_ - y * dotq) / qn);
-    atomicAdd(gr.q + 4 * (size_t)prim + 3, (gz_ - z * dotq) / qn);
+    add4(gr.q + 4 * (size_t)prim, (gw_ - w * dotq) / qn, (gx_ - x * dotq) / qn, (gy_ - y * dotq) / qn,
+         (gz_ - z * dotq) / qn, gr.vec);
 }
 
 // d Y_lm / d dir for the basis of sh_basis_f (rows: coefficient, columns: x, y, z)
@@ -297,10 +316,21 @@ __device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 
     sh_basis_f(dxv, dyv, dzv, Y);
     const float g0 = gc[0], g1 = gc[1], g2 = gc[2];
     float *gs = gr.sh + 48 * (size_t)id;
-    for (int i = 0; i < ncoef; ++i) {
-        if (g0 != 0.f) atomicAdd(gs + 3 * i + 0, Y[i] * g0);
-        if (g1 != 0.f) atomicAdd(gs + 3 * i + 1, Y[i] * g1);
-        if (g2 != 0.f) atomicAdd(gs + 3 * i + 2, Y[i] * g2);
+    if (g0 != 0.f || g1 != 0.f || g2 != 0.f) {
+        // the 3 ncoef coefficients (RGB innermost), four at a time
+        const float gcv[3] = {g0, g1, g2};
+#pragma unroll
+        for (int f0 = 0; f0 < 48; f0 += 4) {   // (unrolled: Y stays in registers)
+            if (f0 < 3 * ncoef) {
+                float v4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int f = f0 + u;
+                    v4[u] = f < 3 * ncoef ? Y[f / 3] * gcv[f % 3] : 0.f;
+                }
+                add4(gs + f0, v4[0], v4[1], v4[2], v4[3], gr.vec);
+            }
+        }
     }
     if (!kRay && gr.mu && (g0 != 0.f || g1 != 0.f || g2 != 0.f)) {
         // colour direction dir = (mu - C) / |mu - C|: dL/dmu = (I - dir dir^T) dL/ddir / |mu - C|
@@ -308,11 +338,14 @@ __device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 
         float dY[16][3];
         sh_basis_grad(dxv, dyv, dzv, dY);
         float gd[3] = {0.f, 0.f, 0.f};
-        for (int i = 0; i < ncoef; ++i) {
-            const float e = shp[3 * i] * g0 + shp[3 * i + 1] * g1 + shp[3 * i + 2] * g2;
-            gd[0] = fmaf(dY[i][0], e, gd[0]);
-            gd[1] = fmaf(dY[i][1], e, gd[1]);
-            gd[2] = fmaf(dY[i][2], e, gd[2]);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {   // (unrolled: dY stays in registers)
+            if (i < ncoef) {
+                const float e = shp[3 * i] * g0 + shp[3 * i + 1] * g1 + shp[3 * i + 2] * g2;
+                gd[0] = fmaf(dY[i][0], e, gd[0]);
+                gd[1] = fmaf(dY[i][1], e, gd[1]);
+                gd[2] = fmaf(dY[i][2], e, gd[2]);
+            }
         }
         const float4 mh = rec[kRecMh], ml = rec[kRecMl];
         const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
@@ -363,17 +396,26 @@ __device__ __forceinline__ int drain(Sm &sm, int wid, int lane, int qn, int cnt,
 // queue_in: only the listed pixels (count in counters[cnt_in]); else every pixel.  Pixels
 // with more hits than kBwHits go to queue_out (count in counters[cnt_out]), or -- without
 // one -- are skipped and counted in counters[kCntBwdSkipped].
+// skip (K5-based backward): skip[pixel] composited hits of the pixel already have their
+// gradients (K5's grad mode emitted them before the pixel overflowed); nullptr = none.
+// all_if: if *all_if != 0 the queue is ignored and every pixel is processed (the K5 path's
+// entry buffer overflowed: its entries are discarded and this kernel does everything).
 template <int N, bool kRay, int kBwWarps, int kBwHits, bool kGlobal>
 __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBatch cb, const float4 *__restrict__ grad,
                                                             BackwardGrads gr, float omega, const uint32_t *queue_in,
                                                             int cnt_in, uint32_t *queue_out, int cnt_out,
-                                                            void *gscratch) {
+                                                            void *gscratch, const uint32_t *skip,
+                                                            const unsigned long long *all_if) {
     extern __shared__ __align__(16) unsigned char bw_raw[];
     using Sm = BwSmem<kBwWarps, kBwHits>;
     Sm &sm = kGlobal ? reinterpret_cast<Sm *>(gscratch)[blockIdx.x] : *reinterpret_cast<Sm *>(bw_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const int W = cb.cams[0].W, H = cb.cams[0].H;
+    if (all_if && *all_if) {
+        queue_in = nullptr;
+        skip = nullptr;
+    }
     const int64_t npix = queue_in ? (int64_t)a.counters[cnt_in] : (int64_t)cb.nv * W * H;
     int qn = 0;   // entries in this warp's gradient queue
     for (int64_t qi = (int64_t)blockIdx.x * kBwWarps + wid; qi < npix; qi += (int64_t)gridDim.x * kBwWarps) {
@@ -508,7 +550,7 @@ __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBat
         __syncwarp();
         // ---- queue the composited hits; drain 32 at a time (all lanes busy)
         const int nc = sm.ncomp[wid];
-        for (int k0 = 0; k0 < nc;) {
+        for (int k0 = skip ? (int)skip[pi] : 0; k0 < nc;) {
             const int m = min(nc - k0, kBwQueue - qn);
             for (int e = lane; e < m; e += 32) {
                 const int k = k0 + e, slot = qn + e;
@@ -548,35 +590,83 @@ int backward_resident() {
     return resident;
 }
 
+// The per-pixel chain.  k5 = false: every pixel (level 1), its overflow through levels 2
+// and 3.  k5 = true: only the pixels K5's grad mode queued (bw_queue[0..]), from their
+// skip counts, or every pixel if the K5 path's entry buffer overflowed.
 template <int N, bool kRay>
 cudaError_t launch_backward_n(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                              float omega, void *scratch, cudaStream_t st) {
+                              float omega, void *scratch, bool k5, cudaStream_t st) {
     const int64_t npix = (int64_t)cb.nv * cb.cams[0].W * cb.cams[0].H;
     if (npix == 0) return cudaSuccess;
     const float4 *g4 = reinterpret_cast<const float4 *>(grad);
-    cudaError_t e = cudaMemsetAsync(a.counters + kCntBwdQueue, 0, sizeof(unsigned long long), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(a.counters + kCntBwdQueue2, 0, sizeof(unsigned long long), st);
+    cudaError_t e = cudaMemsetAsync(a.counters + kCntBwdQueue2, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.counters + kCntBwdQueue3, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess && !k5) e = cudaMemsetAsync(a.counters + kCntBwdQueue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     const int res = backward_resident<N, kRay, kBwWarps, kBwHits>();
     const int64_t want = (npix + kBwWarps - 1) / kBwWarps;
+    uint32_t *q1 = a.bw_queue, *q2 = a.bw_queue + npix, *q3 = a.bw_queue + 2 * npix;
+    const uint32_t *skip = k5 ? a.bw_skip : nullptr;
+    const unsigned long long *all_if = k5 ? a.counters + kCntGradOverflow : nullptr;
     k_backward<N, kRay, kBwWarps, kBwHits, false><<<(unsigned)(want < res ? want : res), kBwThreads,
                                                      sizeof(BwSmem<kBwWarps, kBwHits>), st>>>(
-        a, cb, g4, g, omega, nullptr, 0, a.bw_queue, kCntBwdQueue, nullptr);
+        a, cb, g4, g, omega, k5 ? q1 : nullptr, kCntBwdQueue, q2, kCntBwdQueue2, nullptr, skip, all_if);
     // pixels with more than kBwHits hits: one warp per CTA, kBwBigHits each in shared memory
     k_backward<N, kRay, 1, kBwBigHits, false><<<(unsigned)backward_resident<N, kRay, 1, kBwBigHits>(), 32,
                                                  sizeof(BwSmem<1, kBwBigHits>), st>>>(
-        a, cb, g4, g, omega, a.bw_queue, kCntBwdQueue, a.bw_queue + npix, kCntBwdQueue2, nullptr);
+        a, cb, g4, g, omega, q2, kCntBwdQueue2, q3, kCntBwdQueue3, nullptr, skip, nullptr);
     // and beyond: kBwHugeHits each in the global scratch
     k_backward<N, kRay, 1, kBwHugeHits, true><<<kBwHugeCtas, 32, 0, st>>>(
-        a, cb, g4, g, omega, a.bw_queue + npix, kCntBwdQueue2, nullptr, 0, scratch);
+        a, cb, g4, g, omega, q3, kCntBwdQueue3, nullptr, 0, scratch, skip, nullptr);
+    return cudaGetLastError();
+}
+
+// K7f: the parameter gradients of every hit K5's grad mode emitted (one thread per entry;
+// skipped wholesale if the entry buffer overflowed -- the per-pixel chain then redoes all)
+template <int N, bool kRay>
+__global__ void __launch_bounds__(128) k_grad_entries(RenderArgs a, CamBatch cb, const GradEntry *__restrict__ ent,
+                                                      BackwardGrads gr, float omega) {
+    if (a.counters[kCntGradOverflow]) return;
+    // the batch's cameras in shared memory (a dynamic index into the parameter struct
+    // would copy it to local memory)
+    __shared__ DevCam s_cam[kCamsPerLaunch];
+    for (int i = threadIdx.x; i < cb.nv; i += blockDim.x) s_cam[i] = cb.cams[i];
+    __syncthreads();
+    int64_t n = (int64_t)a.counters[kCntGradEntries];
+    if (n > a.grad_cap) n = a.grad_cap;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const GradEntry e = ent[i];
+        const int vloc = (int)(e.pix >> 24);
+        const DevCam &cam = s_cam[vloc];
+        const uint32_t p = e.pix & 0xffffffu;
+        const int y = (int)(p / (uint32_t)cam.W), x = (int)(p - (uint32_t)y * (uint32_t)cam.W);
+        const Ray ray = make_ray(cam, x, y);
+        const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + e.id) * rec_f4(N);
+        const float gc[3] = {e.gc0, e.gc1, e.gc2};
+        hit_all_grads<N, kRay>(a, rec, ray, e.id, e.gI, gc, omega, gr, cam.xi_t);
+    }
+}
+
+template <int N, bool kRay>
+cudaError_t launch_grad_entries_n(const RenderArgs &a, const CamBatch &cb, const BackwardGrads &g, float omega,
+                                  cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_grad_entries<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, a.grad_entries, g, omega);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t launch_backward_w(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                              float omega, void *scratch, cudaStream_t st) {
-    return a.colour_ray ? launch_backward_n<N, true>(a, cb, grad, g, omega, scratch, st)
-                        : launch_backward_n<N, false>(a, cb, grad, g, omega, scratch, st);
+                              float omega, void *scratch, bool k5, cudaStream_t st) {
+    if (k5) {
+        cudaError_t e = a.colour_ray ? launch_grad_entries_n<N, true>(a, cb, g, omega, st)
+                                     : launch_grad_entries_n<N, false>(a, cb, g, omega, st);
+        if (e != cudaSuccess) return e;
+    }
+    return a.colour_ray ? launch_backward_n<N, true>(a, cb, grad, g, omega, scratch, k5, st)
+                        : launch_backward_n<N, false>(a, cb, grad, g, omega, scratch, k5, st);
 }
 
 }  // namespace
@@ -584,12 +674,12 @@ cudaError_t launch_backward_w(const RenderArgs &a, const CamBatch &cb, const flo
 size_t backward_scratch_bytes() { return (size_t)kBwHugeCtas * sizeof(BwSmem<1, kBwHugeHits>); }
 
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, void *scratch, cudaStream_t st) {
+                            float omega, void *scratch, bool k5, cudaStream_t st) {
     switch (a.n_hidden) {
-        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, scratch, st);
-        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, scratch, st);
-        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, scratch, st);
-        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, scratch, st);
+        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, scratch, k5, st);
+        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, scratch, k5, st);
+        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, scratch, k5, st);
+        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, scratch, k5, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -147,9 +147,20 @@ struct PixelState {
 // (strictly): every hit not yet inserted has t_in >= L (R19), so these are
 // exactly the next hits of the ray in (t_in, id) order (Eq. 4).  The
 // list is sorted, so they are popped from its head.
-template <int N, bool kRay>
+// K5 grad mode (the backward's forward traversal): the pixel's
+// dL/d(out) G and forward result F, and the warp's shared-memory entry staging.
+struct GradCtx {
+    float4 G, F;
+    GradEntry *st;        // this warp's staging (kGradStage entries)
+    int *cnt;             // its fill count (shared atomics)
+    uint32_t pix;         // view within the batch << 24 | y * W + x
+};
+constexpr int kGradStage = kPend * 32;   // one emission call of a warp: at most 16 hits per lane
+
+template <int N, bool kRay, bool kGrad = false>
 __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, float L, float t_floor,
-                                     const float4 *recs, const RenderArgs &a, const Ray &ray) {
+                                     const float4 *recs, const RenderArgs &a, const Ray &ray,
+                                     GradCtx *gx = nullptr) {
     const int tid = threadIdx.x;
     int n = pd.n;
     int h = pd.head;
@@ -169,10 +180,33 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
             break;
         }
         const float4 rgb = hit_rgb<kRay>(recs + (size_t)pid * rec_f4(N), a.sh, a.sh_degree, pid, ray);
-        const float w = ps.T * kap;
+        const float Tb = ps.T;
+        const float w = Tb * kap;
         ps.cr = fmaf(w, rgb.y, ps.cr);
         ps.cg = fmaf(w, rgb.z, ps.cg);
         ps.cb = fmaf(w, rgb.w, ps.cb);
+        if (kGrad) {
+            // out = sum_j T_j k_j c_j + T_end bg, so the light behind this hit is
+            // U = out - (colour accumulated up to and including it); then (K7's formulas)
+            // dL/dk = G_rgb . (T c - U / (1 - k)) + G_a T_end / (1 - k), dL/dI = (1 - k) dL/dk
+            // for I > 0 (Eq. 9), dL/dc = T k G_rgb on unclamped channels
+            const float4 G = gx->G, F = gx->F;
+            if (G.x != 0.f || G.y != 0.f || G.z != 0.f || G.w != 0.f) {
+                const float om = fmaxf(1.0f - kap, 1e-20f), iom = 1.0f / om;
+                float dk = G.w * (1.0f - F.w) * iom;
+                dk = fmaf(G.x, fmaf(-(F.x - ps.cr), iom, Tb * rgb.y), dk);
+                dk = fmaf(G.y, fmaf(-(F.y - ps.cg), iom, Tb * rgb.z), dk);
+                dk = fmaf(G.z, fmaf(-(F.z - ps.cb), iom, Tb * rgb.w), dk);
+                GradEntry e;
+                e.pix = gx->pix;
+                e.id = pid;
+                e.gI = kap > 0.f ? dk * (1.0f - kap) : 0.f;
+                e.gc0 = rgb.y > 0.f ? w * G.x : 0.f;
+                e.gc1 = rgb.z > 0.f ? w * G.y : 0.f;
+                e.gc2 = rgb.w > 0.f ? w * G.z : 0.f;
+                gx->st[atomicAdd(gx->cnt, 1)] = e;
+            }
+        }
         ps.T *= (1.0f - kap);
         ++ps.composited;
         --n;
@@ -221,16 +255,23 @@ __device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimi
     ++pd.n;
 }
 
-template <int N, bool kRay, bool kEager>
-__global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
+// kGrad: the backward's forward traversal (no image output): every composited hit of a
+// pixel with a nonzero dL/d(out) becomes a GradEntry (staged per warp in shared memory
+// after Smem, flushed to a.grad_entries); an overflowing pixel is queued for K7 with its
+// count of already emitted hits.  One CTA per SM (registers and the staging).
+template <int N, bool kRay, bool kEager, bool kGrad = false>
+__global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a, CamBatch cb) {
     constexpr int kStages = Cfg<N>::kStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
+    GradEntry *gstage = reinterpret_cast<GradEntry *>(smem_raw + sizeof(Smem<N>));
+    int *gcount = reinterpret_cast<int *>(gstage + (kGrad ? kConsumers * kGradStage : 0));
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     const int stripe_tiles = a.tiles_x * a.stripe_rows;
     const int total_tiles = stripe_tiles * cb.nv;
 
+    if (kGrad && tid < kConsumers) gcount[tid] = 0;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
@@ -381,9 +422,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     float pxf = 0.f, pyf = 0.f, bx0 = 0.f, by0 = 0.f;
     PixelState ps{1.f, 0.f, 0.f, 0.f, true, false, 0u};
     Pending pd{0, 0, 0.f, 0u, false};
+    GradCtx gx{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), gstage + wid * kGradStage,
+               gcount + wid, 0u};
+    int64_t gpi = 0;   // (kGrad) pixel index within the camera batch
 
     auto finish_tile = [&]() {   // write this warp's pixels; count the warp as done with the tile
-        if (inside) {
+        if (kGrad) {
+            if (inside && ps.overflow) {   // K7 redoes the pixel, from its emitted hits on
+                const unsigned long long q = atomicAdd(a.counters + kCntBwdQueue, 1ull);
+                a.bw_queue[q] = (uint32_t)gpi;
+                a.bw_skip[gpi] = ps.composited;
+            }
+        } else if (inside) {
             if (ps.overflow) {
                 const unsigned long long q = atomicAdd(a.counters + kCntFallbackQueue, 1ull);
                 if ((int64_t)q < a.fallback_capacity)
@@ -439,6 +489,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
             by0 = (float)by + 0.5f;
             ps = PixelState{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
             pd = Pending{0, 0, 0.f, 0u, false};
+            if (kGrad) {
+                gpi = ((int64_t)vloc * cam->H + y) * cam->W + x;
+                const int64_t gi = ((int64_t)view * cam->H + y) * cam->W + x;
+                gx.G = inside ? a.grad_in[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+                gx.F = inside ? a.fwd[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+                gx.pix = ((uint32_t)vloc << 24) | (uint32_t)(inside ? y * cam->W + x : 0);
+            }
             sm.p_in[tid] = 0u;
             tile_finished = false;
         }
@@ -615,11 +672,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                     ++ins_ecalls;
                     ins_enone += (pd.n == 0);
 #endif
-                    emit<N, kRay>(sm, ps, pd, batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
-                                  a.t_floor, recs, a, ray);
+                    emit<N, kRay, kGrad>(sm, ps, pd,
+                                         batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                                         a.t_floor, recs, a, ray, &gx);
 #ifdef SNP_INSTRUMENT
                     ins_emit += clock64() - _e0;
 #endif
+                }
+                if (kGrad) {   // flush the warp's staged gradient entries (one global atomic)
+                    __syncwarp();
+                    const int c = *gx.cnt;
+                    if (c) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(a.counters + kCntGradEntries, (unsigned long long)c);
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        for (int i = lane; i < c; i += 32)
+                            if ((int64_t)(base + i) < a.grad_cap) a.grad_entries[base + i] = gx.st[i];
+                        if (lane == 0 && (int64_t)(base + c) > a.grad_cap)
+                            atomicExch(a.counters + kCntGradOverflow, 1ull);
+                        __syncwarp();
+                        if (lane == 0) *gx.cnt = 0;
+                        __syncwarp();
+                    }
                 }
                 if (batch_end) break;
             }
@@ -661,6 +735,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
     }
 #endif
     __syncwarp();
+    if (kGrad) {   // (the backward's traversal leaves the forward's statistics alone)
+        warp_exit();
+        return;
+    }
     const uint32_t v[5] = {(uint32_t)n_tested, n_cand, n_hit, n_comp, n_ovf};
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
@@ -1231,6 +1309,46 @@ cudaError_t launch_fallback_w(const RenderArgs &a, const CamBatch *cams, int n_b
                         : launch_fallback_n<N, false>(a, cams, n_batches, st);
 }
 }  // namespace
+
+namespace {
+template <int N, bool kRay>
+cudaError_t launch_render_grad_n(const RenderArgs &a, const CamBatch &cams, cudaStream_t st) {
+    const int smem = (int)(sizeof(Smem<N>) + (size_t)kConsumers * kGradStage * sizeof(GradEntry) + 64);
+    static int res[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &resident = res[dev < kMaxDevices ? dev : 0];
+    if (!resident) {
+        int sms = 0, per_sm = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay, false, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N, kRay, false, true>, kThreads, smem);
+        resident = std::max(1, sms) * std::max(1, per_sm);
+    }
+    const int tiles = a.tiles_x * a.stripe_rows * cams.nv;
+    k_render<N, kRay, false, true><<<std::min(tiles, resident), kThreads, smem, st>>>(a, cams);
+    return cudaGetLastError();
+}
+template <int N>
+cudaError_t launch_render_grad_w(const RenderArgs &a, const CamBatch &cams, cudaStream_t st) {
+    return a.colour_ray ? launch_render_grad_n<N, true>(a, cams, st) : launch_render_grad_n<N, false>(a, cams, st);
+}
+}  // namespace
+
+cudaError_t launch_render_grad(const RenderArgs &a, const CamBatch &cams, cudaStream_t st) {
+    if (a.tiles_x * a.stripe_rows * cams.nv == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.counters + kCntTileQueue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    switch (a.n_hidden) {
+        case 4: return launch_render_grad_w<4>(a, cams, st);
+        case 8: return launch_render_grad_w<8>(a, cams, st);
+        case 16: return launch_render_grad_w<16>(a, cams, st);
+        case 32: return launch_render_grad_w<32>(a, cams, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
 
 cudaError_t launch_render(const RenderArgs &a, const CamBatch &cams, bool reset_queue, cudaStream_t st) {
     const int tiles = a.tiles_x * a.stripe_rows * cams.nv;

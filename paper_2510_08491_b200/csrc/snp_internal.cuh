@@ -119,7 +119,10 @@ enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3
                kCntFallbackClaim = 10, kCntK5Done = 11, kCntBigQueue = 12, kCntRenderLast = kCntBigQueue,
                kCntVisibleAcc = 13, kCntBwdSkipped = 14, kCntBwdQueue = 15,
                kCntGraze = 48,          // cumulative until the debug readback
-               kCntBwdQueue2 = 49,      // K7: pixels for the global-memory pass
+               kCntBwdQueue2 = 49,      // K7: pixels for its second (2048-hit) pass
+               kCntBwdQueue3 = 50,      // K7: pixels for the global-memory pass
+               kCntGradEntries = 51,    // K5 grad mode: gradient entries emitted
+               kCntGradOverflow = 52,   // K5 grad mode: the entry buffer overflowed
                kNumCounters = 56 };     // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
@@ -188,6 +191,14 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
                             const unsigned long long *counters, int passes, SortScratch scratch,
                             int64_t expected_n, cudaStream_t st, int *final_idx);
 
+// K5 grad mode (the backward's forward traversal): one entry per composited hit, its
+// dL/dI and dL/dc, from which K7f computes the parameter gradients
+struct GradEntry {
+    uint32_t pix;      // view within the camera batch << 24 | y * W + x
+    uint32_t id;       // primitive
+    float gI, gc0, gc1, gc2;
+};
+
 struct RenderArgs {
     int32_t n_hidden;              // N_sigma (hidden_supported): selects the kernel instantiation
     int32_t colour_ray;            // 1: SH colour at each pixel's ray direction (SNP_COLOUR_RAY)
@@ -197,7 +208,12 @@ struct RenderArgs {
     const float *centers;          // scene centres [n][3] (FP64 grazing branch)
     const float *scales;           // scene semi-axes [n][3] (FP64 grazing branch, backward)
     const float *rotations;        // scene quaternions [n][4] (FP64 grazing branch, backward)
-    uint32_t *bw_queue;            // [2][V*H*W] K7's pixels for the big-capacity and global passes
+    uint32_t *bw_queue;            // [3][V*H*W] K7's pixel queues (K5 grad overflow, > 256, > 2048 hits)
+    uint32_t *bw_skip;             // [V*H*W] composited hits of a pixel K5's grad mode already emitted
+    const float4 *grad_in;         // K5 grad mode: dL/d(out RGBA) [V][H][W]
+    const float4 *fwd;             // K5 grad mode: the forward's out RGBA [V][H][W]
+    GradEntry *grad_entries;       // K5 grad mode: entry buffer
+    int64_t grad_cap;
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;
@@ -238,9 +254,13 @@ struct BackwardGrads {
     float *w1, *b1, *w2, *b2, *sh;
     float *mu, *q, *s;             // geometry gradients, or all nullptr (not computed)
     float *wt;                     // temporal weights' gradient [n][N], or nullptr
+    bool vec;                      // every array 16-byte aligned: vector (float4) atomics
 };
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, void *scratch, cudaStream_t st);
+                            float omega, void *scratch, bool k5, cudaStream_t st);
+// K5 in grad mode over one camera batch (render.cu): the forward traversal emitting
+// GradEntry per composited hit; overflowing pixels go to bw_queue with their skip count
+cudaError_t launch_render_grad(const RenderArgs &a, const CamBatch &cams, cudaStream_t st);
 size_t backward_scratch_bytes();   // K7's global-memory pass (pixels with > 2048 hits)
 // train.cu: L1 loss + gradient, std(s) regulariser, Adam
 cudaError_t launch_l1(const float *out_rgba, const float *target_rgb, int64_t n, float *grad_rgba, float *loss,

@@ -30,7 +30,7 @@ EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
            "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at",
            "snp_render_backward", "snp_loss_l1", "snp_scale_regularizer", "snp_adam_step", "snp_get_params",
-           "snp_set_temporal_grad", "snp_loss_3dgs")
+           "snp_set_temporal_grad", "snp_loss_3dgs", "snp_render_backward_ex")
 
 
 class SnpError(RuntimeError):
@@ -91,6 +91,8 @@ def lib():
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
             L.snp_set_temporal.argtypes = [vp, vp, C.c_int32, vp]
             L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+            L.snp_render_backward_ex.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                                 vp]
             L.snp_loss_l1.argtypes = [vp, vp, C.c_int64, vp, vp, vp]
             L.snp_get_params.argtypes = [vp, C.POINTER(vp), C.c_int32, vp]
             L.snp_set_temporal_grad.argtypes = [vp, vp]
@@ -241,14 +243,15 @@ def render_views(h, cams, opts, out, stream=None, xi_t=None):
         render(h, opts, out, stream)
 
 
-def render_backward(h, opts, grad_rgba, grads, stream=None):
+def render_backward(h, opts, grad_rgba, grads, stream=None, fwd_rgba=None):
     """K7: adds dL/d{w1, b1, w2, b2, sh} and, when ``grads`` has "centers", "rotations" and
     "scales", the geometry gradients (dict of CUDA tensors shaped like the scene's arrays)
-    for grad_rgba = dL/d(out RGBA) (CUDA tensor [V, H, W, 4])."""
-    _check(lib().snp_render_backward(h, C.byref(opts), _ptr(grad_rgba), _ptr(grads["w1"]), _ptr(grads["b1"]),
-                                     _ptr(grads["w2"]), _ptr(grads["b2"]), _ptr(grads["sh"]),
-                                     _ptr(grads.get("centers")), _ptr(grads.get("rotations")),
-                                     _ptr(grads.get("scales")), _stream(stream)))
+    for grad_rgba = dL/d(out RGBA) (CUDA tensor [V, H, W, 4]); fwd_rgba: the forward image
+    the gradients refer to (the render's out), or None (rendered again)."""
+    _check(lib().snp_render_backward_ex(h, C.byref(opts), _ptr(fwd_rgba), _ptr(grad_rgba), _ptr(grads["w1"]),
+                                        _ptr(grads["b1"]), _ptr(grads["w2"]), _ptr(grads["b2"]), _ptr(grads["sh"]),
+                                        _ptr(grads.get("centers")), _ptr(grads.get("rotations")),
+                                        _ptr(grads.get("scales")), _stream(stream)))
 
 
 # P:735 learning rates (MLP 1e-3, means 1.6e-4, scales 5e-3, quaternions 1e-3, SH 2.5e-3)

@@ -64,7 +64,7 @@ class Trainer:
             snp.loss_3dgs(self.h, self.out, target_rgb, self.gout, self.loss, self.dssim_lambda)
         else:
             snp.loss_l1(self.out, target_rgb, self.gout, self.loss)
-        snp.render_backward(self.h, self.opts, self.gout, self.grads)
+        snp.render_backward(self.h, self.opts, self.gout, self.grads, fwd_rgba=self.out)
         if self.check_every and self.step_count % self.check_every == 0:
             skipped = snp.get_stats(self.h)["backward_skipped"]   # (synchronises)
             if skipped:

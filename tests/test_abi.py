@@ -65,6 +65,8 @@ def test_argument_validation_without_gpu(snp):
     assert L.snp_project_at(None, None, 1, None, None) == 1
     assert L.snp_set_temporal(None, None, 0, None) == 1
     assert L.snp_render_backward(None, None, None, None, None, None, None, None, None, None, None, None) == 1
+    assert L.snp_render_backward_ex(None, None, None, None, None, None, None, None, None, None, None, None,
+                                    None) == 1
     assert L.snp_scale_regularizer(None, 0.0, None, None, None) == 1
     assert L.snp_adam_step(None, None, None, 0.9, 0.999, 1e-8, 1, None) == 1
     assert L.snp_get_params(None, None, 0, None) == 1

@@ -27,11 +27,11 @@ for _ in range(args.iters):
     for v in grads.values():
         v.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(); snp.render_backward(h, opts, G, grads); e1.record()
+    e0.record(); snp.render_backward(h, opts, G, grads, fwd_rgba=out); e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1) * 1e3)
 st = snp.get_stats(h)
 skipped = int(snp.get_stats(h)["backward_skipped"])
-print(args.config, "backward us median %.1f (forward render stage for comparison: see stage_bench)" % statistics.median(ts),
+print(args.config, "legacy" if os.environ.get("SNP_BWD_LEGACY") else "k5-path", "backward us median %.1f (forward render stage for comparison: see stage_bench)" % statistics.median(ts),
       "composited", st["composited"], "skipped pixels", skipped)
 snp.destroy(h)
