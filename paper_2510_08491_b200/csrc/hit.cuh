@@ -216,6 +216,10 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
     const float dt = thi - tlo;
     const float tm = 0.5f * (tlo + thi);
     const float hdt = 0.5f * dt;
+    // phase at the segment's midpoint x_m = p + tau_m d (relative to mu) and the half
+    // segment hdt d: g_k + h_k tau_m = W1'_k.x_m + omega b1_k, h_k hdt = W1'_k.(hdt d)
+    const float xmx = fmaf(tm, r.dhx, px), xmy = fmaf(tm, r.dhy, py), xmz = fmaf(tm, r.dhz, pz);
+    const float hx = hdt * r.dhx, hy = hdt * r.dhy, hz = hdt * r.dhz;
     float acc = 0.f;
     float W2[N];
 #pragma unroll
@@ -226,10 +230,9 @@ __device__ __forceinline__ bool exact_hit(const float4 *__restrict__ rec, const 
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const float4 u = rec[kRecUnits + k];
-        const float h = fmaf(u.z, r.dhz, fmaf(u.y, r.dhy, u.x * r.dhx));
-        const float g = fmaf(u.z, pz, fmaf(u.y, py, fmaf(u.x, px, u.w)));
-        const float phi = fmaf(h, tm, g);
-        acc = fmaf(W2[k], __cosf(phi) * sinc_f(h * hdt), acc);
+        const float phi = fmaf(u.z, xmz, fmaf(u.y, xmy, fmaf(u.x, xmx, u.w)));
+        const float x = fmaf(u.z, hz, fmaf(u.y, hy, u.x * hx));
+        acc = fmaf(W2[k], __cosf(phi) * sinc_f(x), acc);
     }
     const float I = dt * (acc + mh.w);
     kap = 1.0f - __expf(-fmaxf(I, 0.0f));

@@ -175,6 +175,7 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
         // a grazing hit whose fp32 kappa could move this pixel by more than 6e-5 (hit.cuh,
         // kGrazeK0): the pixel goes to K6, which evaluates it with FP64 roots
         if (gexp && (gexp == 7 || ps.T * (float)(1 << gexp) > 2.0f)) {
+            atomicAdd(a.counters + kCntGraze, 1ull);   // (rare)
             ps.overflow = true;
             ps.done = true;
             break;
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
     const long long ins_start = clock64();
 #endif
     const int plimit = a.pending_limit < kPend ? a.pending_limit : kPend;
-    uint32_t n_cand = 0, n_hit = 0, n_comp = 0, n_ovf = 0, n_graze = 0;
+    uint32_t n_cand = 0, n_hit = 0, n_comp = 0, n_ovf = 0;
     unsigned long long n_tested = 0;
     // per-tile state
     int cur_seq = -1;
@@ -518,8 +519,9 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
                     // half extents of the conic's bounding box, with a 0.1% + 1e-3 px margin
                     // (which also covers the approximate reciprocal and square roots)
                     const float rdet = rcp_fast(det);
-                    const float rx = __fsqrt_rn(cc * rdet) * 1.001f + 1e-3f;
-                    const float ry = __fsqrt_rn(c0.z * rdet) * 1.001f + 1e-3f;
+                    const float vx = cc * rdet, vy = c0.z * rdet;
+                    const float rx = vx * rsqrtf(vx) * 1.001f + 1e-3f;
+                    const float ry = vy * rsqrtf(vy) * 1.001f + 1e-3f;
                     touch = c0.x + rx >= bx0 && c0.x - rx <= bx0 + 7.0f && c0.y + ry >= by0 &&
                             c0.y - ry <= by0 + 3.0f;
                 } else {
@@ -560,7 +562,6 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
                 if (valid)
                     hit = exact_hit<N, kGrazeDefer>(&sm.rec[slot][j][0], ro, th, tl, kap, nullptr, idj, &graze, &gexp);
                 n_hit += hit;
-                n_graze += hit && graze;
 #ifdef SNP_INSTRUMENT
                 long long _i0 = clock64();
 #endif
@@ -744,10 +745,6 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
     for (int c = 0; c < 5; ++c) {
         const uint32_t s = __reduce_add_sync(0xffffffffu, v[c]);   // per-warp totals fit 32 bits
         if (lane == 0 && s) atomicAdd(a.counters + kCntTested + c, (unsigned long long)s);
-    }
-    {
-        const uint32_t s = __reduce_add_sync(0xffffffffu, n_graze);
-        if (lane == 0 && s) atomicAdd(a.counters + kCntGraze, (unsigned long long)s);
     }
     warp_exit();
 }
