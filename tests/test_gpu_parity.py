@@ -84,14 +84,19 @@ def test_render_sampled_full_size(orc, cfg, n_rand, n_tiles):
 
 
 def test_multiview_batch_C4(orc):
+    """C4 (64 orbit views in one call, two camera batches): every view, 150 random pixels
+    plus one full tile each (9,984 + 64 x 256 pixels) against the oracle."""
     scene, cams, bg = synth.make_config("C4")
-    sel = [0, 21, 63]
     res = gpu_render(scene, cams, bg)
-    for v in sel:
-        px, py = sample_pixels(cams[v], 300, 1, seed=v)
+    worst, flagged, n = 0.0, 0, 0
+    for v in range(len(cams)):
+        px, py = sample_pixels(cams[v], 150, 1, seed=v)
         out_o, fl, _ = orc.render_pixels(scene, cams[v], px, py, bg)
         c = compare(res["img"][v][py, px], out_o, fl)
         assert c["max_unflagged"] <= TOL, (v, c)
+        worst, flagged, n = max(worst, c["max_unflagged"]), flagged + c["n_flagged"], n + c["n"]
+    print("C4 all views:", worst, flagged, n)
+    assert flagged <= 0.005 * n
 
 
 def test_multiview_equals_single_view():
