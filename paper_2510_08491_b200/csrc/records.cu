@@ -391,12 +391,15 @@ __global__ void __launch_bounds__(kProjThreads, 8) k_records(ProjectArgs a, CamB
 namespace {
 template <int N>
 cudaError_t launch_records_n(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};   // per device (the attribute is a per-device property)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    bool &done = attr[dev < 64 ? dev : 0];
+    if (!done) {
         cudaError_t e = cudaFuncSetAttribute(k_records<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sizeof(ProjSmem<N>));
         if (e != cudaSuccess) return e;
-        attr = true;
+        done = true;
     }
     k_records<N><<<(unsigned)((a.n + kProjThreads - 1) / kProjThreads), kProjThreads, sizeof(ProjSmem<N>), st>>>(a,
                                                                                                              cams);

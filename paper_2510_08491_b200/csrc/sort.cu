@@ -249,10 +249,12 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
     if (capacity == 0 || passes == 0) return cudaSuccess;
     const int64_t maxp = (capacity + kPart - 1) / kPart;
     if (maxp > sc.max_partitions) return cudaErrorInvalidValue;
-    static int resident = 0;
+    static int res[64] = {};   // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &resident = res[dev < 64 ? dev : 0];
     if (!resident) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass, kThreads, 0);
         resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
