@@ -570,9 +570,18 @@ def cpu_baseline(scene, cam, bg, budget_s=15.0, gpu_frame=None):
             n_bad += int((err[ok] > 1e-4).sum())
         chunk = min(chunk * 2, 1 << 16)
     pps = n / dt
+    # the same oracle on one core (both timings), a smaller seeded sample
+    m1, t1 = max(256, int(pps * 3.0 / max(cores, 1))), 0.0
+    px1, py1 = rng.integers(0, W, m1), rng.integers(0, H, m1)
+    t0 = time.perf_counter()
+    oracle.render_pixels(scene, cam, px1, py1, bg, nthreads=1)
+    t1 = time.perf_counter() - t0
     res = {"value": pps / (W * H), "unit": "frames/s", "cores": cores, "kind": "oracle",
            "sample": f"{n} seeded random pixels of the C3 view ({dt:.1f} s, OpenMP over pixels)",
-           "pixels_per_s": round(pps, 1)}
+           "pixels_per_s": round(pps, 1),
+           "single_thread": {"pixels_per_s": round(m1 / t1, 1), "frames_per_s": m1 / t1 / (W * H),
+                             "sample": f"{m1} seeded random pixels ({t1:.1f} s, 1 thread; includes the "
+                                       "oracle's per-call scene setup)"}}
     if gpu_frame is not None:
         res["parity"] = {"max_unflagged": worst, "max_all": worst_all, "n_flagged": n_flag, "n": n,
                          "n_over_tol": n_bad, "tol": 1e-4,
