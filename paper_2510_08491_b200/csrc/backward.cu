@@ -637,6 +637,7 @@ __global__ void __launch_bounds__(128) k_grad_entries(RenderArgs a, CamBatch cb,
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const GradEntry e = ent[i];
         const int vloc = (int)(e.pix >> 24);
+        SNP_CHECK(vloc < cb.nv && (int64_t)e.id < a.n);
         const DevCam &cam = s_cam[vloc];
         const uint32_t p = e.pix & 0xffffffu;
         const int y = (int)(p / (uint32_t)cam.W), x = (int)(p - (uint32_t)y * (uint32_t)cam.W);

@@ -683,6 +683,7 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
                 if (kGrad) {   // flush the warp's staged gradient entries (one global atomic)
                     __syncwarp();
                     const int c = *gx.cnt;
+                    SNP_CHECK(c >= 0 && c <= kGradStage);
                     if (c) {
                         unsigned long long base = 0;
                         if (lane == 0) base = atomicAdd(a.counters + kCntGradEntries, (unsigned long long)c);
