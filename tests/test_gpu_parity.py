@@ -624,6 +624,37 @@ def test_backward_k5_path_matches_per_pixel_k7(monkeypatch, colour_mode):
             assert np.abs(a - b).max() <= 2e-4 * scale + 1e-7, (f, np.abs(a - b).max(), scale)
 
 
+def test_backward_two_camera_batches(monkeypatch):
+    """34 views (two camera batches of at most 32): the K5-path backward, batch by batch
+    (entry buffer, fallback queues and skip counts reset per batch), equals the per-pixel
+    K7 on every parameter."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene = synth.make_scene(5, 600, box=0.7)
+    cams = synth.orbit_cameras(34, 3.0, 40, 28, 50.0, elev_deg=(5, 60))
+    G = torch.from_numpy(np.random.default_rng(7).normal(size=(34, 28, 40, 4)).astype(np.float32)).cuda()
+    res = {}
+    for legacy in (0, 1):
+        monkeypatch.setenv("SNP_BWD_LEGACY", str(legacy))
+        h = snp.create_scene(torch_scene(scene), 0)
+        try:
+            snp.set_pending_limit(h, 4)
+            opts = snp.make_opts((0.1, 0.1, 0.1))
+            out = torch.zeros((34, 28, 40, 4), device="cuda")
+            snp.render_views(h, cams, opts, out)
+            grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in snp.FIELDS}
+            snp.render_backward(h, opts, G, grads, fwd_rgba=out if legacy == 0 else None)
+            torch.cuda.synchronize()
+            res[legacy] = {f: v.cpu().numpy().astype(np.float64) for f, v in grads.items()}
+        finally:
+            snp.destroy(h)
+    for f in snp.FIELDS:
+        a, b = res[0][f], res[1][f]
+        scale = np.abs(b).max()
+        assert scale > 0 and np.abs(a - b).max() <= 2e-4 * scale + 1e-7, (f, np.abs(a - b).max(), scale)
+
+
 def test_adam_and_l1_kernels():
     """snp_loss_l1 and snp_adam_step against their plain definitions (numpy, float64)."""
     import torch
