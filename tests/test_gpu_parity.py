@@ -1010,6 +1010,18 @@ def test_render_full_frame_C3(orc):
     assert c["n_flagged"] <= 1e-3 * c["n"], c
 
 
+def test_render_full_frame_C2(orc):
+    """Config C2 (10k primitives, 800x800, white background), every pixel against the
+    oracle's full frame."""
+    scene, cams, bg = synth.make_config("C2")
+    res = gpu_render(scene, cams, bg, sync_check=0, repeat=2)
+    img_o, fl, _ = orc.render_frame(scene, cams[0], bg)
+    c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+    print("C2 full frame", c)
+    assert c["max_unflagged"] <= TOL, c
+    assert c["n_flagged"] <= 1e-3 * c["n"], c
+
+
 def test_repeated_renders_bit_identical():
     """Races in K5's rings, the K5 -> K6w queue or the sort would show as frame-to-frame
     differences: 8 renders of the C3 frame and 3 of C5 (K6w busy) are bit-identical."""
