@@ -1022,6 +1022,20 @@ def test_render_full_frame_C2(orc):
     assert c["n_flagged"] <= 1e-3 * c["n"], c
 
 
+@pytest.mark.skipif(not __import__("os").environ.get("SNP_SLOW_TESTS"),
+                    reason="8 min of oracle time on 16 cores: set SNP_SLOW_TESTS=1 (result in profiles/r02_full_frames.md)")
+def test_render_full_frame_C5(orc):
+    """Config C5 (1M large-footprint primitives, 1920x1080; K6w busy), every pixel against
+    the oracle's full frame (~8 min on the GPU box's 16 host cores)."""
+    scene, cams, bg = synth.make_config("C5")
+    res = gpu_render(scene, cams, bg, sync_check=0, repeat=2)
+    img_o, fl, _ = orc.render_frame(scene, cams[0], bg)
+    c = compare(res["img"][0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+    print("C5 full frame", c, "flag kinds", np.bincount(fl.ravel(), minlength=8).tolist(), res["stats"])
+    assert c["max_unflagged"] <= TOL, c
+    assert c["n_flagged"] <= 3e-3 * c["n"], c
+
+
 def test_repeated_renders_bit_identical():
     """Races in K5's rings, the K5 -> K6w queue or the sort would show as frame-to-frame
     differences: 8 renders of the C3 frame and 3 of C5 (K6w busy) are bit-identical."""
