@@ -430,7 +430,24 @@ def run_c4(args):
         for i in range(args.warmup):
             sf.step(i)
     torch.cuda.synchronize()
+    # K5 roofline of this rank's shard: the snp_render stage (K5 + fallbacks) timed alone
+    # (CUDA events on the render stream, after a project + bin_sort of the same views)
+    rt = []
+    with torch.cuda.stream(st):
+        for _ in range(5):
+            snp.project(h, cams_c, st)
+            snp.bin_sort(h, opts, st)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            snp.render(h, opts, sf.bufs[0][:len(views)], st)
+            e1.record(st)
+            st.synchronize()
+            rt.append(e0.elapsed_time(e1))
     stats = snp.get_stats(h, st)
+    sm_mhz_max, _, peak_kind = _peaks()
+    roof = roofline_k5(stats, statistics.median(rt), sm_mhz_max)
+    roof["peak_kind"] = peak_kind
+    roof["scope"] = f"rank 0's {len(views)} views in one snp_render"
     # render only
     render_ms, clocks = _timed(args, lambda i: sf.render(i), st, ws, dev)
     # render + gather (the gather of step i overlaps the render of step i + 1); the timed
@@ -486,6 +503,7 @@ def run_c4(args):
                                       "stream, overlapped with the next step's render); max over ranks"},
             "bit_identical_to_single_gpu": bit_identical,
             "workload_stats_rank0": stats,
+            "roofline": roof,
             "e2e": e2e,
             "gpu_launches": (8 + 5) * args.steps,
             "clocks": clocks,
