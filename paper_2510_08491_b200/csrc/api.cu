@@ -85,6 +85,8 @@ struct snp_scene_s {
     DevBuf<uint32_t> bw_skip;          // K7: composited hits K5's grad mode already emitted, per pixel
     DevBuf<float> bw_fwd;              // K7: the forward image when the caller does not pass it
     DevBuf<GradEntry> grad_entries;    // K5 grad mode -> K7f
+    DevBuf<int32_t> grad_fill;         //   entries used per chunk
+    DevBuf<float4> gc_acc;             // K7f, primitive colour mode: summed dL/dc per (view, primitive)
     float *grad_w_t = nullptr;       // where snp_render_backward adds dL/dW_t (caller-owned, device)
     bool temporal = false;
     // binning
@@ -688,19 +690,32 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
         if (r != SNP_OK) return r;
         fwd = s->bw_fwd.p;
     }
-    // K5 in grad mode: one GradEntry per composited hit (12 per pixel of a camera batch
-    // before the path falls back to the per-pixel K7 for every pixel)
-    const int64_t cap = 12 * npix_batch;
-    SNP_CUDA(s->grad_entries.ensure((size_t)std::max<int64_t>(1, cap)));
+    // K5 in grad mode: one GradEntry per composited hit, in per-warp chunks (12 per pixel
+    // of a camera batch, plus a partly filled chunk per resident consumer warp, before the
+    // path falls back to the per-pixel K7 for every pixel)
+    int dev_sms = 148;
+    SNP_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device));
+    const int64_t chunks = (12 * npix_batch + kGradChunk - 1) / kGradChunk + 2 * 8 * (int64_t)dev_sms;
+    SNP_CUDA(s->grad_entries.ensure((size_t)(chunks * kGradChunk)));
+    SNP_CUDA(s->grad_fill.ensure((size_t)chunks));
     RenderArgs a = render_args(s, opts);
     a.bw_queue = s->bw_queue.p;
     a.bw_skip = s->bw_skip.p;
     a.grad_in = reinterpret_cast<const float4 *>(grad_rgba);
     a.fwd = reinterpret_cast<const float4 *>(fwd);
     a.grad_entries = s->grad_entries.p;
-    a.grad_cap = cap;
+    a.grad_fill = s->grad_fill.p;
+    a.grad_chunks = chunks;
+    if (!a.colour_ray) {
+        int nv_max = 1;
+        for (const CamBatch &cb : s->cams) nv_max = std::max(nv_max, cb.nv);
+        SNP_CUDA(s->gc_acc.ensure((size_t)nv_max * (size_t)std::max<int64_t>(1, s->n)));
+        a.gc_acc = s->gc_acc.p;
+    }
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     for (size_t k = 0; k < s->cams.size(); ++k) {
+        if (!a.colour_ray)
+            SNP_CUDA(cudaMemsetAsync(a.gc_acc, 0, (size_t)s->cams[k].nv * (size_t)s->n * sizeof(float4), st));
         SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdQueue, 0, sizeof(unsigned long long), st));
         SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGradEntries, 0, 2 * sizeof(unsigned long long), st));
         a.tile_order = s->tile_order.p + k * order_stride;
@@ -834,6 +849,8 @@ snp_status snp_destroy(snp_scene s) {
     s->bw_skip.release();
     s->bw_fwd.release();
     s->grad_entries.release();
+    s->grad_fill.release();
+    s->gc_acc.release();
     s->adam_v.release();
     s->keys0.release();
     s->keys1.release();

@@ -294,13 +294,15 @@ __device__ __forceinline__ void sh_basis_f(float x, float y, float z, float Y[16
     Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
 }
 
-// Every parameter gradient of one composited hit (dL/dI = gI, dL/dc = gc).
-template <int N, bool kRay>
-__device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 *rec, const Ray &ray, uint32_t id,
-                                              float gI, const float gc[3], float omega, const BackwardGrads &gr,
-                                              float xi_t) {
+// The colour part of the gradients for dL/dc = gc: the SH coefficients (dc/dsh_lm =
+// Y_lm(dir) on unclamped channels -- gc is already 0 on clamped ones) and, in primitive
+// colour mode, mu through dir = (mu - C) / |mu - C|.  Linear in gc, so in primitive mode
+// (dir fixed per view and primitive) the K5 path calls it once per (view, primitive) with
+// the summed gc.
+template <bool kRay>
+__device__ __forceinline__ void colour_grads(const RenderArgs &a, const float4 *rec, const Ray &ray, uint32_t id,
+                                             const float gc[3], const BackwardGrads &gr) {
     const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
-    hit_grad<N>(rec, ray, gI, omega, id, a, gr, xi_t);
     // SH colour: dc/dsh_lm = Y_lm(dir) (unclamped channels)
     float dxv, dyv, dzv;
     if (kRay) {
@@ -357,6 +359,15 @@ __device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 
             atomicAdd(gr.mu + 3 * (size_t)id + 2, (gd[2] - dzv * dd) / nrm);
         }
     }
+}
+
+// Every parameter gradient of one composited hit (dL/dI = gI, dL/dc = gc).
+template <int N, bool kRay>
+__device__ __forceinline__ void hit_all_grads(const RenderArgs &a, const float4 *rec, const Ray &ray, uint32_t id,
+                                              float gI, const float gc[3], float omega, const BackwardGrads &gr,
+                                              float xi_t) {
+    hit_grad<N>(rec, ray, gI, omega, id, a, gr, xi_t);
+    colour_grads<kRay>(a, rec, ray, id, gc, gr);
 }
 
 // Processes the first `cnt` (<= 32) entries of the warp's queue, one per lane, and moves
@@ -632,9 +643,11 @@ __global__ void __launch_bounds__(128) k_grad_entries(RenderArgs a, CamBatch cb,
     __shared__ DevCam s_cam[kCamsPerLaunch];
     for (int i = threadIdx.x; i < cb.nv; i += blockDim.x) s_cam[i] = cb.cams[i];
     __syncthreads();
-    int64_t n = (int64_t)a.counters[kCntGradEntries];
-    if (n > a.grad_cap) n = a.grad_cap;
+    int64_t nc = (int64_t)a.counters[kCntGradEntries];
+    if (nc > a.grad_chunks) nc = a.grad_chunks;
+    const int64_t n = nc * kGradChunk;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if ((int)(i & (kGradChunk - 1)) >= a.grad_fill[i / kGradChunk]) continue;
         const GradEntry e = ent[i];
         const int vloc = (int)(e.pix >> 24);
         SNP_CHECK(vloc < cb.nv && (int64_t)e.id < a.n);
@@ -643,8 +656,33 @@ __global__ void __launch_bounds__(128) k_grad_entries(RenderArgs a, CamBatch cb,
         const int y = (int)(p / (uint32_t)cam.W), x = (int)(p - (uint32_t)y * (uint32_t)cam.W);
         const Ray ray = make_ray(cam, x, y);
         const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + e.id) * rec_f4(N);
-        const float gc[3] = {e.gc0, e.gc1, e.gc2};
-        hit_all_grads<N, kRay>(a, rec, ray, e.id, e.gI, gc, omega, gr, cam.xi_t);
+        if (kRay) {
+            const float gc[3] = {e.gc0, e.gc1, e.gc2};
+            hit_all_grads<N, kRay>(a, rec, ray, e.id, e.gI, gc, omega, gr, cam.xi_t);
+        } else {   // colour part per (view, primitive) in k_colour_finalize
+            hit_grad<N>(rec, ray, e.gI, omega, e.id, a, gr, cam.xi_t);
+            if (e.gc0 != 0.f || e.gc1 != 0.f || e.gc2 != 0.f)
+                atomicAdd(a.gc_acc + (size_t)vloc * a.n + e.id, make_float4(e.gc0, e.gc1, e.gc2, 0.f));
+        }
+    }
+}
+
+// Primitive colour mode: the colour gradients of every (view, primitive) from the summed
+// dL/dc of its composited hits (colour_grads is linear in dL/dc).
+template <int N>
+__global__ void __launch_bounds__(128) k_colour_finalize(RenderArgs a, CamBatch cb, BackwardGrads gr) {
+    if (a.counters[kCntGradOverflow]) return;
+    const int64_t total = (int64_t)cb.nv * a.n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 g = a.gc_acc[i];
+        if (g.x == 0.f && g.y == 0.f && g.z == 0.f) continue;
+        const int64_t vloc = i / a.n;
+        const uint32_t id = (uint32_t)(i - vloc * a.n);
+        // (a composited primitive is visible in the view: its record exists)
+        const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + id) * rec_f4(N);
+        const float gc[3] = {g.x, g.y, g.z};
+        const Ray unused{0, 0, 1, 0, 0, 0, 0, 0};
+        colour_grads<false>(a, rec, unused, id, gc, gr);
     }
 }
 
@@ -655,6 +693,7 @@ cudaError_t launch_grad_entries_n(const RenderArgs &a, const CamBatch &cb, const
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     k_grad_entries<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, a.grad_entries, g, omega);
+    if (!kRay) k_colour_finalize<N><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, g);
     return cudaGetLastError();
 }
 

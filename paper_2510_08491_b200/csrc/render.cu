@@ -151,11 +151,10 @@ struct PixelState {
 // dL/d(out) G and forward result F, and the warp's shared-memory entry staging.
 struct GradCtx {
     float4 G, F;
-    GradEntry *st;        // this warp's staging (kGradStage entries)
+    GradEntry *chunk;     // this warp's current chunk of a.grad_entries (nullptr: none)
     int *cnt;             // its fill count (shared atomics)
     uint32_t pix;         // view within the batch << 24 | y * W + x
 };
-constexpr int kGradStage = kPend * 32;   // one emission call of a warp: at most 16 hits per lane
 
 template <int N, bool kRay, bool kGrad = false>
 __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, float L, float t_floor,
@@ -205,7 +204,8 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
                 e.gc0 = rgb.y > 0.f ? w * G.x : 0.f;
                 e.gc1 = rgb.z > 0.f ? w * G.y : 0.f;
                 e.gc2 = rgb.w > 0.f ? w * G.z : 0.f;
-                gx->st[atomicAdd(gx->cnt, 1)] = e;
+                const int slot = atomicAdd(gx->cnt, 1);
+                if (gx->chunk) gx->chunk[slot] = e;
             }
         }
         ps.T *= (1.0f - kap);
@@ -257,16 +257,16 @@ __device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimi
 }
 
 // kGrad: the backward's forward traversal (no image output): every composited hit of a
-// pixel with a nonzero dL/d(out) becomes a GradEntry (staged per warp in shared memory
-// after Smem, flushed to a.grad_entries); an overflowing pixel is queued for K7 with its
-// count of already emitted hits.  One CTA per SM (registers and the staging).
+// pixel with a nonzero dL/d(out) becomes a GradEntry, written straight to the warp's
+// current chunk of a.grad_entries (kGradChunk entries, one global atomic per chunk; fill
+// counts in a.grad_fill); an overflowing pixel is queued for K7 with its count of already
+// emitted hits.  Two CTAs per SM, as in the forward.
 template <int N, bool kRay, bool kEager, bool kGrad = false>
-__global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a, CamBatch cb) {
+__global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
     constexpr int kStages = Cfg<N>::kStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
-    GradEntry *gstage = reinterpret_cast<GradEntry *>(smem_raw + sizeof(Smem<N>));
-    int *gcount = reinterpret_cast<int *>(gstage + (kGrad ? kConsumers * kGradStage : 0));
+    int *gcount = reinterpret_cast<int *>(smem_raw + sizeof(Smem<N>));
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     const int stripe_tiles = a.tiles_x * a.stripe_rows;
@@ -423,8 +423,31 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
     float pxf = 0.f, pyf = 0.f, bx0 = 0.f, by0 = 0.f;
     PixelState ps{1.f, 0.f, 0.f, 0.f, true, false, 0u};
     Pending pd{0, 0, 0.f, 0u, false};
-    GradCtx gx{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), gstage + wid * kGradStage,
-               gcount + wid, 0u};
+    GradCtx gx{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), nullptr, gcount + wid, 0u};
+    int64_t gchunk = -1;   // (kGrad) index of gx.chunk; -2: the chunk table is exhausted
+    // (kGrad) switch to a fresh chunk when this emission call (need entries at most)
+    // might not fit: the old one's fill goes to a.grad_fill (warp-uniform)
+    auto grad_reserve = [&](int need) {
+        __syncwarp();
+        const int c = *gx.cnt;
+        SNP_CHECK(c >= 0 && c <= kGradChunk);
+        if (need == 0 || (gchunk >= 0 && c + need <= kGradChunk)) return;
+        long long k = -2;
+        if (lane == 0) {
+            if (gchunk >= 0) a.grad_fill[gchunk] = c;
+            if (gchunk != -2) {
+                k = (long long)atomicAdd(a.counters + kCntGradEntries, 1ull);
+                if (k >= a.grad_chunks) {
+                    atomicExch(a.counters + kCntGradOverflow, 1ull);
+                    k = -2;
+                }
+            }
+            *gx.cnt = 0;
+        }
+        gchunk = __shfl_sync(0xffffffffu, k, 0);
+        gx.chunk = gchunk >= 0 ? a.grad_entries + gchunk * kGradChunk : nullptr;
+        __syncwarp();
+    };
     int64_t gpi = 0;   // (kGrad) pixel index within the camera batch
 
     auto finish_tile = [&]() {   // write this warp's pixels; count the warp as done with the tile
@@ -667,7 +690,9 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
                 // L[jn] bounds it.  Default: only when the pending list runs nearly full;
                 // kEager: after every exact round -- shorter pending lists (fewer K6
                 // pixels), earlier termination; chosen per scene from the overflow rate
-                if (!ps.done && (batch_end || pd.n > (kEager ? 0 : plimit - 4))) {
+                const bool do_emit = !ps.done && (batch_end || pd.n > (kEager ? 0 : plimit - 4));
+                if (kGrad) grad_reserve(__reduce_add_sync(0xffffffffu, do_emit ? (uint32_t)pd.n : 0u));
+                if (do_emit) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
                     ++ins_ecalls;
@@ -679,23 +704,6 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
 #ifdef SNP_INSTRUMENT
                     ins_emit += clock64() - _e0;
 #endif
-                }
-                if (kGrad) {   // flush the warp's staged gradient entries (one global atomic)
-                    __syncwarp();
-                    const int c = *gx.cnt;
-                    SNP_CHECK(c >= 0 && c <= kGradStage);
-                    if (c) {
-                        unsigned long long base = 0;
-                        if (lane == 0) base = atomicAdd(a.counters + kCntGradEntries, (unsigned long long)c);
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        for (int i = lane; i < c; i += 32)
-                            if ((int64_t)(base + i) < a.grad_cap) a.grad_entries[base + i] = gx.st[i];
-                        if (lane == 0 && (int64_t)(base + c) > a.grad_cap)
-                            atomicExch(a.counters + kCntGradOverflow, 1ull);
-                        __syncwarp();
-                        if (lane == 0) *gx.cnt = 0;
-                        __syncwarp();
-                    }
                 }
                 if (batch_end) break;
             }
@@ -738,6 +746,8 @@ __global__ void __launch_bounds__(kThreads, kGrad ? 1 : 2) k_render(RenderArgs a
 #endif
     __syncwarp();
     if (kGrad) {   // (the backward's traversal leaves the forward's statistics alone)
+        __syncwarp();
+        if (lane == 0 && gchunk >= 0) a.grad_fill[gchunk] = *gx.cnt;
         warp_exit();
         return;
     }
@@ -1311,7 +1321,7 @@ cudaError_t launch_fallback_w(const RenderArgs &a, const CamBatch *cams, int n_b
 namespace {
 template <int N, bool kRay>
 cudaError_t launch_render_grad_n(const RenderArgs &a, const CamBatch &cams, cudaStream_t st) {
-    const int smem = (int)(sizeof(Smem<N>) + (size_t)kConsumers * kGradStage * sizeof(GradEntry) + 64);
+    const int smem = (int)(sizeof(Smem<N>) + 64);
     static int res[kMaxDevices] = {};
     int dev = 0;
     cudaGetDevice(&dev);

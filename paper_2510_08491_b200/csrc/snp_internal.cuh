@@ -121,7 +121,7 @@ enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3
                kCntGraze = 48,          // cumulative until the debug readback
                kCntBwdQueue2 = 49,      // K7: pixels for its second (2048-hit) pass
                kCntBwdQueue3 = 50,      // K7: pixels for the global-memory pass
-               kCntGradEntries = 51,    // K5 grad mode: gradient entries emitted
+               kCntGradEntries = 51,    // K5 grad mode: entry chunks reserved
                kCntGradOverflow = 52,   // K5 grad mode: the entry buffer overflowed
                kNumCounters = 56 };     // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
@@ -193,6 +193,10 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
 
 // K5 grad mode (the backward's forward traversal): one entry per composited hit, its
 // dL/dI and dL/dc, from which K7f computes the parameter gradients
+// K5 grad mode: a consumer warp writes its entries to a chunk of this many, reserved with
+// one global atomic (>= the 32 x kPend entries one emission call can produce)
+constexpr int kGradChunk = 1024;
+
 struct GradEntry {
     uint32_t pix;      // view within the camera batch << 24 | y * W + x
     uint32_t id;       // primitive
@@ -212,8 +216,10 @@ struct RenderArgs {
     uint32_t *bw_skip;             // [V*H*W] composited hits of a pixel K5's grad mode already emitted
     const float4 *grad_in;         // K5 grad mode: dL/d(out RGBA) [V][H][W]
     const float4 *fwd;             // K5 grad mode: the forward's out RGBA [V][H][W]
-    GradEntry *grad_entries;       // K5 grad mode: entry buffer
-    int64_t grad_cap;
+    GradEntry *grad_entries;       // K5 grad mode: entry buffer, grad_chunks chunks of kGradChunk
+    int32_t *grad_fill;            //   entries used per chunk
+    int64_t grad_chunks;
+    float4 *gc_acc;                // K7f, primitive colour mode: [batch views][n] summed dL/dc
     int32_t tiles_x, tiles_y, tiles_per_view;
     int32_t tile_bits;
     int32_t row_begin, row_stride, stripe_rows;

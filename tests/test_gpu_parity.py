@@ -893,13 +893,15 @@ def test_eager_emission_rule(orc, monkeypatch):
     assert c["max_unflagged"] <= TOL and c["n_flagged"] <= 0.02 * c["n"], c
 
 
-@pytest.mark.parametrize("n_hits", [600, 2600])
-def test_backward_long_hit_lists(orc, n_hits):
-    """K7's big-capacity passes: every pixel of the deep-overlap scene has 600 hits (more
-    than the first pass holds: the 2048-hit shared-memory pass) or 2600 (more than that:
-    the global-memory pass), none is skipped, and sampled W2/b2/centre gradients match
-    central differences of the oracle."""
+@pytest.mark.parametrize("n_hits,legacy", [(600, 1), (2600, 1), (2600, 0)])
+def test_backward_long_hit_lists(orc, monkeypatch, n_hits, legacy):
+    """K7's big-capacity passes (legacy = 1: the per-pixel K7 on every pixel): every pixel
+    of the deep-overlap scene has 600 hits (more than the first pass holds: the 2048-hit
+    shared-memory pass) or 2600 (more than that: the global-memory pass), none is skipped,
+    and sampled W2/b2/centre gradients match central differences of the oracle; legacy =
+    0: the same through K5's gradient mode (2600 entries per pixel) and K7f."""
     import torch
+    monkeypatch.setenv("SNP_BWD_LEGACY", str(legacy))
     from paper_2510_08491_b200 import snp
     from gpu_util import torch_scene
     scene = _deep_scene(n_hits)
@@ -915,11 +917,13 @@ def test_backward_long_hit_lists(orc, n_hits):
         snp.render_backward(h, opts, torch.from_numpy(G).cuda(), grads)
         torch.cuda.synchronize()
         dc = snp.get_debug_counters(h, 56)
-        # 600+ composited hits per pixel overflow K5's gradient-entry buffer (12 per pixel):
-        # the per-pixel K7 then differentiates every pixel, past its first (256-hit) pass,
-        # and for 2600 hits past its second (2048)
-        assert dc[52] == 1 and dc[49] == 32 * 24, (dc[52], dc[49])
-        assert dc[50] == (32 * 24 if n_hits > 2048 else 0), dc[50]
+        if legacy:
+            # the per-pixel K7 differentiates every pixel past its first (256-hit) pass,
+            # and for 2600 hits past its second (2048)
+            assert dc[49] == 32 * 24, dc[49]
+            assert dc[50] == (32 * 24 if n_hits > 2048 else 0), dc[50]
+        else:   # all through K5 + K7f: no entry overflow, no per-pixel K7 pass
+            assert dc[52] == 0 and dc[49] == 0 and dc[51] * 1024 >= 32 * 24 * n_hits, (dc[52], dc[49], dc[51])
         assert snp.get_stats(h)["backward_skipped"] == 0              # none skipped
         g = {f: v.cpu().numpy().astype(np.float64) for f, v in grads.items()}
     finally:
