@@ -86,6 +86,11 @@ struct snp_scene_s {
     DevBuf<float> bw_fwd;              // K7: the forward image when the caller does not pass it
     DevBuf<GradEntry> grad_entries;    // K5 grad mode -> K7f
     DevBuf<int32_t> grad_fill;         //   entries used per chunk
+    DevBuf<uint32_t> grad_keys;        //   per slot: vloc * n + primitive
+    DevBuf<uint32_t> grad_count;       //   entries per key -> offsets (K7s counting sort)
+    DevBuf<uint32_t> es_bsum;
+    DevBuf<uint32_t> es_sorted;
+    DevBuf<unsigned long long> es_cnt;
     DevBuf<float4> gc_acc;             // K7f, primitive colour mode: summed dL/dc per (view, primitive)
     float *grad_w_t = nullptr;       // where snp_render_backward adds dL/dW_t (caller-owned, device)
     bool temporal = false;
@@ -679,7 +684,7 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
         RenderArgs a = render_args(s, opts);
         a.bw_queue = s->bw_queue.p;
         for (const CamBatch &cb : s->cams)
-            SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, s->bw_scratch.p, false, st));
+            SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, s->bw_scratch.p, false, nullptr, st));
         return SNP_OK;
     }
     // the forward result the gradients refer to (the caller's, or rendered here)
@@ -706,9 +711,28 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
     a.grad_entries = s->grad_entries.p;
     a.grad_fill = s->grad_fill.p;
     a.grad_chunks = chunks;
+    // K7s (default; SNP_K7F_UNSORTED=1: K7f in slot order, A/B)
+    const bool unsorted = [] {
+        const char *e = std::getenv("SNP_K7F_UNSORTED");
+        return e && std::atoi(e) != 0;
+    }();
+    EntrySort es{};
+    int nv_max = 1;
+    for (const CamBatch &cb : s->cams) nv_max = std::max(nv_max, cb.nv);
+    if (!unsorted) {
+        const int64_t slots = chunks * kGradChunk, nk = (int64_t)nv_max * std::max<int64_t>(1, s->n);
+        SNP_CUDA(s->grad_keys.ensure((size_t)slots));
+        SNP_CUDA(s->grad_count.ensure((size_t)nk));
+        SNP_CUDA(s->es_bsum.ensure((size_t)((nk + 4095) / 4096)));
+        SNP_CUDA(s->es_sorted.ensure((size_t)slots));
+        SNP_CUDA(s->es_cnt.ensure(64));
+        a.grad_keys = s->grad_keys.p;
+        a.grad_count = s->grad_count.p;
+        es.bsum = s->es_bsum.p;
+        es.sorted = s->es_sorted.p;
+        es.cnt = s->es_cnt.p;
+    }
     if (!a.colour_ray) {
-        int nv_max = 1;
-        for (const CamBatch &cb : s->cams) nv_max = std::max(nv_max, cb.nv);
         SNP_CUDA(s->gc_acc.ensure((size_t)nv_max * (size_t)std::max<int64_t>(1, s->n)));
         a.gc_acc = s->gc_acc.p;
     }
@@ -716,12 +740,14 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
     for (size_t k = 0; k < s->cams.size(); ++k) {
         if (!a.colour_ray)
             SNP_CUDA(cudaMemsetAsync(a.gc_acc, 0, (size_t)s->cams[k].nv * (size_t)s->n * sizeof(float4), st));
+        if (a.grad_count)
+            SNP_CUDA(cudaMemsetAsync(a.grad_count, 0, (size_t)s->cams[k].nv * (size_t)s->n * sizeof(uint32_t), st));
         SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdQueue, 0, sizeof(unsigned long long), st));
         SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGradEntries, 0, 2 * sizeof(unsigned long long), st));
         a.tile_order = s->tile_order.p + k * order_stride;
         if (s->n > 0) SNP_CUDA(launch_render_grad(a, s->cams[k], st));
         // K7f over the entries, then the per-pixel K7 for the pixels K5 queued
-        SNP_CUDA(launch_backward(a, s->cams[k], grad_rgba, g, s->omega, s->bw_scratch.p, true, st));
+        SNP_CUDA(launch_backward(a, s->cams[k], grad_rgba, g, s->omega, s->bw_scratch.p, true, unsorted ? nullptr : &es, st));
     }
     return SNP_OK;
 }
@@ -850,6 +876,11 @@ snp_status snp_destroy(snp_scene s) {
     s->bw_fwd.release();
     s->grad_entries.release();
     s->grad_fill.release();
+    s->grad_keys.release();
+    s->grad_count.release();
+    s->es_bsum.release();
+    s->es_sorted.release();
+    s->es_cnt.release();
     s->gc_acc.release();
     s->adam_v.release();
     s->keys0.release();

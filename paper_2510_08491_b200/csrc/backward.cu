@@ -24,6 +24,8 @@
 // than that by one-warp CTAs whose arrays live in a global scratch (kBwHugeHits each);
 // only beyond that (tile lists of more than 16384 hits per ray) is a pixel skipped,
 // counted in counters[kCntBwdSkipped] (reset by every call, reported by snp_get_stats).
+#include <algorithm>
+
 #include "hit.cuh"
 #include "snp_internal.cuh"
 
@@ -58,9 +60,21 @@ struct BwSmem {
     float q_gc[kBwWarps][3][kBwQueue];
 };
 
+__device__ __forceinline__ void add1(float *p, float a) {
+#ifdef SNP_AB_NOATOM
+    asm volatile("" ::"f"(a), "l"(p));
+#else
+    atomicAdd(p, a);
+#endif
+}
+
 // Four consecutive gradient entries: one 16-byte vector atomic (red.global.add.v4.f32,
 // sm_90+) when the arrays are 16-byte aligned (gr.vec), else four scalar atomics.
 __device__ __forceinline__ void add4(float *p, float a, float b, float c, float d, bool vec) {
+#ifdef SNP_AB_NOATOM   // A/B: the arithmetic without the gradient atomics
+    asm volatile("" ::"f"(a), "f"(b), "f"(c), "f"(d), "l"(p));
+    return;
+#endif
     if (vec) {
         atomicAdd(reinterpret_cast<float4 *>(p), make_float4(a, b, c, d));
     } else {
@@ -123,9 +137,11 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     const float *s3 = ra.scales + 3 * (size_t)prim;
     const float sv[3] = {s3[0], s3[1], s3[2]};
     const int imax = (sv[1] > sv[0]) ? ((sv[2] > sv[1]) ? 2 : 1) : ((sv[2] > sv[0]) ? 2 : 0);
-    const float smax = sv[imax];
+    // (reciprocals once: an IEEE division per use takes its slow path on tiny adjoints)
+    const float isv[3] = {1.0f / sv[0], 1.0f / sv[1], 1.0f / sv[2]};
+    const float ismax = isv[imax];
     const uint32_t wbase = (uint32_t)N * prim;
-    const float s1 = omega / smax;
+    const float s1 = omega * ismax;
     float sumc = mh.w;                    // sum_k W2_k cos(phi_k) S_k + b2
     float gdt = 0.f, gtm = 0.f, gsmax = 0.f;
     float gp[3] = {0.f, 0.f, 0.f};        // dI/dp through the phases
@@ -159,7 +175,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
             const float gw[3] = {fmaf(coef, fmaf(tm, d[0], p[0]), chs * d[0]),
                                  fmaf(coef, fmaf(tm, d[1], p[1]), chs * d[1]),
                                  fmaf(coef, fmaf(tm, d[2], p[2]), chs * d[2])};
-            gsmax -= (gw[0] * u.x + gw[1] * u.y + gw[2] * u.z) / smax;
+            gsmax = fmaf(-(gw[0] * u.x + gw[1] * u.y + gw[2] * u.z), ismax, gsmax);
             a_w2[uu] = gI * dt * cs * S;
             a_b1[uu] = gI * omega * coef;
             a_w1[3 * uu + 0] = gI * s1 * gw[0];
@@ -175,7 +191,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
         for (int v = 0; v < 3; ++v)
             add4(gr.w1 + 3 * k0 + 4 * v, a_w1[4 * v], a_w1[4 * v + 1], a_w1[4 * v + 2], a_w1[4 * v + 3], gr.vec);
     }
-    atomicAdd(gr.b2 + prim, gI * dt);
+    add1(gr.b2 + prim, gI * dt);
     if (!gr.mu) return;
     // ---- geometry
     const float G_dt = gI * fmaf(dt, gdt, sumc), G_tm = gI * dt * gtm;
@@ -184,7 +200,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     float G_tc = (clip_lo ? -G_tlo : 0.f) + (clip_hi ? -G_thi : 0.f);
     float G_ts = G_t0 + G_t1;
     const float G_hc = G_t1 - G_t0;
-    const float G_Q = G_hc * hc / (2.0f * Q);
+    const float G_Q = G_hc * hc * (0.5f / Q);
     float G_A = -G_hc * hc * 0.5f * iA;
     float G_a[3], G_b[3];
 #pragma unroll
@@ -212,9 +228,9 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
         }
     G_tc = fmaf(Gp[2], d[2], fmaf(Gp[1], d[1], fmaf(Gp[0], d[0], G_tc)));
     // m = mu - C: p = t_c d - m, t_c = d.m
-    atomicAdd(gr.mu + 3 * (size_t)prim + 0, fmaf(d[0], G_tc, -Gp[0]));
-    atomicAdd(gr.mu + 3 * (size_t)prim + 1, fmaf(d[1], G_tc, -Gp[1]));
-    atomicAdd(gr.mu + 3 * (size_t)prim + 2, fmaf(d[2], G_tc, -Gp[2]));
+    add1(gr.mu + 3 * (size_t)prim + 0, fmaf(d[0], G_tc, -Gp[0]));
+    add1(gr.mu + 3 * (size_t)prim + 1, fmaf(d[1], G_tc, -Gp[1]));
+    add1(gr.mu + 3 * (size_t)prim + 2, fmaf(d[2], G_tc, -Gp[2]));
     // Wh[k][j] = R[j][k] / s_k
     float G_s[3], G_R[9];
 #pragma unroll
@@ -223,17 +239,18 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             acc = fmaf(G_Wh[3 * k + j], Wh[3 * k + j], acc);
-            G_R[3 * j + k] = G_Wh[3 * k + j] / sv[k];
+            G_R[3 * j + k] = G_Wh[3 * k + j] * isv[k];
         }
-        G_s[k] = -acc / sv[k];
+        G_s[k] = -acc * isv[k];
     }
     G_s[imax] += gI * gsmax;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) atomicAdd(gr.s + 3 * (size_t)prim + k, G_s[k]);
+    for (int k = 0; k < 3; ++k) add1(gr.s + 3 * (size_t)prim + k, G_s[k]);
     // R(q^), q^ = q / |q| (w, x, y, z)
     const float *q4 = ra.rotations + 4 * (size_t)prim;
     const float qn = sqrtf(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
-    const float w = q4[0] / qn, x = q4[1] / qn, y = q4[2] / qn, z = q4[3] / qn;
+    const float iqn = 1.0f / qn;
+    const float w = q4[0] * iqn, x = q4[1] * iqn, y = q4[2] * iqn, z = q4[3] * iqn;
     const float gw_ = 2.0f * (-z * G_R[1] + y * G_R[2] + z * G_R[3] - x * G_R[5] - y * G_R[6] + x * G_R[7]);
     const float gx_ = 2.0f * (y * G_R[1] + z * G_R[2] + y * G_R[3] - 2.0f * x * G_R[4] - w * G_R[5] + z * G_R[6] +
                               w * G_R[7] - 2.0f * x * G_R[8]);
@@ -242,8 +259,8 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     const float gz_ = 2.0f * (-2.0f * z * G_R[0] - w * G_R[1] + x * G_R[2] + w * G_R[3] - 2.0f * z * G_R[4] +
                               y * G_R[5] + x * G_R[6] + y * G_R[7]);
     const float dotq = w * gw_ + x * gx_ + y * gy_ + z * gz_;
-    add4(gr.q + 4 * (size_t)prim, (gw_ - w * dotq) / qn, (gx_ - x * dotq) / qn, (gy_ - y * dotq) / qn,
-         (gz_ - z * dotq) / qn, gr.vec);
+    add4(gr.q + 4 * (size_t)prim, (gw_ - w * dotq) * iqn, (gx_ - x * dotq) * iqn, (gy_ - y * dotq) * iqn,
+         (gz_ - z * dotq) * iqn, gr.vec);
 }
 
 // d Y_lm / d dir for the basis of sh_basis_f (rows: coefficient, columns: x, y, z)
@@ -353,10 +370,10 @@ __device__ __forceinline__ void colour_grads(const RenderArgs &a, const float4 *
         const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
         const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
         if (nrm > 0.f) {
-            const float dd = dxv * gd[0] + dyv * gd[1] + dzv * gd[2];
-            atomicAdd(gr.mu + 3 * (size_t)id + 0, (gd[0] - dxv * dd) / nrm);
-            atomicAdd(gr.mu + 3 * (size_t)id + 1, (gd[1] - dyv * dd) / nrm);
-            atomicAdd(gr.mu + 3 * (size_t)id + 2, (gd[2] - dzv * dd) / nrm);
+            const float dd = dxv * gd[0] + dyv * gd[1] + dzv * gd[2], inrm = 1.0f / nrm;
+            atomicAdd(gr.mu + 3 * (size_t)id + 0, (gd[0] - dxv * dd) * inrm);
+            atomicAdd(gr.mu + 3 * (size_t)id + 1, (gd[1] - dyv * dd) * inrm);
+            atomicAdd(gr.mu + 3 * (size_t)id + 2, (gd[2] - dzv * dd) * inrm);
         }
     }
 }
@@ -543,11 +560,11 @@ __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBat
                 }
                 const float Uk[3] = {U0 + sfx[0] - w[0], U1 + sfx[1] - w[1], U2 + sfx[2] - w[2]};
                 if (valid) {
-                    const float om = fmaxf(1.0f - kp, 1e-20f);
-                    float dk = G.w * Tend / om;
+                    const float iom = 1.0f / fmaxf(1.0f - kp, 1e-20f);
+                    float dk = G.w * Tend * iom;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {
-                        dk = fmaf(gr_[ch], Tk * c[ch] - Uk[ch] / om, dk);
+                        dk = fmaf(gr_[ch], fmaf(-Uk[ch], iom, Tk * c[ch]), dk);
                         sm.gc[wid][k][ch] = c[ch] > 0.f ? Tk * kp * gr_[ch] : 0.f;
                     }
                     sm.gI[wid][k] = kp > 0.f ? dk * (1.0f - kp) : 0.f;
@@ -646,23 +663,460 @@ __global__ void __launch_bounds__(128) k_grad_entries(RenderArgs a, CamBatch cb,
     int64_t nc = (int64_t)a.counters[kCntGradEntries];
     if (nc > a.grad_chunks) nc = a.grad_chunks;
     const int64_t n = nc * kGradChunk;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        if ((int)(i & (kGradChunk - 1)) >= a.grad_fill[i / kGradChunk]) continue;
-        const GradEntry e = ent[i];
-        const int vloc = (int)(e.pix >> 24);
-        SNP_CHECK(vloc < cb.nv && (int64_t)e.id < a.n);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    auto used = [&](int64_t j) { return j < n && (int)(j & (kGradChunk - 1)) < a.grad_fill[j / kGradChunk]; };
+    // software pipeline: the next entry is loaded, and its record prefetched into L1,
+    // while this one is differentiated
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = used(i);
+    GradEntry e{};
+    if (ok) e = ent[i];
+    for (; i < n; i += stride) {
+        const bool okn = used(i + stride);
+        GradEntry en{};
+        if (okn) en = ent[i + stride];
+        if (ok) {
+            const int vloc = (int)(e.pix >> 24);
+            SNP_CHECK(vloc < cb.nv && (int64_t)e.id < a.n);
+            const DevCam &cam = s_cam[vloc];
+            const uint32_t p = e.pix & 0xffffffu;
+            const int y = (int)(p / (uint32_t)cam.W), x = (int)(p - (uint32_t)y * (uint32_t)cam.W);
+            const Ray ray = make_ray(cam, x, y);
+            const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + e.id) * rec_f4(N);
+            if (okn) {
+                const char *rn = reinterpret_cast<const char *>(
+                    a.records + ((size_t)(cb.view0 + (en.pix >> 24)) * (size_t)a.n + en.id) * rec_f4(N));
+#pragma unroll
+                for (int b = 0; b < 16 * rec_f4(N); b += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rn + b));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.scales + 3 * (size_t)en.id));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rotations + 4 * (size_t)en.id));
+            }
+            if (kRay) {
+                const float gc[3] = {e.gc0, e.gc1, e.gc2};
+                hit_all_grads<N, kRay>(a, rec, ray, e.id, e.gI, gc, omega, gr, cam.xi_t);
+            } else {   // colour part per (view, primitive) in k_colour_finalize
+                hit_grad<N>(rec, ray, e.gI, omega, e.id, a, gr, cam.xi_t);
+                if (e.gc0 != 0.f || e.gc1 != 0.f || e.gc2 != 0.f)
+                    atomicAdd(a.gc_acc + (size_t)vloc * a.n + e.id, make_float4(e.gc0, e.gc1, e.gc2, 0.f));
+            }
+        }
+        e = en;
+        ok = okn;
+    }
+}
+
+// ---- K7s: K7f over the entries grouped by (view, primitive).
+// The gradient atomics are what bound K7f (an A/B without them: 587 -> 94 us at C3):
+// every entry adds ~50 values to its primitive's parameters.  Grouped by key
+// vloc * n + primitive (a counting sort: K5 writes each entry's key, k_entry_count
+// counts, k_key_* scan, k_entry_count<true> places), the 32 entries of a warp form a few
+// runs of one key; each value is summed over its run in shared memory and added once.
+
+constexpr int kRedRows = 64;    // values per flush (two per lane)
+constexpr int kRedStride = 33;  // (row of 32 entries + 1: the per-lane column writes and
+                                //  per-row reads are both conflict-free)
+
+// A flush row's destination: base + mult * (by_key ? key : primitive).
+struct RowDesc {
+    float *base;
+    uint32_t mult;
+    bool by_key;
+};
+
+// Row `row` of a flush block: MLP groups g0 .. g0 + ng - 1 (per 4 hidden units: W2 x4,
+// b1 x4, W1 x12, [W_t x4]), then, in the last block, b2 [, mu x3, s x3, q x4] [, dL/dc
+// x3 -> gc_acc, by key vloc * n + primitive].
+template <int N>
+__device__ __forceinline__ RowDesc row_desc(const BackwardGrads &gr, const RenderArgs &a, int row, int g0, int ng,
+                                            int GR) {
+    if (row < ng * GR) {
+        const int gi = row / GR, r = row - gi * GR;
+        const int k0 = 4 * (g0 + gi);
+        if (r < 4) return {gr.w2 + k0 + r, (uint32_t)N, false};
+        if (r < 8) return {gr.b1 + k0 + (r - 4), (uint32_t)N, false};
+        if (r < 20) return {gr.w1 + 3 * k0 + (r - 8), 3u * N, false};
+        return {gr.wt + k0 + (r - 20), (uint32_t)N, false};
+    }
+    const int t = row - ng * GR;
+    if (t == 0) return {gr.b2, 1u, false};
+    const int tc = gr.mu ? 11 : 1;
+    if (t < tc) {
+        if (t < 4) return {gr.mu + (t - 1), 3u, false};
+        if (t < 7) return {gr.s + (t - 4), 3u, false};
+        return {gr.q + (t - 7), 4u, false};
+    }
+    return {reinterpret_cast<float *>(a.gc_acc) + (t - tc), 4u, true};
+}
+
+// Sums rows [0, nrows) of s (s[row][entry], this warp's 32 entries) over the runs that
+// `ends` marks (bit e: entry e ends a run; warp-uniform) and adds each nonzero sum once,
+// at desc(row)'s address for the run's primitive pr / key k2.
+template <class Desc>
+__device__ __forceinline__ void run_flush(float (*s)[kRedStride], int nrows, uint32_t ends, uint32_t pr, uint32_t k2,
+                                          Desc desc) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    const bool h0 = lane < nrows, h1 = lane + 32 < nrows;
+    const RowDesc d0 = h0 ? desc(lane) : RowDesc{nullptr, 0u, false};
+    const RowDesc d1 = h1 ? desc(lane + 32) : RowDesc{nullptr, 0u, false};
+    int start = 0;
+    while (ends) {
+        const int end = __ffs(ends) - 1;
+        ends &= ends - 1;
+        const uint32_t rp = __shfl_sync(0xffffffffu, pr, end), rk = __shfl_sync(0xffffffffu, k2, end);
+        float a0 = 0.f, a1 = 0.f;
+        for (int e = start; e <= end; ++e) {
+            a0 += s[lane][e];
+            a1 += s[lane + 32][e];
+        }
+        if (h0 && a0 != 0.f) atomicAdd(d0.base + (size_t)d0.mult * (d0.by_key ? rk : rp), a0);
+        if (h1 && a1 != 0.f) atomicAdd(d1.base + (size_t)d1.mult * (d1.by_key ? rk : rp), a1);
+        start = end + 1;
+    }
+    __syncwarp();
+}
+
+// hit_grad's values for one entry per lane (ok = false: the lane contributes zeros) into
+// the warp's rows, flushed per block of at most kRedRows; dL/dc (primitive colour mode)
+// rides in the last block.  Same arithmetic as hit_grad, in the same order.
+template <int N, bool kRay>
+__device__ __forceinline__ void hit_grad_rows(const float4 *__restrict__ rec, const Ray &r, float gI, float omega,
+                                              bool ok, const RenderArgs &ra, const BackwardGrads &gr, float xi_t,
+                                              uint32_t prim, uint32_t k2, const float gc[3],
+                                              float (*s)[kRedStride], uint32_t ends) {
+    const int lane = threadIdx.x & 31;
+    // (the primitive's own parameters first: the shared-memory stores and atomics below
+    //  would keep the compiler from hoisting these loads)
+    const float *s3 = ra.scales + 3 * (size_t)prim;
+    const float sv[3] = {s3[0], s3[1], s3[2]};
+    float q4[4] = {0.f, 0.f, 0.f, 0.f};
+    if (gr.mu) {
+        const float *qp = ra.rotations + 4 * (size_t)prim;
+        q4[0] = qp[0]; q4[1] = qp[1]; q4[2] = qp[2]; q4[3] = qp[3];
+    }
+    const float4 mh = rec[kRecMh];
+    const float4 ml = rec[kRecMl];
+    const float4 w0 = rec[kRecWh0];
+    const float4 w1 = rec[kRecWh1];
+    const float Wh[9] = {ml.w, w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const float d[3] = {r.dhx, r.dhy, r.dhz};
+    const float tc = fmaf(r.dhz, mh.z, fmaf(r.dhy, mh.y, r.dhx * mh.x));
+    const float p[3] = {fmaf(tc, r.dhx, -mh.x) + fmaf(tc, r.dlx, -ml.x),
+                        fmaf(tc, r.dhy, -mh.y) + fmaf(tc, r.dly, -ml.y),
+                        fmaf(tc, r.dhz, -mh.z) + fmaf(tc, r.dlz, -ml.z)};
+    float av[3], bv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        av[k] = fmaf(Wh[3 * k + 2], d[2], fmaf(Wh[3 * k + 1], d[1], Wh[3 * k] * d[0]));
+        bv[k] = fmaf(Wh[3 * k + 2], p[2], fmaf(Wh[3 * k + 1], p[1], Wh[3 * k] * p[0]));
+    }
+    const float A = fmaf(av[2], av[2], fmaf(av[1], av[1], av[0] * av[0]));
+    const float B = fmaf(av[2], bv[2], fmaf(av[1], bv[1], av[0] * bv[0]));
+    const float iA = 1.0f / A;
+    const float ts = -B * iA;
+    const float bp[3] = {fmaf(ts, av[0], bv[0]), fmaf(ts, av[1], bv[1]), fmaf(ts, av[2], bv[2])};
+    const float Q = 1.0f - fmaf(bp[2], bp[2], fmaf(bp[1], bp[1], bp[0] * bp[0]));
+    ok = ok && Q > 0.0f;
+    const float hc = sqrtf(Q * iA);
+    const float t0 = ts - hc, t1 = ts + hc;
+    const float lo_lim = r.t_near - tc, hi_lim = r.t_far - tc;
+    const bool clip_lo = !(t0 > lo_lim), clip_hi = !(t1 < hi_lim);
+    const float tlo = clip_lo ? lo_lim : t0;
+    const float thi = clip_hi ? hi_lim : t1;
+    ok = ok && thi > tlo;
+    const float dt = thi - tlo, tm = 0.5f * (tlo + thi), hdt = 0.5f * dt;
+    const int imax = (sv[1] > sv[0]) ? ((sv[2] > sv[1]) ? 2 : 1) : ((sv[2] > sv[0]) ? 2 : 0);
+    const float isv[3] = {1.0f / sv[0], 1.0f / sv[1], 1.0f / sv[2]};
+    const float ismax = isv[imax];
+    const float s1 = omega * ismax;
+    float sumc = mh.w;
+    float gdt = 0.f, gtm = 0.f, gsmax = 0.f;
+    float gp[3] = {0.f, 0.f, 0.f};
+    const int GR = gr.wt ? 24 : 20;
+    const int tail = (gr.mu ? 11 : 1) + (kRay ? 0 : 3);
+    int g0 = 0, used = 0;
+    auto flush = [&](int ng, int nrows) {
+        run_flush(s, nrows, ends, prim, k2, [&](int row) { return row_desc<N>(gr, ra, row, g0, ng, GR); });
+    };
+#pragma unroll 1
+    for (int gq = 0; gq < N / 4; ++gq) {
+        if (used + GR > kRedRows) {   // (warp-uniform)
+            flush(gq - g0, used);
+            g0 = gq;
+            used = 0;
+        }
+        float(*sg)[kRedStride] = s + used;
+        const float4 w4 = rec[rec_w2(N) + gq];
+        const float w2s[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int uu = 0; uu < 4; ++uu) {
+            const int k = 4 * gq + uu;
+            const float4 u = rec[kRecUnits + k];
+            const float w2 = w2s[uu];
+            const float h = fmaf(u.z, d[2], fmaf(u.y, d[1], u.x * d[0]));
+            const float g = fmaf(u.z, p[2], fmaf(u.y, p[1], fmaf(u.x, p[0], u.w)));
+            const float phi = fmaf(h, tm, g);
+            float sn, cs;
+            __sincosf(phi, &sn, &cs);
+            const float x = h * hdt;
+            const float S = sinc_f(x);
+            const float Sp = dsinc_f(x);
+            sumc = fmaf(w2 * cs, S, sumc);
+            gdt = fmaf(w2 * cs * Sp, 0.5f * h, gdt);
+            gtm = fmaf(-w2 * sn * S, h, gtm);
+            const float coef = -dt * w2 * sn * S;
+            const float chs = dt * w2 * cs * Sp * hdt;
+            gp[0] = fmaf(coef, u.x, gp[0]);
+            gp[1] = fmaf(coef, u.y, gp[1]);
+            gp[2] = fmaf(coef, u.z, gp[2]);
+            const float gw[3] = {fmaf(coef, fmaf(tm, d[0], p[0]), chs * d[0]),
+                                 fmaf(coef, fmaf(tm, d[1], p[1]), chs * d[1]),
+                                 fmaf(coef, fmaf(tm, d[2], p[2]), chs * d[2])};
+            gsmax = fmaf(-(gw[0] * u.x + gw[1] * u.y + gw[2] * u.z), ismax, gsmax);
+            const float gb1 = gI * omega * coef;
+            sg[uu][lane] = ok ? gI * dt * cs * S : 0.f;
+            sg[4 + uu][lane] = ok ? gb1 : 0.f;
+            sg[8 + 3 * uu + 0][lane] = ok ? gI * s1 * gw[0] : 0.f;
+            sg[8 + 3 * uu + 1][lane] = ok ? gI * s1 * gw[1] : 0.f;
+            sg[8 + 3 * uu + 2][lane] = ok ? gI * s1 * gw[2] : 0.f;
+            if (gr.wt) sg[20 + uu][lane] = ok ? xi_t * gb1 : 0.f;   // phase offset omega (b1 + xi_t W_t) (R24)
+        }
+        used += GR;
+    }
+    const int ng = N / 4 - g0;
+    if (used + tail > kRedRows) {
+        flush(ng, used);
+        g0 = N / 4;
+        used = 0;
+    }
+    const int ngl = N / 4 - g0;
+    float(*st)[kRedStride] = s + used;
+    st[0][lane] = ok ? gI * dt : 0.f;
+    int t = 1;
+    if (gr.mu) {
+        const float G_dt = gI * fmaf(dt, gdt, sumc), G_tm = gI * dt * gtm;
+        const float G_tlo = -G_dt + 0.5f * G_tm, G_thi = G_dt + 0.5f * G_tm;
+        const float G_t0 = clip_lo ? 0.f : G_tlo, G_t1 = clip_hi ? 0.f : G_thi;
+        float G_tc = (clip_lo ? -G_tlo : 0.f) + (clip_hi ? -G_thi : 0.f);
+        float G_ts = G_t0 + G_t1;
+        const float G_hc = G_t1 - G_t0;
+        const float G_Q = G_hc * hc * (0.5f / Q);
+        float G_A = -G_hc * hc * 0.5f * iA;
+        float G_a[3], G_b[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float gbp = -2.0f * bp[k] * G_Q;
+            G_b[k] = gbp;
+            G_a[k] = ts * gbp;
+            G_ts = fmaf(gbp, av[k], G_ts);
+        }
+        const float G_B = -G_ts * iA;
+        G_A = fmaf(G_ts * B, iA * iA, G_A);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            G_a[k] = fmaf(2.0f * av[k], G_A, fmaf(bv[k], G_B, G_a[k]));
+            G_b[k] = fmaf(av[k], G_B, G_b[k]);
+        }
+        float Gp[3] = {gI * gp[0], gI * gp[1], gI * gp[2]};
+        float G_Wh[9];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                G_Wh[3 * k + j] = fmaf(G_a[k], d[j], G_b[k] * p[j]);
+                Gp[j] = fmaf(Wh[3 * k + j], G_b[k], Gp[j]);
+            }
+        G_tc = fmaf(Gp[2], d[2], fmaf(Gp[1], d[1], fmaf(Gp[0], d[0], G_tc)));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) st[1 + k][lane] = ok ? fmaf(d[k], G_tc, -Gp[k]) : 0.f;
+        float G_s[3], G_R[9];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                acc = fmaf(G_Wh[3 * k + j], Wh[3 * k + j], acc);
+                G_R[3 * j + k] = G_Wh[3 * k + j] * isv[k];
+            }
+            G_s[k] = -acc * isv[k];
+        }
+        G_s[imax] += gI * gsmax;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) st[4 + k][lane] = ok ? G_s[k] : 0.f;
+        const float qn = sqrtf(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
+        const float iqn = 1.0f / qn;
+        const float w = q4[0] * iqn, x = q4[1] * iqn, y = q4[2] * iqn, z = q4[3] * iqn;
+        const float gw_ = 2.0f * (-z * G_R[1] + y * G_R[2] + z * G_R[3] - x * G_R[5] - y * G_R[6] + x * G_R[7]);
+        const float gx_ = 2.0f * (y * G_R[1] + z * G_R[2] + y * G_R[3] - 2.0f * x * G_R[4] - w * G_R[5] +
+                                  z * G_R[6] + w * G_R[7] - 2.0f * x * G_R[8]);
+        const float gy_ = 2.0f * (-2.0f * y * G_R[0] + x * G_R[1] + w * G_R[2] + x * G_R[3] + z * G_R[5] -
+                                  w * G_R[6] + z * G_R[7] - 2.0f * y * G_R[8]);
+        const float gz_ = 2.0f * (-2.0f * z * G_R[0] - w * G_R[1] + x * G_R[2] + w * G_R[3] - 2.0f * z * G_R[4] +
+                                  y * G_R[5] + x * G_R[6] + y * G_R[7]);
+        const float dotq = w * gw_ + x * gx_ + y * gy_ + z * gz_;
+        st[7][lane] = ok ? (gw_ - w * dotq) * iqn : 0.f;
+        st[8][lane] = ok ? (gx_ - x * dotq) * iqn : 0.f;
+        st[9][lane] = ok ? (gy_ - y * dotq) * iqn : 0.f;
+        st[10][lane] = ok ? (gz_ - z * dotq) * iqn : 0.f;
+        t = 11;
+    }
+    if (!kRay) {   // (summed per (view, primitive) for k_colour_finalize; the entry's own validity)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) st[t + c][lane] = gc[c];
+    }
+    flush(ngl, used + tail);
+}
+
+// Counting sort of the entries by key vloc * n + primitive (K5 wrote each slot's key):
+// counts per key, exclusive scan in place (block sums, their scan, block scans), then the
+// entries' slots go to their key's next position.
+constexpr int kScanPer = 4096;   // keys per block (1024 threads x 4)
+__device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t *s_w, uint32_t *total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t w = s_w[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_w[lane] = wi - w;
+        if (lane == 31) s_w[32] = wi;
+    }
+    __syncthreads();
+    const uint32_t r = s_w[wid] + incl - v;
+    *total = s_w[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) k_key_sums(const uint32_t *__restrict__ cnt, int64_t nk, uint32_t *bsum) {
+    __shared__ uint32_t s_w[33];
+    const int64_t b0 = (int64_t)blockIdx.x * kScanPer;
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = b0 + k * 1024 + threadIdx.x;
+        if (i < nk) v += cnt[i];
+    }
+    uint32_t tot;
+    block_excl_scan_1024(v, s_w, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_key_top(uint32_t *bsum, int64_t nb, unsigned long long *scnt) {
+    __shared__ uint32_t s_w[33];
+    uint32_t run = 0;
+    for (int64_t b = 0; b < nb; b += 1024) {
+        const int64_t i = b + threadIdx.x;
+        const uint32_t v = i < nb ? bsum[i] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_1024(v, s_w, &tot);
+        if (i < nb) bsum[i] = run + ex;
+        run += tot;
+    }
+    if (threadIdx.x == 0) scnt[kCntDup] = run;
+}
+
+__global__ void __launch_bounds__(1024) k_key_apply(uint32_t *cnt, int64_t nk, const uint32_t *bsum) {
+    __shared__ uint32_t s_w[33];
+    const int64_t b0 = (int64_t)blockIdx.x * kScanPer + 4 * (int64_t)threadIdx.x;
+    uint32_t v[4], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = b0 + k < nk ? cnt[b0 + k] : 0u;
+        sum += v[k];
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan_1024(sum, s_w, &tot) + bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (b0 + k < nk) cnt[b0 + k] = ex;
+        ex += v[k];
+    }
+}
+
+// (lanes with equal keys -- neighbouring pixels' hits of one primitive -- share one atomic)
+template <bool kScatter>
+__global__ void __launch_bounds__(256) k_entry_count(RenderArgs a, uint32_t *__restrict__ key_cnt,
+                                                     uint32_t *__restrict__ sorted) {
+    int64_t nc = (int64_t)a.counters[kCntGradEntries];
+    if (nc > a.grad_chunks) nc = a.grad_chunks;
+    if (a.counters[kCntGradOverflow]) nc = 0;
+    const int64_t n = nc * kGradChunk;
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;   // (warp-uniform trip count: i0 steps by whole blocks)
+        const bool used = i < n && (int)(i & (kGradChunk - 1)) < a.grad_fill[i / kGradChunk];
+        const uint32_t key = used ? a.grad_keys[i] : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (used && lane == leader) {
+            if (kScatter) base = atomicAdd(key_cnt + key, (uint32_t)__popc(peers));
+            else atomicAdd(key_cnt + key, (uint32_t)__popc(peers));
+        }
+        if (kScatter) {
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (used) sorted[base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)i;
+        }
+    }
+}
+
+template <int N, bool kRay>
+__global__ void __launch_bounds__(128) k_grad_sorted(RenderArgs a, CamBatch cb, const uint32_t *__restrict__ sorted,
+                                                     const unsigned long long *scnt, BackwardGrads gr, float omega) {
+    if (a.counters[kCntGradOverflow]) return;
+    __shared__ DevCam s_cam[kCamsPerLaunch];
+    __shared__ float s_red[4][kRedRows][kRedStride];
+    for (int i = threadIdx.x; i < cb.nv; i += blockDim.x) s_cam[i] = cb.cams[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float(*s)[kRedStride] = s_red[wid];
+    const int64_t n = (int64_t)scnt[kCntDup];
+    const int64_t step = (int64_t)gridDim.x * 4 * 32;
+    int64_t base = ((int64_t)blockIdx.x * 4 + wid) * 32;
+    GradEntry en{};   // (the next iteration's entry, loaded one iteration ahead)
+    if (base + lane < n) en = a.grad_entries[sorted[base + lane]];
+    for (; base < n; base += step) {
+        const int64_t pos = base + lane;
+        const bool valid = pos < n;
+        const GradEntry e = en;   // (zero on lanes past the end)
+        en = GradEntry{};
+        if (base + step + lane < n) en = a.grad_entries[sorted[base + step + lane]];
+        const int vloc = valid ? (int)(e.pix >> 24) : 0;
+        SNP_CHECK(!valid || (vloc < cb.nv && (int64_t)e.id < a.n));
+        const uint32_t k2 = valid ? (uint32_t)vloc * (uint32_t)a.n + e.id : 0xffffffffu;
+        const uint32_t nk2 = __shfl_down_sync(0xffffffffu, k2, 1);
+        const uint32_t ends = __ballot_sync(0xffffffffu, lane == 31 || nk2 != k2);
         const DevCam &cam = s_cam[vloc];
         const uint32_t p = e.pix & 0xffffffu;
         const int y = (int)(p / (uint32_t)cam.W), x = (int)(p - (uint32_t)y * (uint32_t)cam.W);
         const Ray ray = make_ray(cam, x, y);
         const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + e.id) * rec_f4(N);
-        if (kRay) {
-            const float gc[3] = {e.gc0, e.gc1, e.gc2};
-            hit_all_grads<N, kRay>(a, rec, ray, e.id, e.gI, gc, omega, gr, cam.xi_t);
-        } else {   // colour part per (view, primitive) in k_colour_finalize
-            hit_grad<N>(rec, ray, e.gI, omega, e.id, a, gr, cam.xi_t);
-            if (e.gc0 != 0.f || e.gc1 != 0.f || e.gc2 != 0.f)
-                atomicAdd(a.gc_acc + (size_t)vloc * a.n + e.id, make_float4(e.gc0, e.gc1, e.gc2, 0.f));
+        const float gc[3] = {e.gc0, e.gc1, e.gc2};   // (zero on invalid lanes)
+        hit_grad_rows<N, kRay>(rec, ray, e.gI, omega, valid, a, gr, cam.xi_t, e.id, k2, gc, s, ends);
+        if (kRay) {   // SH at the pixel's ray direction: 3 ncoef (<= 48) values, one flush
+            const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
+            float Y[16];
+            sh_basis_f(ray.dhx, ray.dhy, ray.dhz, Y);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i < ncoef) {
+                    s[3 * i][lane] = Y[i] * gc[0];
+                    s[3 * i + 1][lane] = Y[i] * gc[1];
+                    s[3 * i + 2][lane] = Y[i] * gc[2];
+                }
+            run_flush(s, 3 * ncoef, ends, e.id, k2, [&](int row) { return RowDesc{gr.sh + row, 48u, false}; });
         }
     }
 }
@@ -688,21 +1142,33 @@ __global__ void __launch_bounds__(128) k_colour_finalize(RenderArgs a, CamBatch 
 
 template <int N, bool kRay>
 cudaError_t launch_grad_entries_n(const RenderArgs &a, const CamBatch &cb, const BackwardGrads &g, float omega,
-                                  cudaStream_t st) {
+                                  const EntrySort *es, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    k_grad_entries<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, a.grad_entries, g, omega);
+    if (es) {   // counting sort by (view, primitive) key, then K7s
+        const int64_t nk = (int64_t)cb.nv * a.n;
+        const int64_t nb = (nk + kScanPer - 1) / kScanPer;
+        if (nb == 0) return cudaSuccess;   // (no primitives: no entries)
+        k_entry_count<false><<<(unsigned)(sms * 8), 256, 0, st>>>(a, a.grad_count, nullptr);
+        k_key_sums<<<(unsigned)nb, 1024, 0, st>>>(a.grad_count, nk, es->bsum);
+        k_key_top<<<1, 1024, 0, st>>>(es->bsum, nb, es->cnt);
+        k_key_apply<<<(unsigned)nb, 1024, 0, st>>>(a.grad_count, nk, es->bsum);
+        k_entry_count<true><<<(unsigned)(sms * 8), 256, 0, st>>>(a, a.grad_count, es->sorted);
+        k_grad_sorted<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, es->sorted, es->cnt, g, omega);
+    } else {
+        k_grad_entries<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, a.grad_entries, g, omega);
+    }
     if (!kRay) k_colour_finalize<N><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, g);
     return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t launch_backward_w(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                              float omega, void *scratch, bool k5, cudaStream_t st) {
+                              float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st) {
     if (k5) {
-        cudaError_t e = a.colour_ray ? launch_grad_entries_n<N, true>(a, cb, g, omega, st)
-                                     : launch_grad_entries_n<N, false>(a, cb, g, omega, st);
+        cudaError_t e = a.colour_ray ? launch_grad_entries_n<N, true>(a, cb, g, omega, es, st)
+                                     : launch_grad_entries_n<N, false>(a, cb, g, omega, es, st);
         if (e != cudaSuccess) return e;
     }
     return a.colour_ray ? launch_backward_n<N, true>(a, cb, grad, g, omega, scratch, k5, st)
@@ -714,12 +1180,12 @@ cudaError_t launch_backward_w(const RenderArgs &a, const CamBatch &cb, const flo
 size_t backward_scratch_bytes() { return (size_t)kBwHugeCtas * sizeof(BwSmem<1, kBwHugeHits>); }
 
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, void *scratch, bool k5, cudaStream_t st) {
+                            float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st) {
     switch (a.n_hidden) {
-        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, scratch, k5, st);
-        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, scratch, k5, st);
-        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, scratch, k5, st);
-        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, scratch, k5, st);
+        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, scratch, k5, es, st);
+        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, scratch, k5, es, st);
+        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, scratch, k5, es, st);
+        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, scratch, k5, es, st);
         default: return cudaErrorInvalidValue;
     }
 }

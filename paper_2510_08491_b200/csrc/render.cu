@@ -205,7 +205,11 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
                 e.gc1 = rgb.z > 0.f ? w * G.y : 0.f;
                 e.gc2 = rgb.w > 0.f ? w * G.z : 0.f;
                 const int slot = atomicAdd(gx->cnt, 1);
-                if (gx->chunk) gx->chunk[slot] = e;
+                if (gx->chunk) {
+                    gx->chunk[slot] = e;
+                    if (a.grad_keys)   // K7s's counting sort key
+                        a.grad_keys[(gx->chunk - a.grad_entries) + slot] = (gx->pix >> 24) * (uint32_t)a.n + pid;
+                }
             }
         }
         ps.T *= (1.0f - kap);

@@ -218,6 +218,8 @@ struct RenderArgs {
     const float4 *fwd;             // K5 grad mode: the forward's out RGBA [V][H][W]
     GradEntry *grad_entries;       // K5 grad mode: entry buffer, grad_chunks chunks of kGradChunk
     int32_t *grad_fill;            //   entries used per chunk
+    uint32_t *grad_keys;           //   per slot: vloc * n + primitive (K7s)
+    uint32_t *grad_count;          //   [nv * n] entries per key -> offsets (K7s; zeroed per batch)
     int64_t grad_chunks;
     float4 *gc_acc;                // K7f, primitive colour mode: [batch views][n] summed dL/dc
     int32_t tiles_x, tiles_y, tiles_per_view;
@@ -262,8 +264,17 @@ struct BackwardGrads {
     float *wt;                     // temporal weights' gradient [n][N], or nullptr
     bool vec;                      // every array 16-byte aligned: vector (float4) atomics
 };
+// K7s: the K5-path entries grouped by key vloc * n + primitive (a counting sort over
+// RenderArgs::grad_keys, which K5 writes, with RenderArgs::grad_count)
+struct EntrySort {
+    uint32_t *bsum;                // [ceil(nv n / 4096)] scan block sums
+    uint32_t *sorted;              // [grad_chunks * kGradChunk] entry slots in key order
+    unsigned long long *cnt;       // cnt[kCntDup] = entries
+};
+// k5: K7f (es: sorted, K7s; nullptr: in slot order) over the K5 entries, then the
+// per-pixel K7 for the pixels K5 queued; !k5: the per-pixel K7 for every pixel
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, void *scratch, bool k5, cudaStream_t st);
+                            float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st);
 // K5 in grad mode over one camera batch (render.cu): the forward traversal emitting
 // GradEntry per composited hit; overflowing pixels go to bw_queue with their skip count
 cudaError_t launch_render_grad(const RenderArgs &a, const CamBatch &cams, cudaStream_t st);
