@@ -127,6 +127,8 @@ typedef struct {
     uint64_t capacity_overflow;/* 1 if the last no-sync bin_sort overflowed the key buffer */
     uint64_t backward_skipped; /* pixels the last snp_render_backward skipped (more than 16384
                                   hits on the ray: no gradient from them); 0 otherwise */
+    uint64_t dead_keys;        /* keys of the last bin_sort that SNP_BIN_CONIC_TILES found
+                                  outside the silhouette (sorted last, never rendered) */
 } snp_stats;
 
 /* Library version string. */
@@ -262,8 +264,22 @@ snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream);
  * K6 (more hits than K6w holds); slot 48 counts the grazing hits K5 evaluated with a
  * kappa error bound above 1.5e-5 (R23) since the last readback; slots 16..47
  * are only written by instrumented A/B builds (per-warp clock64 accounting).  The
- * call clears slots >= 16 after reading.  Not part of the hot path. */
+ * call clears slots 16..52 after reading.  Not part of the hot path. */
 snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *cuda_stream);
+
+/* Tight binning, from the next snp_project on:
+ *   SNP_BIN_CONIC_TILES: K2 drops the keys of rect tiles whose pixel-centre rectangle the
+ *     primitive's silhouette ellipse (the perspective image of the ellipsoid)
+ *     does not reach -- such a tile holds no pixel whose ray hits the primitive, so the
+ *     frame is unchanged; the keys are kept as dead keys sorted after all live ones
+ *     (snp_stats.dead_keys);
+ *   SNP_BIN_TILE_DEPTH: each key's depth is the larger of the primitive's bound and a
+ *     per-tile bound (the support function of the ellipsoid along the tile's central ray),
+ *     so K5 emits hits sooner (R19 holds with either bound).
+ * 0 (the default) is the rect binning whose keys are bit-exact with the oracle's binning
+ * definition.  Flags outside these two: SNP_ERR_INVALID_ARGUMENT. */
+enum { SNP_BIN_CONIC_TILES = 1, SNP_BIN_TILE_DEPTH = 2 };
+snp_status snp_set_binning(snp_scene s, int32_t flags);
 
 /* Test hook: caps the per-pixel pending buffer of K5 at `k` entries (1..16) so
  * that the exact fallback K6 is exercised; 0 restores the default (16). */

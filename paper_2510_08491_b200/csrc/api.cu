@@ -84,6 +84,10 @@ struct snp_scene_s {
     DevBuf<float> loss_scratch;        // snp_loss_3dgs: moment / SSIM-derivative maps
     DevBuf<uint32_t> bw_skip;          // K7: composited hits K5's grad mode already emitted, per pixel
     DevBuf<float> bw_fwd;              // K7: the forward image when the caller does not pass it
+    DevBuf<float4> tight;              // K1a -> K2, tight binning (SNP_BIN_*): per item, see tight_geom
+    DevBuf<float4> intr;               //   per view (1/fx, 1/fy, cx, cy)
+    int32_t bin_flags = 0;             // snp_set_binning (applies from the next snp_project)
+    int32_t projected_bin_flags = 0;   // the flags of the current projection
     DevBuf<GradEntry> grad_entries;    // K5 grad mode -> K7f
     DevBuf<int32_t> grad_fill;         //   entries used per chunk
     DevBuf<uint32_t> grad_keys;        //   per slot: vloc * n + primitive
@@ -159,6 +163,8 @@ void fill_args(snp_scene s, ProjectArgs &a) {
     a.w_t = s->temporal ? s->w_t.p : nullptr;
     a.tiles_x = s->tiles_x; a.tiles_y = s->tiles_y;
     a.rects = s->rects.p; a.depth = s->depth.p; a.records = s->records.p;
+    a.tight = s->bin_flags ? s->tight.p : nullptr;
+    a.intr = s->bin_flags ? s->intr.p : nullptr;
     a.counters = s->counters.p;
 }
 
@@ -375,6 +381,10 @@ snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, 
     const size_t items = (size_t)n_views * (size_t)s->n;
     SNP_CUDA(s->rects.ensure(items + 2));   // (+2: K1b bulk-copies rect rows rounded up to 16 bytes)
     SNP_CUDA(s->depth.ensure(items));
+    if (s->bin_flags) {
+        SNP_CUDA(s->tight.ensure(items * 4));
+        SNP_CUDA(s->intr.ensure((size_t)n_views));
+    }
     SNP_CUDA(s->records.ensure(items * rec_f4(s->n_hidden)));
     s->cams.clear();
     for (int v0 = 0; v0 < n_views; v0 += kCamsPerLaunch) {
@@ -405,6 +415,7 @@ snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, 
         SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntVisibleAcc, 0, sizeof(unsigned long long), st));
     ProjectArgs a{};
     fill_args(s, a);
+    s->projected_bin_flags = s->bin_flags;
     for (const CamBatch &cb : s->cams) SNP_CUDA(launch_bin_geom(a, cb, st));
     // fork: K1b on the side stream, overlapping K2-K4 (which need only K1a's output)
     SNP_CUDA(cudaEventRecord(s->ev_fork, st));
@@ -448,6 +459,9 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     b.row_stride = s->row_stride;
     b.rects = s->rects.p;
     b.depth = s->depth.p;
+    b.bin_flags = s->projected_bin_flags;
+    b.tight = s->projected_bin_flags ? s->tight.p : nullptr;
+    b.intr = s->projected_bin_flags ? s->intr.p : nullptr;
     b.dup_status = s->dup_status.p;
     b.counters = s->counters.p;
     auto alloc_keys = [&](int64_t cap) -> cudaError_t {
@@ -498,6 +512,7 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
             SNP_CUDA(ensure_sort_scratch());
             SNP_CUDA(cudaMemsetAsync(s->sort_scratch.p, 0, sizeof(uint32_t) * 8 * 256, st));
             SNP_CUDA(cudaMemsetAsync(s->dup_status.p, 0, sizeof(unsigned long long) * s->dup_status.cap, st));
+            SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntDeadKeysAcc, 0, sizeof(unsigned long long), st));
             b.capacity = s->key_capacity;
             b.hist = s->sort_scratch.p;
             b.keys = s->keys0.p;
@@ -875,6 +890,8 @@ snp_status snp_destroy(snp_scene s) {
     s->bw_skip.release();
     s->bw_fwd.release();
     s->grad_entries.release();
+    s->tight.release();
+    s->intr.release();
     s->grad_fill.release();
     s->grad_keys.release();
     s->grad_count.release();
@@ -957,6 +974,7 @@ snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream) {
     out->overflow_pixels = c[kCntOverflow];
     out->capacity_overflow = c[kCntCapOverflow];
     out->backward_skipped = c[kCntBwdSkipped];
+    out->dead_keys = c[kCntDeadKeys];
     return SNP_OK;
 }
 
@@ -971,8 +989,16 @@ snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *c
     SNP_CUDA(cudaStreamSynchronize(st));
     for (int i = 0; i < n; ++i) out[i] = s->h_counters[i];
     // the instrumented slots accumulate until read: clear them for the next measurement
-    SNP_CUDA(cudaMemsetAsync(s->counters.p + 16, 0, sizeof(unsigned long long) * (kNumCounters - 16), st));
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + 16, 0, sizeof(unsigned long long) * (kCntDeadKeysAcc - 16), st));
     SNP_CUDA(cudaStreamSynchronize(st));
+    return SNP_OK;
+}
+
+snp_status snp_set_binning(snp_scene s, int32_t flags) {
+    g_err.clear();
+    if (!s) return fail(SNP_ERR_INVALID_ARGUMENT, "scene handle is NULL");
+    if (flags & ~(SNP_BIN_CONIC_TILES | SNP_BIN_TILE_DEPTH)) return fail(SNP_ERR_INVALID_ARGUMENT, "unknown binning flag");
+    s->bin_flags = flags;
     return SNP_OK;
 }
 

@@ -98,6 +98,48 @@ __device__ __forceinline__ unsigned long long dup_lookback(const unsigned long l
 // output range; lanes walk it 32 keys at a time (coalesced 8-byte key + 4-byte
 // value stores), each lane finding its key's item by binary search over the warp's
 // item offsets in shared memory.  The last block writes the key count.
+// Tight binning (scene flag SNP_BIN_CONIC_TILES): does the silhouette
+// ellipse (d^T [[A, B], [B, C]] d <= 1, d = p - centre) reach the rectangle [dx0, dx1] x
+// [dy0, dy1] of a tile's pixel centres (offsets from the centre)?  The minimum of the
+// quadratic over the rectangle is at the centre when the centre is inside, else on an
+// edge (the clamped vertex of the edge's 1D quadratic).  Margins: the rectangle is grown
+// by 1/256 px, the threshold by 1e-3 (the float data and the fp32 hit test, hit.cuh).
+__device__ __forceinline__ bool ellipse_meets_rect(float A, float B, float C, float dx0, float dx1, float dy0,
+                                                   float dy1) {
+    if (dx0 <= 0.f && 0.f <= dx1 && dy0 <= 0.f && 0.f <= dy1) return true;
+    float qmin = INFINITY;
+    const float xs[2] = {dx0, dx1}, ys[2] = {dy0, dy1};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float X = xs[k];
+        const float dy = fminf(fmaxf(-B * X / C, dy0), dy1);
+        qmin = fminf(qmin, A * X * X + 2.0f * B * X * dy + C * dy * dy);
+        const float Y = ys[k];
+        const float dx = fminf(fmaxf(-B * Y / A, dx0), dx1);
+        qmin = fminf(qmin, A * dx * dx + 2.0f * B * dx * Y + C * Y * Y);
+    }
+    return qmin <= 1.0f + 1e-3f;
+}
+
+// Tight binning (SNP_BIN_TILE_DEPTH): a per-tile depth lower bound.  For any unit u,
+// every point x of the ellipsoid has |x| >= u.x >= u.m - sqrt(u^T S u) (its support
+// function), so with u the tile's central ray this bounds t_in of every ray (the unit
+// ray's t = |x|), and is tight for rays near u.  Rounded down with a 4e-6 relative margin
+// (float data); the key keeps the larger of it and K1a's bound.
+__device__ __forceinline__ float tile_depth_bound(const float4 &f1, const float4 &f2, const float4 &f3,
+                                                  const float4 &intr, int col, int row) {
+    const float px = (float)(col * kTile) + 0.5f * kTile, py = (float)(row * kTile) + 0.5f * kTile;
+    float u0 = (px - intr.z) * intr.x, u1 = (py - intr.w) * intr.y, u2 = 1.0f;
+    const float inv = rsqrtf(u0 * u0 + u1 * u1 + 1.0f);
+    u0 *= inv; u1 *= inv; u2 *= inv;
+    const float um = u0 * f1.y + u1 * f1.z + u2 * f1.w;
+    const float S00 = f2.x, S01 = f2.y, S02 = f2.z, S11 = f2.w, S12 = f3.x, S22 = f3.y;
+    const float uSu = S00 * u0 * u0 + S11 * u1 * u1 + S22 * u2 * u2 + 2.0f * (S01 * u0 * u1 + S02 * u0 * u2 + S12 * u1 * u2);
+    if (!(uSu >= 0.f)) return 0.f;
+    const float r = sqrtf(uSu);
+    return (um - r) - 4e-6f * (fabsf(um) + r) - 1e-30f;
+}
+
 __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
     pdl_prologue();
     __shared__ uint32_t sw[32];
@@ -169,6 +211,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
     const uint32_t wbeg = s_off[i0];
     const uint32_t wend = (wid == kScanThreads / 32 - 1) ? s_off[kScanTile] : s_off[i0 + 32 * kScanItems];
     const uint64_t view_shift = (uint64_t)a.tile_bits + kDepthBits;
+    uint32_t n_dead = 0;
     for (uint32_t e = wbeg + lane; e < wend; e += 32) {
         // largest item j in [i0, i0+256) with s_off[j] <= e (and count > 0)
         int lo = i0, hi = i0 + 32 * kScanItems - 1;
@@ -186,13 +229,41 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
         const uint32_t prim = (uint32_t)(o - (int64_t)view * a.n);
         const uint64_t tile = (uint64_t)row * (uint64_t)a.tiles_x + (uint64_t)(s_x0[lo] + c);
         SNP_CHECK(lo >= i0 && lo < i0 + 32 * kScanItems && row < a.tiles_y && s_x0[lo] + c < a.tiles_x);
-        const uint64_t key = (view << view_shift) | (tile << kDepthBits) | (uint64_t)s_dep[lo];
+        uint64_t key = (view << view_shift) | (tile << kDepthBits) | (uint64_t)s_dep[lo];
+        if (a.tight) {   // tight binning: drop tiles the silhouette misses, per-tile depth bounds
+            const float4 *t4 = a.tight + 4 * o;
+            const float4 f3 = __ldg(t4 + 3);
+            if (f3.z != 0.f) {
+                const int col = s_x0[lo] + c;
+                if (a.bin_flags & 1) {
+                    const float4 f0 = __ldg(t4), f1c = __ldg(t4 + 1);
+                    const float x0 = (float)(col * kTile) + 0.5f - 1.0f / 256.0f, y0 = (float)(row * kTile) + 0.5f - 1.0f / 256.0f;
+                    const float w = (float)(kTile - 1) + 2.0f / 256.0f;
+                    if (!ellipse_meets_rect(f0.z, f0.w, f1c.x, x0 - f0.x, x0 + w - f0.x, y0 - f0.y, y0 + w - f0.y)) {
+                        key = kDeadKey;
+                        ++n_dead;
+                    }
+                }
+                if (key != kDeadKey && (a.bin_flags & 2)) {
+                    const float Lt = tile_depth_bound(__ldg(t4 + 1), __ldg(t4 + 2), f3, __ldg(a.intr + view), col, row);
+                    const float Lp = __uint_as_float(a.depth[o]);
+                    if (Lt > Lp) {
+                        const uint64_t dep = (uint64_t)(__float_as_uint(Lt) >> kDepthDrop);
+                        key = (key & ~((1ull << kDepthBits) - 1ull)) | dep;
+                    }
+                }
+            }
+        }
         const uint64_t g = gbase + e;
         if (g < (uint64_t)a.capacity) {
             a.keys[g] = key;
             a.vals[g] = prim;
             for (int p = 0; p < a.passes; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
         }
+    }
+    if (a.tight) {
+        const uint32_t d = __reduce_add_sync(0xffffffffu, n_dead);
+        if (lane == 0 && d) atomicAdd(a.counters + kCntDeadKeysAcc, (unsigned long long)d);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < a.passes * 256; i += kScanThreads) {
@@ -209,7 +280,12 @@ __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *co
     // clean block states and digit histograms (no memset node)
     if (blockIdx.x == 0 && threadIdx.x <= kCntRenderLast - kCntTested)
         const_cast<unsigned long long *>(counters)[kCntTested + threadIdx.x] = 0ull;
-    if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<unsigned long long *>(counters)[kCntVisibleAcc] = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long *c = const_cast<unsigned long long *>(counters);
+        c[kCntVisibleAcc] = 0ull;
+        c[kCntDeadKeys] = c[kCntDeadKeysAcc];   // (K2 is complete)
+        c[kCntDeadKeysAcc] = 0ull;
+    }
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < dup_blocks; j += (int64_t)gridDim.x * blockDim.x)
         dup_status[j] = 0ull;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < hist_words; j += (int64_t)gridDim.x * blockDim.x)
@@ -218,6 +294,7 @@ __global__ void k_tile_ranges(const uint64_t *keys, const unsigned long long *co
     if (n > capacity) n = capacity;
     const uint64_t tmask = (1ull << tile_bits) - 1ull;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (keys[i] == kDeadKey) continue;   // (tight binning: sorted after every live key)
         const uint64_t vt = keys[i] >> kDepthBits;
         const uint64_t slot = (vt >> tile_bits) * (uint64_t)tiles + (vt & tmask);
         SNP_CHECK((vt & tmask) < (uint64_t)tiles);

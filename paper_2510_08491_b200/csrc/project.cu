@@ -72,6 +72,51 @@ __device__ __forceinline__ bool geom_prelude(const DevCam &cam, float mu0, float
     return true;
 }
 
+// Tight binning data of a visible (view, primitive): the silhouette as an
+// image ellipse (p - c)^T [[A, B], [B, C]] (p - c) <= 1 and the camera-frame centre m and
+// covariance S for per-tile depth bounds, as floats (K2 applies margins).  The silhouette
+// is the point conic adj(K (m m^T - S) K^T) (the dual conic of the tangent planes through
+// the camera centre, whose x / y extents are the rect's above), defined when the
+// ellipsoid lies in front of the camera (zmin > 0, m_z^2 > S_zz); otherwise flag 0 and K2
+// keeps every rect tile.
+__device__ __forceinline__ void tight_geom(const DevCam &cam, const Geom &g, double aq, float4 *t4) {
+    const double *m = g.m, *S = g.S;
+    const double fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
+    float xc = 0.f, yc = 0.f, A = 0.f, B = 0.f, Cc = 0.f, ok = 0.f;
+    if (g.zmin > 0.0 && aq > 0.0) {
+        const double M00 = m[0] * m[0] - S[0], M01 = m[0] * m[1] - S[1], M02 = m[0] * m[2] - S[2];
+        const double M11 = m[1] * m[1] - S[4], M12 = m[1] * m[2] - S[5], M22 = m[2] * m[2] - S[8];
+        // C* = K M K^T
+        const double d00 = fx * fx * M00 + 2.0 * fx * cx * M02 + cx * cx * M22;
+        const double d01 = fx * fy * M01 + fx * cy * M02 + cx * fy * M12 + cx * cy * M22;
+        const double d02 = fx * M02 + cx * M22;
+        const double d11 = fy * fy * M11 + 2.0 * fy * cy * M12 + cy * cy * M22;
+        const double d12 = fy * M12 + cy * M22;
+        const double d22 = M22;
+        // point conic = adj(C*)
+        const double c00 = d11 * d22 - d12 * d12, c01 = d02 * d12 - d01 * d22, c02 = d01 * d12 - d02 * d11;
+        const double c11 = d00 * d22 - d02 * d02, c12 = d01 * d02 - d00 * d12, c22 = d00 * d11 - d01 * d01;
+        const double det = c00 * c11 - c01 * c01;
+        if (det > 0.0) {
+            const double ex = -(c11 * c02 - c01 * c12) / det, ey = -(c00 * c12 - c01 * c02) / det;
+            const double qc = c22 + c02 * ex + c12 * ey;   // q at the centre
+            if (qc != 0.0 && (c00 > 0.0) == (qc < 0.0)) {  // a real ellipse: interior q / qc > 0
+                const double s = -1.0 / qc;
+                xc = (float)ex;
+                yc = (float)ey;
+                A = (float)(c00 * s);
+                B = (float)(c01 * s);
+                Cc = (float)(c11 * s);
+                ok = 1.f;
+            }
+        }
+    }
+    t4[0] = make_float4(xc, yc, A, B);
+    t4[1] = make_float4(Cc, (float)m[0], (float)m[1], (float)m[2]);
+    t4[2] = make_float4((float)S[0], (float)S[1], (float)S[2], (float)S[4]);
+    t4[3] = make_float4((float)S[5], (float)S[8], ok, 0.f);
+}
+
 // ============================================================================
 // K1a: binning geometry only (critical path of the frame): per (view,
 // primitive) cull, tile rect and depth key from 40 B of parameters.
@@ -153,11 +198,14 @@ __global__ void __launch_bounds__(kGeomThreads) k_bin_geom(ProjectArgs a, CamBat
                         }
                         if (g.zmin > L) L = g.zmin;
                         dep = __float_as_uint(__double2float_rd(L));
+                        if (a.tight) tight_geom(cam, g, aq, a.tight + 4 * o);
                     }
                 }
             }
             a.rects[o] = rect;
             a.depth[o] = dep;
+            if (i == 0 && a.intr)
+                a.intr[view] = make_float4((float)(1.0 / (double)cam.fx), (float)(1.0 / (double)cam.fy), cam.cx, cam.cy);
             n_vis += keep;
         }
     }

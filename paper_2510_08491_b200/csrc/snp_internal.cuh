@@ -67,6 +67,7 @@ __host__ __device__ constexpr int rec_f4(int N) { return 6 + N + N / 4; }
 // the fp32 lower bound L truncated to 11 mantissa bits (still a lower bound, R19).
 constexpr int kDepthBits = 19;
 constexpr int kDepthDrop = 12;
+constexpr uint64_t kDeadKey = ~0ull;   // K2, tight binning: a key of a tile the silhouette misses
 __host__ __device__ __forceinline__ float key_depth(uint64_t key) {
     const uint32_t c = ((uint32_t)key & ((1u << kDepthBits) - 1u)) << kDepthDrop;
 #ifdef __CUDA_ARCH__
@@ -123,6 +124,8 @@ enum Counter { kCntVisible = 0, kCntDup = 1, kCntCapOverflow = 2, kCntTested = 3
                kCntBwdQueue3 = 50,      // K7: pixels for the global-memory pass
                kCntGradEntries = 51,    // K5 grad mode: entry chunks reserved
                kCntGradOverflow = 52,   // K5 grad mode: the entry buffer overflowed
+               kCntDeadKeysAcc = 53,    // K2, tight binning: keys of tiles the silhouette misses
+               kCntDeadKeys = 54,       //   (moved here by K4, which clears the accumulator)
                kNumCounters = 56 };     // 16..47: instrumented (A/B) builds only, cleared by the debug readback
 
 struct ProjectArgs {
@@ -135,6 +138,8 @@ struct ProjectArgs {
     int32_t tiles_x, tiles_y;
     short4 *rects;          // [V*n] tile rect or (-1,-1,-1,-1)
     uint32_t *depth;        // [V*n] fp32 bits of the depth lower bound
+    float4 *tight;          // [V*n][4] tight binning data (nullptr: rect binning), see k_bin_geom
+    float4 *intr;           // [V] (1/fx, 1/fy, cx, cy) for K2's per-tile depth bounds (with tight)
     float4 *records;        // [V*n*16]
     unsigned long long *counters;
 };
@@ -154,6 +159,9 @@ struct BinArgs {
     int32_t row_begin, row_stride;
     const short4 *rects;    // [V*n]
     const uint32_t *depth;  // [V*n]
+    const float4 *tight;    // [V*n][4] or nullptr (SURVEY 8(f)3 tight binning, bin_flags)
+    const float4 *intr;     // [V] (1/fx, 1/fy, cx, cy)
+    int32_t bin_flags;      // SNP_BIN_CONIC_TILES | SNP_BIN_TILE_DEPTH
     uint64_t *keys;         // [capacity]
     uint32_t *vals;         // [capacity]
     int64_t capacity;

@@ -18,7 +18,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kIpt = 12;                     // keys per thread
+#ifndef SNP_SORT_IPT
+#define SNP_SORT_IPT 12
+#endif
+constexpr int kIpt = SNP_SORT_IPT;           // keys per thread
 constexpr int kPart = kThreads * kIpt;       // 3072 keys per partition
 constexpr int kWarpKeys = kPart / kWarps;    // 384 keys per warp (warp-striped)
 constexpr uint32_t kFlagAgg = 1u << 30;

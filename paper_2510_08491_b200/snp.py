@@ -25,12 +25,14 @@ SNP_MEM_DEVICE = 1
 SNP_MEM_HOST_ASYNC = 2   # snp_render output only: copy enqueued on the stream, no synchronisation
 SNP_COLOUR_PRIMITIVE = 0  # colour_mode: SH at normalize(mu - C) per primitive and view (default)
 SNP_COLOUR_RAY = 1        # colour_mode: SH at each pixel's ray direction
+SNP_BIN_CONIC_TILES = 1   # snp_set_binning: drop rect tiles the silhouette ellipse misses
+SNP_BIN_TILE_DEPTH = 2    # snp_set_binning: per-tile depth lower bounds in the keys
 
 EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project", "snp_bin_sort", "snp_render",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
            "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at",
            "snp_render_backward", "snp_loss_l1", "snp_scale_regularizer", "snp_adam_step", "snp_get_params",
-           "snp_set_temporal_grad", "snp_loss_3dgs", "snp_render_backward_ex")
+           "snp_set_temporal_grad", "snp_loss_3dgs", "snp_render_backward_ex", "snp_set_binning")
 
 
 class SnpError(RuntimeError):
@@ -60,7 +62,8 @@ class RenderOpts(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(f, C.c_uint64) for f in ("n_visible", "n_dup", "key_capacity", "tested_pairs",
                                           "candidate_pairs", "hit_pairs", "composited",
-                                          "overflow_pixels", "capacity_overflow", "backward_skipped")]
+                                          "overflow_pixels", "capacity_overflow", "backward_skipped",
+                                          "dead_keys")]
 
 
 _lock = threading.Lock()
@@ -89,6 +92,7 @@ def lib():
             L.snp_get_binning.argtypes = [vp, vp, vp, vp, vp, C.c_int64, C.POINTER(C.c_int64), vp, vp]
             L.snp_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
+            L.snp_set_binning.argtypes = [vp, C.c_int32]
             L.snp_set_temporal.argtypes = [vp, vp, C.c_int32, vp]
             L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
             L.snp_render_backward_ex.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
@@ -302,6 +306,11 @@ def destroy(h):
 
 def set_pending_limit(h, k):
     _check(lib().snp_set_pending_limit(h, int(k)))
+
+
+def set_binning(h, flags):
+    """snp_set_binning: SNP_BIN_CONIC_TILES | SNP_BIN_TILE_DEPTH (0 = rect binning)."""
+    _check(lib().snp_set_binning(h, int(flags)))
 
 
 def get_debug_counters(h, n=56, stream=None):

@@ -1060,3 +1060,69 @@ def test_repeated_renders_bit_identical():
                 assert torch.equal(out, ref), cfg
         finally:
             snp.destroy(h)
+
+
+def _render_with_binning(scene, cams, bg, flags, colour_mode=0):
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    h = snp.create_scene(torch_scene(scene), 0)
+    try:
+        snp.set_binning(h, flags)
+        V, H, W = len(cams), cams[0].height, cams[0].width
+        out = torch.zeros((V, H, W, 4), device="cuda")
+        snp.render_views(h, cams, snp.make_opts(bg, colour_mode=colour_mode), out)
+        torch.cuda.synchronize()
+        return out.cpu().numpy(), snp.get_stats(h)
+    finally:
+        snp.destroy(h)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "elongated"])
+def test_tight_binning(orc, cfg):
+    """§8(f)3 tight binning (snp_set_binning).  SNP_BIN_CONIC_TILES drops only tiles whose
+    pixel centres the silhouette ellipse misses: the frame equals the rect binning's (up to
+    an ulp on pixels that moved between K5 and K6), with fewer tested pairs.  With
+    SNP_BIN_TILE_DEPTH as well (per-tile depth bounds: the per-ray order is unchanged, only
+    when hits are emitted) the frame stays within the parity tolerance of the oracle."""
+    if cfg == "elongated":   # thin diagonal primitives: their rects are mostly empty
+        rng = np.random.default_rng(12)
+        scene = synth.make_scene(12, 3000, box=0.8)
+        s = rng.uniform(0.004, 0.01, (3000, 3)).astype(np.float32)
+        s[:, 0] = rng.uniform(0.08, 0.25, 3000).astype(np.float32)
+        scene.scales[:] = s
+        cams = synth.orbit_cameras(2, 3.0, 320, 240, 300.0)
+        bg = (0.1, 0.2, 0.3)
+    else:
+        scene, cams, bg = synth.make_config(cfg)
+    ref, st0 = _render_with_binning(scene, cams, bg, 0)
+    con, st1 = _render_with_binning(scene, cams, bg, 1)
+    both, st3 = _render_with_binning(scene, cams, bg, 3)
+    print(cfg, "dead keys", st1["dead_keys"], "of", st1["n_dup"], "tested", st0["tested_pairs"], "->",
+          st1["tested_pairs"], "overflow", st0["overflow_pixels"], st1["overflow_pixels"], st3["overflow_pixels"])
+    assert st0["dead_keys"] == 0 and st1["dead_keys"] > 0 and st1["n_dup"] == st0["n_dup"]
+    # No hit is lost: the frame equals the rect binning's except for pixels that moved
+    # between K5 and K6 (fewer records per batch move K5's emission points, and with them
+    # which pixels overflow; the two paths may round the blend an ulp apart) -- and so do
+    # K5's counters, which count an overflowing pixel's hits twice
+    d = np.abs(con - ref)
+    assert d.max() <= 2.5e-7 and (d.max(-1) > 0).sum() <= 4 * max(st0["overflow_pixels"], st1["overflow_pixels"]), \
+        (d.max(), (d.max(-1) > 0).sum())
+    assert st1["tested_pairs"] < st0["tested_pairs"]
+    assert st3["dead_keys"] == st1["dead_keys"]
+    assert np.abs(both - ref).max() <= 1e-5, np.abs(both - ref).max()
+    # (and the oracle on the first view)
+    img_o, fl, _ = orc.render_frame(scene, cams[0], bg)
+    cmp_ = compare(both[0].reshape(-1, 4), img_o.reshape(-1, 4), fl.ravel())
+    assert cmp_["max_unflagged"] <= TOL, cmp_
+
+
+def test_tight_binning_deep_overlap(orc):
+    """Tight binning on the deep-overlap scene (600 hits per pixel, K6 and the long pending
+    lists): the per-tile depth bounds change when hits are emitted, never which or in
+    what order, so the frame matches the rect binning's within 1e-5."""
+    scene = _deep_scene(600)
+    cam = synth.look_at((0, 0, 0), (1, 0, 0), 32, 24, 1600.0)
+    ref, st0 = _render_with_binning(scene, [cam], (0.0, 0.0, 0.0), 0)
+    both, st3 = _render_with_binning(scene, [cam], (0.0, 0.0, 0.0), 3)
+    assert np.abs(both - ref).max() <= 1e-5

@@ -11,6 +11,7 @@ ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--views", type=int, default=0)
 ap.add_argument("--plimit", type=int, default=0)
 ap.add_argument("--n-hidden", type=int, default=8)
+ap.add_argument("--bin-flags", type=int, default=0)   # snp_set_binning (tight binning, 8(f)3)
 args = ap.parse_args()
 scene, cams, bg = synth.make_config(args.config, views=args.views or None, n_hidden=args.n_hidden)
 ns = types.SimpleNamespace(omega=scene.omega, sh_degree=scene.sh_degree)
@@ -19,6 +20,8 @@ for f in snp.FIELDS:
 h = snp.create_scene(ns, 0)
 if args.plimit:
     snp.set_pending_limit(h, args.plimit)
+if args.bin_flags:
+    snp.set_binning(h, args.bin_flags)
 out = torch.empty((len(cams), cams[0].height, cams[0].width, 4), device="cuda")
 snp.render_views(h, cams, snp.make_opts(bg, sync_check=1), out)
 opts = snp.make_opts(bg, sync_check=0)
