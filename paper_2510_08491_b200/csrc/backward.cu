@@ -1048,7 +1048,7 @@ __global__ void __launch_bounds__(1024) k_key_apply(uint32_t *cnt, int64_t nk, c
 // (lanes with equal keys -- neighbouring pixels' hits of one primitive -- share one atomic)
 template <bool kScatter>
 __global__ void __launch_bounds__(256) k_entry_count(RenderArgs a, uint32_t *__restrict__ key_cnt,
-                                                     uint32_t *__restrict__ sorted) {
+                                                     uint32_t *__restrict__ sorted, int64_t nk) {
     int64_t nc = (int64_t)a.counters[kCntGradEntries];
     if (nc > a.grad_chunks) nc = a.grad_chunks;
     if (a.counters[kCntGradOverflow]) nc = 0;
@@ -1058,6 +1058,7 @@ __global__ void __launch_bounds__(256) k_entry_count(RenderArgs a, uint32_t *__r
         const int64_t i = i0 + threadIdx.x;   // (warp-uniform trip count: i0 steps by whole blocks)
         const bool used = i < n && (int)(i & (kGradChunk - 1)) < a.grad_fill[i / kGradChunk];
         const uint32_t key = used ? a.grad_keys[i] : 0xffffffffu;
+        SNP_CHECK(!used || (int64_t)key < nk);
         const uint32_t peers = __match_any_sync(0xffffffffu, key);
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
@@ -1067,6 +1068,7 @@ __global__ void __launch_bounds__(256) k_entry_count(RenderArgs a, uint32_t *__r
         }
         if (kScatter) {
             base = __shfl_sync(0xffffffffu, base, leader);
+            SNP_CHECK(!used || (int64_t)(base + __popc(peers)) <= (int64_t)a.grad_chunks * kGradChunk);
             if (used) sorted[base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)i;
         }
     }
@@ -1150,11 +1152,11 @@ cudaError_t launch_grad_entries_n(const RenderArgs &a, const CamBatch &cb, const
         const int64_t nk = (int64_t)cb.nv * a.n;
         const int64_t nb = (nk + kScanPer - 1) / kScanPer;
         if (nb == 0) return cudaSuccess;   // (no primitives: no entries)
-        k_entry_count<false><<<(unsigned)(sms * 8), 256, 0, st>>>(a, a.grad_count, nullptr);
+        k_entry_count<false><<<(unsigned)(sms * 8), 256, 0, st>>>(a, a.grad_count, nullptr, nk);
         k_key_sums<<<(unsigned)nb, 1024, 0, st>>>(a.grad_count, nk, es->bsum);
         k_key_top<<<1, 1024, 0, st>>>(es->bsum, nb, es->cnt);
         k_key_apply<<<(unsigned)nb, 1024, 0, st>>>(a.grad_count, nk, es->bsum);
-        k_entry_count<true><<<(unsigned)(sms * 8), 256, 0, st>>>(a, a.grad_count, es->sorted);
+        k_entry_count<true><<<(unsigned)(sms * 8), 256, 0, st>>>(a, a.grad_count, es->sorted, nk);
         k_grad_sorted<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, es->sorted, es->cnt, g, omega);
     } else {
         k_grad_entries<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, a.grad_entries, g, omega);

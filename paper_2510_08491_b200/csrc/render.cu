@@ -152,14 +152,13 @@ struct PixelState {
 struct GradCtx {
     float4 G, F;
     GradEntry *chunk;     // this warp's current chunk of a.grad_entries (nullptr: none)
-    int *cnt;             // its fill count (shared atomics)
+    int *cnt;             // its fill count (shared; read and written warp-synchronously)
     uint32_t pix;         // view within the batch << 24 | y * W + x
 };
 
-template <int N, bool kRay, bool kGrad = false>
+template <int N, bool kRay>
 __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, float L, float t_floor,
-                                     const float4 *recs, const RenderArgs &a, const Ray &ray,
-                                     GradCtx *gx = nullptr) {
+                                     const float4 *recs, const RenderArgs &a, const Ray &ray) {
     const int tid = threadIdx.x;
     int n = pd.n;
     int h = pd.head;
@@ -180,38 +179,10 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
             break;
         }
         const float4 rgb = hit_rgb<kRay>(recs + (size_t)pid * rec_f4(N), a.sh, a.sh_degree, pid, ray);
-        const float Tb = ps.T;
-        const float w = Tb * kap;
+        const float w = ps.T * kap;
         ps.cr = fmaf(w, rgb.y, ps.cr);
         ps.cg = fmaf(w, rgb.z, ps.cg);
         ps.cb = fmaf(w, rgb.w, ps.cb);
-        if (kGrad) {
-            // out = sum_j T_j k_j c_j + T_end bg, so the light behind this hit is
-            // U = out - (colour accumulated up to and including it); then (K7's formulas)
-            // dL/dk = G_rgb . (T c - U / (1 - k)) + G_a T_end / (1 - k), dL/dI = (1 - k) dL/dk
-            // for I > 0 (Eq. 9), dL/dc = T k G_rgb on unclamped channels
-            const float4 G = gx->G, F = gx->F;
-            if (G.x != 0.f || G.y != 0.f || G.z != 0.f || G.w != 0.f) {
-                const float om = fmaxf(1.0f - kap, 1e-20f), iom = 1.0f / om;
-                float dk = G.w * (1.0f - F.w) * iom;
-                dk = fmaf(G.x, fmaf(-(F.x - ps.cr), iom, Tb * rgb.y), dk);
-                dk = fmaf(G.y, fmaf(-(F.y - ps.cg), iom, Tb * rgb.z), dk);
-                dk = fmaf(G.z, fmaf(-(F.z - ps.cb), iom, Tb * rgb.w), dk);
-                GradEntry e;
-                e.pix = gx->pix;
-                e.id = pid;
-                e.gI = kap > 0.f ? dk * (1.0f - kap) : 0.f;
-                e.gc0 = rgb.y > 0.f ? w * G.x : 0.f;
-                e.gc1 = rgb.z > 0.f ? w * G.y : 0.f;
-                e.gc2 = rgb.w > 0.f ? w * G.z : 0.f;
-                const int slot = atomicAdd(gx->cnt, 1);
-                if (gx->chunk) {
-                    gx->chunk[slot] = e;
-                    if (a.grad_keys)   // K7s's counting sort key
-                        a.grad_keys[(gx->chunk - a.grad_entries) + slot] = (gx->pix >> 24) * (uint32_t)a.n + pid;
-                }
-            }
-        }
         ps.T *= (1.0f - kap);
         ++ps.composited;
         --n;
@@ -221,6 +192,94 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
             break;
         }
     }
+    pd.n = n;
+    pd.head = h;
+}
+
+// K5 grad mode's emission: the same blend (same order and arithmetic), warp-synchronous
+// (every lane of the warp calls it; `active` = this lane's pixel emits) so that the
+// entries' chunk slots come from a ballot instead of shared-memory atomics.  Each
+// composited hit of a pixel with a nonzero dL/d(out) becomes a GradEntry:
+// out = sum_j T_j k_j c_j + T_end bg, so the light behind this hit is U = out - (colour
+// accumulated up to and including it); then (K7's formulas) dL/dk = G_rgb . (T c -
+// U / (1 - k)) + G_a T_end / (1 - k), dL/dI = (1 - k) dL/dk for I > 0 (Eq. 9),
+// dL/dc = T k G_rgb on unclamped channels.
+template <int N, bool kRay>
+__device__ __forceinline__ void emit_grad(Smem<N> &sm, PixelState &ps, Pending &pd, bool active, float L,
+                                          float t_floor, const float4 *recs, const RenderArgs &a, const Ray &ray,
+                                          GradCtx &gx) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int n = pd.n;
+    int h = pd.head;
+    bool more = active && n > 0;
+    int fill = *gx.cnt;   // (warp-uniform: grad_reserve synchronised the warp)
+    const bool has_g = gx.G.x != 0.f || gx.G.y != 0.f || gx.G.z != 0.f || gx.G.w != 0.f;
+    while (__any_sync(0xffffffffu, more)) {
+        bool write = false;
+        GradEntry e{};
+        if (more) {
+            const float t = sm.p_thi[h][tid];
+            if (!(t < L)) {
+                more = false;
+            } else {
+                const float kap = sm.p_kap[h][tid];
+                const uint32_t word = sm.p_id[h][tid];
+                const uint32_t pid = word & kIdMask;
+                SNP_CHECK(h >= 0 && h < kPend && n <= kPend && (int64_t)pid < a.n);
+                const int gexp = (int)((word >> 24) & 7u);
+                if (gexp && (gexp == 7 || ps.T * (float)(1 << gexp) > 2.0f)) {   // -> K7 per pixel
+                    atomicAdd(a.counters + kCntGraze, 1ull);
+                    ps.overflow = true;
+                    ps.done = true;
+                    more = false;
+                } else {
+                    const float4 rgb = hit_rgb<kRay>(recs + (size_t)pid * rec_f4(N), a.sh, a.sh_degree, pid, ray);
+                    const float Tb = ps.T;
+                    const float w = Tb * kap;
+                    ps.cr = fmaf(w, rgb.y, ps.cr);
+                    ps.cg = fmaf(w, rgb.z, ps.cg);
+                    ps.cb = fmaf(w, rgb.w, ps.cb);
+                    if (has_g) {
+                        const float4 G = gx.G, F = gx.F;
+                        const float om = fmaxf(1.0f - kap, 1e-20f), iom = 1.0f / om;
+                        float dk = G.w * (1.0f - F.w) * iom;
+                        dk = fmaf(G.x, fmaf(-(F.x - ps.cr), iom, Tb * rgb.y), dk);
+                        dk = fmaf(G.y, fmaf(-(F.y - ps.cg), iom, Tb * rgb.z), dk);
+                        dk = fmaf(G.z, fmaf(-(F.z - ps.cb), iom, Tb * rgb.w), dk);
+                        e.pix = gx.pix;
+                        e.id = pid;
+                        e.gI = kap > 0.f ? dk * (1.0f - kap) : 0.f;
+                        e.gc0 = rgb.y > 0.f ? w * G.x : 0.f;
+                        e.gc1 = rgb.z > 0.f ? w * G.y : 0.f;
+                        e.gc2 = rgb.w > 0.f ? w * G.z : 0.f;
+                        write = true;
+                    }
+                    ps.T *= (1.0f - kap);
+                    ++ps.composited;
+                    --n;
+                    h = (h + 1) & (kPend - 1);
+                    if (ps.T < t_floor) {
+                        ps.done = true;
+                        more = false;
+                    }
+                    if (n == 0) more = false;
+                }
+            }
+        }
+        const uint32_t wm = __ballot_sync(0xffffffffu, write);
+        if (write) {
+            const int slot = fill + __popc(wm & lt_mask);
+            SNP_CHECK(slot >= 0 && slot < kGradChunk);
+            if (gx.chunk) {
+                gx.chunk[slot] = e;
+                if (a.grad_keys)   // K7s's counting sort key
+                    a.grad_keys[(gx.chunk - a.grad_entries) + slot] = (gx.pix >> 24) * (uint32_t)a.n + e.id;
+            }
+        }
+        fill += __popc(wm);
+    }
+    if (lane == 0) *gx.cnt = fill;
     pd.n = n;
     pd.head = h;
 }
@@ -586,8 +645,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 float th = 0.f, tl = 0.f, kap = 0.f;
                 SNP_CHECK(!valid || (j < cnt && owner < 32));
                 const uint32_t idj = sm.id[slot][j];
+
                 if (valid)
                     hit = exact_hit<N, kGrazeDefer>(&sm.rec[slot][j][0], ro, th, tl, kap, nullptr, idj, &graze, &gexp);
+
                 n_hit += hit;
 #ifdef SNP_INSTRUMENT
                 long long _i0 = clock64();
@@ -695,16 +756,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch c
                 // kEager: after every exact round -- shorter pending lists (fewer K6
                 // pixels), earlier termination; chosen per scene from the overflow rate
                 const bool do_emit = !ps.done && (batch_end || pd.n > (kEager ? 0 : plimit - 4));
-                if (kGrad) grad_reserve(__reduce_add_sync(0xffffffffu, do_emit ? (uint32_t)pd.n : 0u));
-                if (do_emit) {
+                if (kGrad) {
+                    grad_reserve(__reduce_add_sync(0xffffffffu, do_emit ? (uint32_t)pd.n : 0u));
+                    emit_grad<N, kRay>(sm, ps, pd, do_emit,
+                                       batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                                       a.t_floor, recs, a, ray, gx);
+                } else if (do_emit) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
                     ++ins_ecalls;
                     ins_enone += (pd.n == 0);
 #endif
-                    emit<N, kRay, kGrad>(sm, ps, pd,
-                                         batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
-                                         a.t_floor, recs, a, ray, &gx);
+                    emit<N, kRay>(sm, ps, pd,
+                                  batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                                  a.t_floor, recs, a, ray);
 #ifdef SNP_INSTRUMENT
                     ins_emit += clock64() - _e0;
 #endif
