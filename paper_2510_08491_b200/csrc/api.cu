@@ -124,6 +124,7 @@ struct snp_scene_s {
     // after K1a and joined at the end of snp_bin_sort (also under stream capture)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_bw_fork = nullptr, ev_bw_join = nullptr;   // backward: K7s beside the per-pixel K7
     bool join_pending = false;
     bool render_dirty = false;       // a render has used the counters since the last binning
     // K5's eager mid-batch emission: set by a synchronising snp_bin_sort when the tile
@@ -261,6 +262,8 @@ snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stre
     if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
     if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
     if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&s->ev_bw_fork, cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&s->ev_bw_join, cudaEventDisableTiming);
     if (ce != cudaSuccess) {
         snp_destroy(s);
         return fail(ce == cudaErrorMemoryAllocation ? SNP_ERR_OUT_OF_MEMORY : SNP_ERR_CUDA,
@@ -699,7 +702,7 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
         RenderArgs a = render_args(s, opts);
         a.bw_queue = s->bw_queue.p;
         for (const CamBatch &cb : s->cams)
-            SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, s->bw_scratch.p, false, nullptr, st));
+            SNP_CUDA(launch_backward(a, cb, grad_rgba, g, s->omega, s->bw_scratch.p, false, nullptr, st, st));
         return SNP_OK;
     }
     // the forward result the gradients refer to (the caller's, or rendered here)
@@ -761,8 +764,15 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
         SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGradEntries, 0, 2 * sizeof(unsigned long long), st));
         a.tile_order = s->tile_order.p + k * order_stride;
         if (s->n > 0) SNP_CUDA(launch_render_grad(a, s->cams[k], st));
-        // K7f over the entries, then the per-pixel K7 for the pixels K5 queued
-        SNP_CUDA(launch_backward(a, s->cams[k], grad_rgba, g, s->omega, s->bw_scratch.p, true, unsorted ? nullptr : &es, st));
+        // K7s over the entries, and beside it (side stream) the per-pixel K7 for the pixels
+        // K5 queued (latency-bound long pixels: they overlap K7s; joined before the next
+        // batch reuses the queue)
+        SNP_CUDA(cudaEventRecord(s->ev_bw_fork, st));
+        SNP_CUDA(cudaStreamWaitEvent(s->side, s->ev_bw_fork, 0));
+        SNP_CUDA(launch_backward(a, s->cams[k], grad_rgba, g, s->omega, s->bw_scratch.p, true, unsorted ? nullptr : &es,
+                                 st, s->side));
+        SNP_CUDA(cudaEventRecord(s->ev_bw_join, s->side));
+        SNP_CUDA(cudaStreamWaitEvent(st, s->ev_bw_join, 0));
     }
     return SNP_OK;
 }
@@ -877,6 +887,8 @@ snp_status snp_destroy(snp_scene s) {
     cudaDeviceSynchronize();
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->ev_bw_fork) cudaEventDestroy(s->ev_bw_fork);
+    if (s->ev_bw_join) cudaEventDestroy(s->ev_bw_join);
     if (s->side) cudaStreamDestroy(s->side);
     s->params.release();
     s->rects.release();

@@ -1167,14 +1167,15 @@ cudaError_t launch_grad_entries_n(const RenderArgs &a, const CamBatch &cb, const
 
 template <int N>
 cudaError_t launch_backward_w(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                              float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st) {
+                              float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st,
+                              cudaStream_t st_pix) {
     if (k5) {
         cudaError_t e = a.colour_ray ? launch_grad_entries_n<N, true>(a, cb, g, omega, es, st)
                                      : launch_grad_entries_n<N, false>(a, cb, g, omega, es, st);
         if (e != cudaSuccess) return e;
     }
-    return a.colour_ray ? launch_backward_n<N, true>(a, cb, grad, g, omega, scratch, k5, st)
-                        : launch_backward_n<N, false>(a, cb, grad, g, omega, scratch, k5, st);
+    return a.colour_ray ? launch_backward_n<N, true>(a, cb, grad, g, omega, scratch, k5, st_pix)
+                        : launch_backward_n<N, false>(a, cb, grad, g, omega, scratch, k5, st_pix);
 }
 
 }  // namespace
@@ -1182,12 +1183,13 @@ cudaError_t launch_backward_w(const RenderArgs &a, const CamBatch &cb, const flo
 size_t backward_scratch_bytes() { return (size_t)kBwHugeCtas * sizeof(BwSmem<1, kBwHugeHits>); }
 
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st) {
+                            float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st,
+                            cudaStream_t st_pix) {
     switch (a.n_hidden) {
-        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, scratch, k5, es, st);
-        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, scratch, k5, es, st);
-        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, scratch, k5, es, st);
-        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, scratch, k5, es, st);
+        case 4: return launch_backward_w<4>(a, cb, grad, g, omega, scratch, k5, es, st, st_pix);
+        case 8: return launch_backward_w<8>(a, cb, grad, g, omega, scratch, k5, es, st, st_pix);
+        case 16: return launch_backward_w<16>(a, cb, grad, g, omega, scratch, k5, es, st, st_pix);
+        case 32: return launch_backward_w<32>(a, cb, grad, g, omega, scratch, k5, es, st, st_pix);
         default: return cudaErrorInvalidValue;
     }
 }

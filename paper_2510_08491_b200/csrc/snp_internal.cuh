@@ -279,10 +279,12 @@ struct EntrySort {
     uint32_t *sorted;              // [grad_chunks * kGradChunk] entry slots in key order
     unsigned long long *cnt;       // cnt[kCntDup] = entries
 };
-// k5: K7f (es: sorted, K7s; nullptr: in slot order) over the K5 entries, then the
-// per-pixel K7 for the pixels K5 queued; !k5: the per-pixel K7 for every pixel
+// k5: K7f (es: sorted, K7s; nullptr: in slot order) over the K5 entries on st, and the
+// per-pixel K7 for the pixels K5 queued on st_pix (the caller forks and joins; st_pix may
+// be st); !k5: the per-pixel K7 for every pixel (on st_pix)
 cudaError_t launch_backward(const RenderArgs &a, const CamBatch &cb, const float *grad, const BackwardGrads &g,
-                            float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st);
+                            float omega, void *scratch, bool k5, const EntrySort *es, cudaStream_t st,
+                            cudaStream_t st_pix);
 // K5 in grad mode over one camera batch (render.cu): the forward traversal emitting
 // GradEntry per composited hit; overflowing pixels go to bw_queue with their skip count
 cudaError_t launch_render_grad(const RenderArgs &a, const CamBatch &cams, cudaStream_t st);
