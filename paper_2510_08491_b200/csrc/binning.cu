@@ -140,6 +140,7 @@ __device__ __forceinline__ float tile_depth_bound(const float4 &f1, const float4
     return (um - r) - 4e-6f * (fabsf(um) + r) - 1e-30f;
 }
 
+template <bool kTight>   // tight binning (a.tight) in its own instantiation: the default one is unchanged
 __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
     pdl_prologue();
     __shared__ uint32_t sw[32];
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
         const uint64_t tile = (uint64_t)row * (uint64_t)a.tiles_x + (uint64_t)(s_x0[lo] + c);
         SNP_CHECK(lo >= i0 && lo < i0 + 32 * kScanItems && row < a.tiles_y && s_x0[lo] + c < a.tiles_x);
         uint64_t key = (view << view_shift) | (tile << kDepthBits) | (uint64_t)s_dep[lo];
-        if (a.tight) {   // tight binning: drop tiles the silhouette misses, per-tile depth bounds
+        if (kTight) {   // tight binning: drop tiles the silhouette misses, per-tile depth bounds
             const float4 *t4 = a.tight + 4 * o;
             const float4 f3 = __ldg(t4 + 3);
             if (f3.z != 0.f) {
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dup(BinArgs a) {
             for (int p = 0; p < a.passes; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
         }
     }
-    if (a.tight) {
+    if (kTight) {
         const uint32_t d = __reduce_add_sync(0xffffffffu, n_dead);
         if (lane == 0 && d) atomicAdd(a.counters + kCntDeadKeysAcc, (unsigned long long)d);
     }
@@ -319,7 +320,8 @@ cudaError_t launch_dup(const BinArgs &a, cudaStream_t st) {
         if (a.n_slots > 0) e = cudaMemsetAsync(a.ranges, 0, sizeof(uint32_t) * 2 * (size_t)a.n_slots, st);
         return e;
     }
-    cudaError_t e0 = launch_hi(k_scan_dup, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a);
+    cudaError_t e0 = a.tight ? launch_hi(k_scan_dup<true>, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a)
+                             : launch_hi(k_scan_dup<false>, dim3((unsigned)nb), dim3(kScanThreads), 0, st, a);
     if (e0 != cudaSuccess) return e0;
     return cudaGetLastError();
 }

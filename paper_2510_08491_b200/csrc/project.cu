@@ -122,6 +122,7 @@ __device__ __forceinline__ void tight_geom(const DevCam &cam, const Geom &g, dou
 // primitive) cull, tile rect and depth key from 40 B of parameters.
 constexpr int kGeomThreads = 256;
 
+template <bool kTight>   // tight binning data (a.tight) in its own instantiation
 __global__ void __launch_bounds__(kGeomThreads) k_bin_geom(ProjectArgs a, CamBatch cb) {
     const int64_t i = (int64_t)blockIdx.x * kGeomThreads + threadIdx.x;
     unsigned long long n_vis = 0;
@@ -198,13 +199,13 @@ __global__ void __launch_bounds__(kGeomThreads) k_bin_geom(ProjectArgs a, CamBat
                         }
                         if (g.zmin > L) L = g.zmin;
                         dep = __float_as_uint(__double2float_rd(L));
-                        if (a.tight) tight_geom(cam, g, aq, a.tight + 4 * o);
+                        if (kTight) tight_geom(cam, g, aq, a.tight + 4 * o);
                     }
                 }
             }
             a.rects[o] = rect;
             a.depth[o] = dep;
-            if (i == 0 && a.intr)
+            if (kTight && i == 0)
                 a.intr[view] = make_float4((float)(1.0 / (double)cam.fx), (float)(1.0 / (double)cam.fy), cam.cx, cam.cy);
             n_vis += keep;
         }
@@ -264,7 +265,9 @@ cudaError_t launch_validate_finite(const float *v, int64_t count, int *d_bad, cu
 
 cudaError_t launch_bin_geom(const ProjectArgs &a, const CamBatch &cams, cudaStream_t st) {
     if (a.n == 0) return cudaSuccess;
-    k_bin_geom<<<(unsigned)((a.n + kGeomThreads - 1) / kGeomThreads), kGeomThreads, 0, st>>>(a, cams);
+    const unsigned grid = (unsigned)((a.n + kGeomThreads - 1) / kGeomThreads);
+    if (a.tight) k_bin_geom<true><<<grid, kGeomThreads, 0, st>>>(a, cams);
+    else k_bin_geom<false><<<grid, kGeomThreads, 0, st>>>(a, cams);
     return cudaGetLastError();
 }
 
