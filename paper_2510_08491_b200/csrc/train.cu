@@ -77,91 +77,164 @@ constexpr int kWin = 11, kHalf = 5;
 struct Gauss {
     float w[kWin];
 };
-// maps are planar [V][planes][H][W]; separable blur with zero padding (dir 0: x, 1: y)
-__global__ void k_blur(const float *__restrict__ in, float *__restrict__ out, int64_t planes, int H, int W, int dir,
-                       Gauss g) {
-    const int64_t total = planes * (int64_t)H * W;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(i % W), y = (int)((i / W) % H);
-        const float *row = in + (i - (dir ? (int64_t)y * W : x));   // start of the column (dir 1) / row (dir 0)
-        float acc = 0.f;
-#pragma unroll
-        for (int k = -kHalf; k <= kHalf; ++k) {
-            const int c = (dir ? y : x) + k;
-            if (c >= 0 && c < (dir ? H : W)) acc = fmaf(g.w[k + kHalf], row[dir ? (int64_t)c * W : c], acc);
-        }
-        out[i] = acc;
-    }
-}
-// the 5 moment maps per channel: x, y, x^2, y^2, x y  ->  m[V][5][3][H][W]
-__global__ void k_ssim_moments(const float4 *__restrict__ out, const float *__restrict__ target, int V, int H, int W,
-                               float *__restrict__ m) {
-    const int64_t hw = (int64_t)H * W, total = (int64_t)V * hw;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / hw, p = i - v * hw;
-        const float4 o = out[i];
-        const float xs[3] = {o.x, o.y, o.z};
-        float *b = m + v * 15 * hw + p;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float x = xs[c], y = target[3 * i + c];
-            b[(0 * 3 + c) * hw] = x;
-            b[(1 * 3 + c) * hw] = y;
-            b[(2 * 3 + c) * hw] = x * x;
-            b[(3 * 3 + c) * hw] = y * y;
-            b[(4 * 3 + c) * hw] = x * y;
-        }
-    }
-}
-// per pixel and channel: SSIM s from the blurred moments mu[V][5][3][H][W]; its partial
-// derivatives w.r.t. (mu_x, E[x^2], E[xy]) into d[V][3][3][H][W]; sum of s into *ssum
-__global__ void k_ssim_map(const float *__restrict__ mu, int V, int H, int W, float *__restrict__ d, float *ssum) {
+// Fused, tiled D-SSIM (R25): a CTA takes a kTx x kTy tile of one view, loads x (the
+// render) and y (the target) of one channel at a time over the tile plus the 5-pixel
+// halo (zero outside the image: conv2d's zero padding), blurs the five moments x, y, x^2,
+// y^2, x y separably in shared memory (x pass over the halo rows, then y), and writes per
+// pixel the SSIM s's partial derivatives w.r.t. (mu_x, E[x^2], E[xy]) -- three maps per
+// channel -- while summing s and |x - y|.  k_ssim_back blurs those maps the same way and
+// forms dL/d(out).  Two passes over HBM instead of 24 planar blur passes.
+constexpr int kTx = 32, kTy = 16, kHx = kTx + 2 * kHalf, kHy = kTy + 2 * kHalf;
+constexpr int kSsimThreads = 256;
+
+__global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const float4 *__restrict__ out,
+                                                           const float *__restrict__ target, int H, int W, Gauss g,
+                                                           float *__restrict__ d, float *sums) {
+    __shared__ float sx[kHy][kHx], sy[kHy][kHx];
+    __shared__ float hb[5][kHy][kTx];
+    const int v = blockIdx.z, x0 = blockIdx.x * kTx - kHalf, y0 = blockIdx.y * kTy - kHalf;
+    const int64_t hw = (int64_t)H * W;
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
-    const int64_t hw = (int64_t)H * W, total = (int64_t)V * 3 * hw;
-    float acc = 0.f;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / (3 * hw), r = i - v * 3 * hw;   // r = c * hw + p
-        const float *b = mu + v * 15 * hw + r;
-        const float mx = b[0], my = b[3 * hw], exx = b[6 * hw], eyy = b[9 * hw], exy = b[12 * hw];
-        const float n1 = 2.f * mx * my + C1, n2 = 2.f * (exy - mx * my) + C2;
-        const float d1 = mx * mx + my * my + C1, d2 = (exx - mx * mx) + (eyy - my * my) + C2;
-        const float sv = (n1 * n2) / (d1 * d2);
-        acc += sv;
-        float *o = d + v * 9 * hw + r;
-        o[0] = sv * (2.f * my / n1 - 2.f * my / n2 - 2.f * mx / d1 + 2.f * mx / d2);   // ds/dmu_x
-        o[3 * hw] = -sv / d2;                                                          // ds/dE[x^2]
-        o[6 * hw] = 2.f * sv / n2;                                                     // ds/dE[xy]
+    float ssum = 0.f, l1sum = 0.f;
+    for (int c = 0; c < 3; ++c) {
+        for (int i = threadIdx.x; i < kHx * kHy; i += kSsimThreads) {
+            const int r = i / kHx, q = i - r * kHx, gy = y0 + r, gx = x0 + q;
+            float xv = 0.f, yv = 0.f;
+            if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+                const int64_t pi = (int64_t)v * hw + (int64_t)gy * W + gx;
+                xv = reinterpret_cast<const float *>(out)[4 * pi + c];
+                yv = target[3 * pi + c];
+            }
+            sx[r][q] = xv;
+            sy[r][q] = yv;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kHy * kTx; i += kSsimThreads) {   // x pass
+            const int r = i / kTx, q = i - r * kTx;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                const float xv = sx[r][q + k], yv = sy[r][q + k], w = g.w[k];
+                a0 = fmaf(w, xv, a0);
+                a1 = fmaf(w, yv, a1);
+                a2 = fmaf(w, xv * xv, a2);
+                a3 = fmaf(w, yv * yv, a3);
+                a4 = fmaf(w, xv * yv, a4);
+            }
+            hb[0][r][q] = a0;
+            hb[1][r][q] = a1;
+            hb[2][r][q] = a2;
+            hb[3][r][q] = a3;
+            hb[4][r][q] = a4;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kTy * kTx; i += kSsimThreads) {   // y pass + SSIM
+            const int r = i / kTx, q = i - r * kTx, gy = y0 + kHalf + r, gx = x0 + kHalf + q;
+            if (gy >= H || gx >= W) continue;
+            float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                const float w = g.w[k];
+#pragma unroll
+                for (int j = 0; j < 5; ++j) m[j] = fmaf(w, hb[j][r + k][q], m[j]);
+            }
+            const float mx = m[0], my = m[1], exx = m[2], eyy = m[3], exy = m[4];
+            const float n1 = 2.f * mx * my + C1, n2 = 2.f * (exy - mx * my) + C2;
+            const float d1 = mx * mx + my * my + C1, d2 = (exx - mx * mx) + (eyy - my * my) + C2;
+            const float sv = (n1 * n2) / (d1 * d2);
+            ssum += sv;
+            l1sum += fabsf(sx[r + kHalf][q + kHalf] - sy[r + kHalf][q + kHalf]);
+            float *o = d + ((int64_t)v * 9 + 3 * c) * hw + (int64_t)gy * W + gx;
+            o[0] = sv * (2.f * my / n1 - 2.f * my / n2 - 2.f * mx / d1 + 2.f * mx / d2);   // ds/dmu_x
+            o[hw] = -sv / d2;                                                              // ds/dE[x^2]
+            o[2 * hw] = 2.f * sv / n2;                                                     // ds/dE[xy]
+        }
+        __syncthreads();
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(ssum, acc);
+    for (int o = 16; o > 0; o >>= 1) {
+        ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+        l1sum += __shfl_xor_sync(0xffffffffu, l1sum, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(sums, ssum);
+        atomicAdd(sums + 1, l1sum);
+    }
 }
-// grad = (1 - lambda) dL1/dout - lambda / M (blur(ds/dmu) + 2 x blur(ds/dE[x^2]) + y blur(ds/dE[xy]));
-// loss += (1 - lambda) L1 (k_l1 with that weight) + lambda (1 - ssum / M), M = 3 V H W
-__global__ void k_ssim_grad(const float4 *__restrict__ out, const float *__restrict__ target, const float *__restrict__ bd,
-                            int V, int H, int W, float lam, float4 *__restrict__ grad) {
-    const int64_t hw = (int64_t)H * W, total = (int64_t)V * hw;
+
+// grad = (1 - lambda) dL1/dout - lambda / M (blur(ds/dmu) + 2 x blur(ds/dE[x^2]) + y blur(ds/dE[xy]))
+// (the blur is self-adjoint: same Gaussian, zero padding), M = 3 V H W
+__global__ void __launch_bounds__(kSsimThreads) k_ssim_back(const float4 *__restrict__ out,
+                                                            const float *__restrict__ target,
+                                                            const float *__restrict__ d, int H, int W, int64_t total,
+                                                            float lam, Gauss g, float4 *__restrict__ grad) {
+    __shared__ float sd[3][kHy][kHx];
+    __shared__ float hb[3][kHy][kTx];
+    const int v = blockIdx.z, x0 = blockIdx.x * kTx - kHalf, y0 = blockIdx.y * kTy - kHalf;
+    const int64_t hw = (int64_t)H * W;
     const float inv = 1.0f / (3.0f * (float)total);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / hw, p = i - v * hw;
-        const float4 o = out[i];
-        const float xs[3] = {o.x, o.y, o.z};
-        float g[3];
+    float gacc[2][3];   // (2 output pixels per thread)
+    for (int c = 0; c < 3; ++c) {
+        for (int i = threadIdx.x; i < kHx * kHy; i += kSsimThreads) {
+            const int r = i / kHx, q = i - r * kHx, gy = y0 + r, gx = x0 + q;
+            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            const float *b = d + ((int64_t)v * 9 + 3 * c) * hw + (int64_t)gy * W + gx;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float x = xs[c], y = target[3 * i + c];
-            const float *b = bd + v * 9 * hw + (int64_t)c * hw + p;
-            const float dssim = b[0] + 2.f * x * b[3 * hw] + y * b[6 * hw];
+            for (int m = 0; m < 3; ++m) sd[m][r][q] = in ? b[m * hw] : 0.f;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kHy * kTx; i += kSsimThreads) {
+            const int r = i / kTx, q = i - r * kTx;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                const float w = g.w[k];
+                a0 = fmaf(w, sd[0][r][q + k], a0);
+                a1 = fmaf(w, sd[1][r][q + k], a1);
+                a2 = fmaf(w, sd[2][r][q + k], a2);
+            }
+            hb[0][r][q] = a0;
+            hb[1][r][q] = a1;
+            hb[2][r][q] = a2;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int i = threadIdx.x + t * kSsimThreads;
+            const int r = i / kTx, q = i - r * kTx, gy = y0 + kHalf + r, gx = x0 + kHalf + q;
+            gacc[t][c] = 0.f;
+            if (gy >= H || gx >= W) continue;
+            float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                const float w = g.w[k];
+                b0 = fmaf(w, hb[0][r + k][q], b0);
+                b1 = fmaf(w, hb[1][r + k][q], b1);
+                b2 = fmaf(w, hb[2][r + k][q], b2);
+            }
+            const int64_t pi = (int64_t)v * hw + (int64_t)gy * W + gx;
+            const float x = reinterpret_cast<const float *>(out)[4 * pi + c], y = target[3 * pi + c];
+            const float dssim = b0 + 2.f * x * b1 + y * b2;
             const float dl = x - y;
             const float l1 = dl > 0.f ? inv : (dl < 0.f ? -inv : 0.f);
-            g[c] = (1.0f - lam) * l1 - lam * inv * dssim;
+            gacc[t][c] = (1.0f - lam) * l1 - lam * inv * dssim;
         }
-        grad[i] = make_float4(g[0], g[1], g[2], 0.f);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int i = threadIdx.x + t * kSsimThreads;
+        const int r = i / kTx, q = i - r * kTx, gy = y0 + kHalf + r, gx = x0 + kHalf + q;
+        if (gy < H && gx < W)
+            grad[(int64_t)v * hw + (int64_t)gy * W + gx] = make_float4(gacc[t][0], gacc[t][1], gacc[t][2], 0.f);
     }
 }
-__global__ void k_ssim_loss(const float *ssum, float *l1sum, int64_t total, float lam, float *loss) {
-    // (k_l1 accumulated the L1 mean into *l1sum)
-    if (threadIdx.x == 0) atomicAdd(loss, (1.0f - lam) * l1sum[0] + lam * (1.0f - ssum[0] / (3.0f * (float)total)));
+static_assert(kTx * kTy == 2 * kSsimThreads, "k_ssim_back: two output pixels per thread");
+
+__global__ void k_ssim_loss(const float *sums, int64_t total, float lam, float *loss) {
+    // sums[0] = sum of SSIM, sums[1] = sum of |x - y| over the 3 V H W values
+    const float m = 3.0f * (float)total;
+    if (threadIdx.x == 0) atomicAdd(loss, (1.0f - lam) * (sums[1] / m) + lam * (1.0f - sums[0] / m));
 }
 
 unsigned grid_for(int64_t n) {
@@ -196,15 +269,14 @@ cudaError_t launch_adam(float *p, const float *g, float *m, float *v, int64_t co
 }  // namespace snp
 
 namespace snp {
-size_t loss_3dgs_scratch_floats(int V, int H, int W) { return (size_t)V * H * W * (15 + 15 + 9 + 9) + 2; }
+size_t loss_3dgs_scratch_floats(int V, int H, int W) { return (size_t)V * H * W * 9 + 2; }
 
 cudaError_t launch_loss_3dgs(const float *out_rgba, const float *target_rgb, int V, int H, int W, float lam,
                              float *grad_rgba, float *loss, float *scratch, cudaStream_t st) {
     const int64_t total = (int64_t)V * H * W;
     if (total == 0) return cudaSuccess;
-    const int64_t hw = (int64_t)H * W;
-    float *m = scratch, *t = m + 15 * total, *d = t + 15 * total, *t2 = d + 9 * total;
-    float *sums = t2 + 9 * total;   // [0] = sum of SSIM, [1] = L1 mean
+    float *d = scratch;                      // [V][3 channels][3 maps][H][W]
+    float *sums = d + 9 * total;             // [0] = sum of SSIM, [1] = sum of |x - y|
     Gauss g{};
     double gs[kWin], tot = 0.0;
     for (int k = 0; k < kWin; ++k) {
@@ -214,20 +286,12 @@ cudaError_t launch_loss_3dgs(const float *out_rgba, const float *target_rgb, int
     for (int k = 0; k < kWin; ++k) g.w[k] = (float)(gs[k] / tot);
     cudaError_t e = cudaMemsetAsync(sums, 0, 2 * sizeof(float), st);
     if (e != cudaSuccess) return e;
-    const unsigned gp = grid_for(total), g15 = grid_for(15 * total), g9 = grid_for(9 * total), g3 = grid_for(3 * total);
-    k_ssim_moments<<<gp, 256, 0, st>>>(reinterpret_cast<const float4 *>(out_rgba), target_rgb, V, H, W, m);
-    k_blur<<<g15, 256, 0, st>>>(m, t, 15 * (int64_t)V, H, W, 0, g);
-    k_blur<<<g15, 256, 0, st>>>(t, m, 15 * (int64_t)V, H, W, 1, g);
-    k_ssim_map<<<g3, 256, 0, st>>>(m, V, H, W, d, sums);
-    k_blur<<<g9, 256, 0, st>>>(d, t2, 9 * (int64_t)V, H, W, 0, g);
-    k_blur<<<g9, 256, 0, st>>>(t2, d, 9 * (int64_t)V, H, W, 1, g);
-    // L1 mean into sums[1] (k_l1 writes a gradient we overwrite below)
-    k_l1<<<gp, 256, 0, st>>>(reinterpret_cast<const float4 *>(out_rgba), target_rgb, total,
-                             reinterpret_cast<float4 *>(grad_rgba), sums + 1);
-    k_ssim_grad<<<gp, 256, 0, st>>>(reinterpret_cast<const float4 *>(out_rgba), target_rgb, d, V, H, W, lam,
-                                    reinterpret_cast<float4 *>(grad_rgba));
-    k_ssim_loss<<<1, 32, 0, st>>>(sums, sums + 1, total, lam, loss);
-    (void)hw;
+    const dim3 grid((unsigned)((W + kTx - 1) / kTx), (unsigned)((H + kTy - 1) / kTy), (unsigned)V);
+    k_ssim_fwd<<<grid, kSsimThreads, 0, st>>>(reinterpret_cast<const float4 *>(out_rgba), target_rgb, H, W, g, d,
+                                              sums);
+    k_ssim_back<<<grid, kSsimThreads, 0, st>>>(reinterpret_cast<const float4 *>(out_rgba), target_rgb, d, H, W,
+                                               total, lam, g, reinterpret_cast<float4 *>(grad_rgba));
+    k_ssim_loss<<<1, 32, 0, st>>>(sums, total, lam, loss);
     return cudaGetLastError();
 }
 }  // namespace snp

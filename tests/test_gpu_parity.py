@@ -720,19 +720,23 @@ def _ssim_loss_torch(out, tgt, lam):
     return (1 - lam) * (x - y).abs().mean() + lam * (1 - ssim.mean())
 
 
-@pytest.mark.parametrize("lam", [0.2, 0.0, 1.0])
-def test_loss_3dgs_against_torch(lam):
+@pytest.mark.parametrize("lam,shape", [(0.2, (2, 29, 37)), (0.0, (2, 29, 37)), (1.0, (2, 29, 37)),
+                                       (0.2, (3, 70, 101)), (1.0, (1, 5, 7))])
+def test_loss_3dgs_against_torch(lam, shape):
     """snp_loss_3dgs (the 3DGS loss, R25) against the torch float64 definition:
-    loss and dL/d(out) by autograd, on 2 views of a ragged 37x29 image."""
+    loss and dL/d(out) by autograd, on views of a ragged 37x29 image (one 32x16 tile
+    plus ragged ones), a 101x70 image (many tiles, ragged right/bottom edges) and a 7x5
+    image (the 5-pixel halo wider than the image)."""
     import torch
     from paper_2510_08491_b200 import snp
     from gpu_util import torch_scene
-    rng = np.random.default_rng(77)
-    out = rng.uniform(0, 1, (2, 29, 37, 4)).astype(np.float32)
-    tgt = np.clip(out[..., :3] + rng.normal(0, 0.15, (2, 29, 37, 3)), 0, 1).astype(np.float32)
+    V, H, W = shape
+    rng = np.random.default_rng(77 + H)
+    out = rng.uniform(0, 1, (V, H, W, 4)).astype(np.float32)
+    tgt = np.clip(out[..., :3] + rng.normal(0, 0.15, (V, H, W, 3)), 0, 1).astype(np.float32)
     h = snp.create_scene(torch_scene(synth.make_scene(1, 4)), 0)
     try:
-        g = torch.zeros((2, 29, 37, 4), device="cuda")
+        g = torch.zeros((V, H, W, 4), device="cuda")
         loss = torch.zeros(1, device="cuda")
         snp.loss_3dgs(h, torch.from_numpy(out).cuda(), torch.from_numpy(tgt).cuda(), g, loss, lam)
         torch.cuda.synchronize()
