@@ -783,7 +783,7 @@ template <int N, bool kRay>
 __device__ __forceinline__ void hit_grad_rows(const float4 *__restrict__ rec, const Ray &r, float gI, float omega,
                                               bool ok, const RenderArgs &ra, const BackwardGrads &gr, float xi_t,
                                               uint32_t prim, uint32_t k2, const float gc[3],
-                                              float (*s)[kRedStride], uint32_t ends) {
+                                              float (*s)[kRedStride], uint32_t ends, const RowDesc *fd) {
     const int lane = threadIdx.x & 31;
     // (the primitive's own parameters first: the shared-memory stores and atomics below
     //  would keep the compiler from hoisting these loads)
@@ -812,7 +812,7 @@ __device__ __forceinline__ void hit_grad_rows(const float4 *__restrict__ rec, co
     }
     const float A = fmaf(av[2], av[2], fmaf(av[1], av[1], av[0] * av[0]));
     const float B = fmaf(av[2], bv[2], fmaf(av[1], bv[1], av[0] * bv[0]));
-    const float iA = 1.0f / A;
+    const float iA = rcp_fast(A);   // (as exact_hit computes it)
     const float ts = -B * iA;
     const float bp[3] = {fmaf(ts, av[0], bv[0]), fmaf(ts, av[1], bv[1]), fmaf(ts, av[2], bv[2])};
     const float Q = 1.0f - fmaf(bp[2], bp[2], fmaf(bp[1], bp[1], bp[0] * bp[0]));
@@ -826,7 +826,7 @@ __device__ __forceinline__ void hit_grad_rows(const float4 *__restrict__ rec, co
     ok = ok && thi > tlo;
     const float dt = thi - tlo, tm = 0.5f * (tlo + thi), hdt = 0.5f * dt;
     const int imax = (sv[1] > sv[0]) ? ((sv[2] > sv[1]) ? 2 : 1) : ((sv[2] > sv[0]) ? 2 : 0);
-    const float isv[3] = {1.0f / sv[0], 1.0f / sv[1], 1.0f / sv[2]};
+    const float isv[3] = {rcp_fast(sv[0]), rcp_fast(sv[1]), rcp_fast(sv[2])};
     const float ismax = isv[imax];
     const float s1 = omega * ismax;
     float sumc = mh.w;
@@ -836,7 +836,10 @@ __device__ __forceinline__ void hit_grad_rows(const float4 *__restrict__ rec, co
     const int tail = (gr.mu ? 11 : 1) + (kRay ? 0 : 3);
     int g0 = 0, used = 0;
     auto flush = [&](int ng, int nrows) {
-        run_flush(s, nrows, ends, prim, k2, [&](int row) { return row_desc<N>(gr, ra, row, g0, ng, GR); });
+        if (fd && g0 == 0 && ng == N / 4 && nrows == ng * GR + tail)   // (the usual single block: N <= 8)
+            run_flush(s, nrows, ends, prim, k2, [&](int row) { return row == (threadIdx.x & 31) ? fd[0] : fd[1]; });
+        else
+            run_flush(s, nrows, ends, prim, k2, [&](int row) { return row_desc<N>(gr, ra, row, g0, ng, GR); });
     };
 #pragma unroll 1
     for (int gq = 0; gq < N / 4; ++gq) {
@@ -900,7 +903,7 @@ __device__ __forceinline__ void hit_grad_rows(const float4 *__restrict__ rec, co
         float G_tc = (clip_lo ? -G_tlo : 0.f) + (clip_hi ? -G_thi : 0.f);
         float G_ts = G_t0 + G_t1;
         const float G_hc = G_t1 - G_t0;
-        const float G_Q = G_hc * hc * (0.5f / Q);
+        const float G_Q = G_hc * hc * 0.5f * rcp_fast(Q);
         float G_A = -G_hc * hc * 0.5f * iA;
         float G_a[3], G_b[3];
 #pragma unroll
@@ -944,7 +947,7 @@ __device__ __forceinline__ void hit_grad_rows(const float4 *__restrict__ rec, co
 #pragma unroll
         for (int k = 0; k < 3; ++k) st[4 + k][lane] = ok ? G_s[k] : 0.f;
         const float qn = sqrtf(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
-        const float iqn = 1.0f / qn;
+        const float iqn = rcp_fast(qn);
         const float w = q4[0] * iqn, x = q4[1] * iqn, y = q4[2] * iqn, z = q4[3] * iqn;
         const float gw_ = 2.0f * (-z * G_R[1] + y * G_R[2] + z * G_R[3] - x * G_R[5] - y * G_R[6] + x * G_R[7]);
         const float gx_ = 2.0f * (y * G_R[1] + z * G_R[2] + y * G_R[3] - 2.0f * x * G_R[4] - w * G_R[5] +
@@ -1085,6 +1088,9 @@ __global__ void __launch_bounds__(128) k_grad_sorted(RenderArgs a, CamBatch cb, 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     float(*s)[kRedStride] = s_red[wid];
     const int64_t n = (int64_t)scnt[kCntDup];
+    // this lane's two flush rows when all values fit one block (N <= 8): fixed per kernel
+    const int GR = gr.wt ? 24 : 20;
+    const RowDesc fd[2] = {row_desc<N>(gr, a, lane, 0, N / 4, GR), row_desc<N>(gr, a, lane + 32, 0, N / 4, GR)};
     const int64_t step = (int64_t)gridDim.x * 4 * 32;
     int64_t base = ((int64_t)blockIdx.x * 4 + wid) * 32;
     GradEntry en{};   // (the next iteration's entry, loaded one iteration ahead)
@@ -1106,7 +1112,8 @@ __global__ void __launch_bounds__(128) k_grad_sorted(RenderArgs a, CamBatch cb, 
         const Ray ray = make_ray(cam, x, y);
         const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + e.id) * rec_f4(N);
         const float gc[3] = {e.gc0, e.gc1, e.gc2};   // (zero on invalid lanes)
-        hit_grad_rows<N, kRay>(rec, ray, e.gI, omega, valid, a, gr, cam.xi_t, e.id, k2, gc, s, ends);
+        hit_grad_rows<N, kRay>(rec, ray, e.gI, omega, valid, a, gr, cam.xi_t, e.id, k2, gc, s, ends,
+                               (N / 4) * GR + (gr.mu ? 11 : 1) + (kRay ? 0 : 3) <= kRedRows ? fd : nullptr);
         if (kRay) {   // SH at the pixel's ray direction: 3 ncoef (<= 48) values, one flush
             const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
             float Y[16];

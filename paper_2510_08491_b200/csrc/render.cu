@@ -45,10 +45,18 @@ constexpr int kQueue = 128;         // per-warp candidate ring (power of two, >=
 template <int N>
 struct Cfg {
     static constexpr int kRecStride = rec_f4(N) | 1;
+#ifdef SNP_AB_STAGES
+    static constexpr int kStages = N <= 8 ? SNP_AB_STAGES : (N == 16 ? 4 : 2);
+#else
     static constexpr int kStages = N <= 8 ? 6 : (N == 16 ? 4 : 2);
+#endif
     static constexpr uint32_t kRecBytes = 16u * rec_f4(N);
 };
+#ifdef SNP_AB_PEND
+constexpr int kPend = SNP_AB_PEND;
+#else
 constexpr int kPend = 16;           // per-pixel pending hits (sorted ring)
+#endif
 static_assert((kPend & (kPend - 1)) == 0, "the pending ring needs a power of two");
 constexpr int kTileRing = 8;        // tiles in flight tracked for early skipping
 
@@ -325,7 +333,10 @@ __device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimi
 // counts in a.grad_fill); an overflowing pixel is queued for K7 with its count of already
 // emitted hits.  Two CTAs per SM, as in the forward.
 template <int N, bool kRay, bool kEager, bool kGrad = false>
-__global__ void __launch_bounds__(kThreads, 2) k_render(RenderArgs a, CamBatch cb) {
+#ifndef SNP_AB_K5_CTAS
+#define SNP_AB_K5_CTAS 2
+#endif
+__global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs a, CamBatch cb) {
     constexpr int kStages = Cfg<N>::kStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
