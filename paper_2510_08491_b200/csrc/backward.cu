@@ -121,7 +121,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     }
     const float A = fmaf(av[2], av[2], fmaf(av[1], av[1], av[0] * av[0]));
     const float B = fmaf(av[2], bv[2], fmaf(av[1], bv[1], av[0] * bv[0]));
-    const float iA = 1.0f / A;
+    const float iA = rcp_fast(A);   // (as exact_hit computes it)
     const float ts = -B * iA;
     const float bp[3] = {fmaf(ts, av[0], bv[0]), fmaf(ts, av[1], bv[1]), fmaf(ts, av[2], bv[2])};
     const float Q = 1.0f - fmaf(bp[2], bp[2], fmaf(bp[1], bp[1], bp[0] * bp[0]));
@@ -138,7 +138,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     const float sv[3] = {s3[0], s3[1], s3[2]};
     const int imax = (sv[1] > sv[0]) ? ((sv[2] > sv[1]) ? 2 : 1) : ((sv[2] > sv[0]) ? 2 : 0);
     // (reciprocals once: an IEEE division per use takes its slow path on tiny adjoints)
-    const float isv[3] = {1.0f / sv[0], 1.0f / sv[1], 1.0f / sv[2]};
+    const float isv[3] = {rcp_fast(sv[0]), rcp_fast(sv[1]), rcp_fast(sv[2])};
     const float ismax = isv[imax];
     const uint32_t wbase = (uint32_t)N * prim;
     const float s1 = omega * ismax;
@@ -200,7 +200,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     float G_tc = (clip_lo ? -G_tlo : 0.f) + (clip_hi ? -G_thi : 0.f);
     float G_ts = G_t0 + G_t1;
     const float G_hc = G_t1 - G_t0;
-    const float G_Q = G_hc * hc * (0.5f / Q);
+    const float G_Q = G_hc * hc * 0.5f * rcp_fast(Q);
     float G_A = -G_hc * hc * 0.5f * iA;
     float G_a[3], G_b[3];
 #pragma unroll
@@ -249,7 +249,7 @@ __device__ __forceinline__ void hit_grad(const float4 *__restrict__ rec, const R
     // R(q^), q^ = q / |q| (w, x, y, z)
     const float *q4 = ra.rotations + 4 * (size_t)prim;
     const float qn = sqrtf(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
-    const float iqn = 1.0f / qn;
+    const float iqn = rcp_fast(qn);
     const float w = q4[0] * iqn, x = q4[1] * iqn, y = q4[2] * iqn, z = q4[3] * iqn;
     const float gw_ = 2.0f * (-z * G_R[1] + y * G_R[2] + z * G_R[3] - x * G_R[5] - y * G_R[6] + x * G_R[7]);
     const float gx_ = 2.0f * (y * G_R[1] + z * G_R[2] + y * G_R[3] - 2.0f * x * G_R[4] - w * G_R[5] + z * G_R[6] +
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kBwWarps * 32) k_backward(RenderArgs a, CamBat
                 }
                 const float Uk[3] = {U0 + sfx[0] - w[0], U1 + sfx[1] - w[1], U2 + sfx[2] - w[2]};
                 if (valid) {
-                    const float iom = 1.0f / fmaxf(1.0f - kp, 1e-20f);
+                    const float iom = rcp_fast(fmaxf(1.0f - kp, 1e-20f));
                     float dk = G.w * Tend * iom;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) {

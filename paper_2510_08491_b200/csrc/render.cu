@@ -250,7 +250,7 @@ __device__ __forceinline__ void emit_grad(Smem<N> &sm, PixelState &ps, Pending &
                     ps.cb = fmaf(w, rgb.w, ps.cb);
                     if (has_g) {
                         const float4 G = gx.G, F = gx.F;
-                        const float om = fmaxf(1.0f - kap, 1e-20f), iom = 1.0f / om;
+                        const float iom = rcp_fast(fmaxf(1.0f - kap, 1e-20f));
                         float dk = G.w * (1.0f - F.w) * iom;
                         dk = fmaf(G.x, fmaf(-(F.x - ps.cr), iom, Tb * rgb.y), dk);
                         dk = fmaf(G.y, fmaf(-(F.y - ps.cg), iom, Tb * rgb.z), dk);
