@@ -230,6 +230,12 @@ snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n
                        void *cuda_stream);
 snp_status snp_loss_3dgs(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views, int32_t height,
                          int32_t width, float lambda_dssim, float *grad_rgba, float *loss, void *cuda_stream);
+/* snp_loss_3dgs over n_views of a training step of step_views (>= n_views) views: the
+ * means (loss and gradient) divide by step_views x height x width, so that the parts of
+ * a step taken one camera batch at a time add up to snp_loss_3dgs over the whole step. */
+snp_status snp_loss_3dgs_part(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views,
+                              int32_t height, int32_t width, int32_t step_views, float lambda_dssim, float *grad_rgba,
+                              float *loss, void *cuda_stream);
 snp_status snp_scale_regularizer(snp_scene s, float weight, float *grad_scales, float *loss, void *cuda_stream);
 snp_status snp_adam_step(snp_scene s, const float *const *grads, const float *lr, float beta1, float beta2, float eps,
                          int32_t step, void *cuda_stream);
@@ -264,8 +270,17 @@ snp_status snp_get_stats(snp_scene s, snp_stats *out, void *cuda_stream);
  * K6 (more hits than K6w holds); slot 48 counts the grazing hits K5 evaluated with a
  * kappa error bound above 1.5e-5 (R23) since the last readback; slots 16..47
  * are only written by instrumented A/B builds (per-warp clock64 accounting).  The
- * call clears slots 16..52 after reading.  Not part of the hot path. */
+ * call clears slots 16..48 after reading.  Not part of the hot path. */
 snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *cuda_stream);
+
+/* Training: with `on`, every later snp_render / snp_render_views that covers one camera
+ * batch (<= 32 views) and the whole image also records its composited hits (per hit: the
+ * pixel, the primitive, the transmittance in front of it, its kappa and the colour
+ * accumulated up to it; about 32 B per hit), and the next snp_render_backward_ex of the
+ * same projection and colour mode forms dL/dI and dL/dc from them (Eq. 4, 9)
+ * instead of traversing the frame again -- the same gradients.  A new snp_project or
+ * snp_update_scene drops the record.  Off (0) by default. */
+snp_status snp_set_record(snp_scene s, int32_t on);
 
 /* Tight binning, from the next snp_project on:
  *   SNP_BIN_CONIC_TILES: K2 drops the keys of rect tiles whose pixel-centre rectangle the

@@ -84,6 +84,11 @@ struct snp_scene_s {
     DevBuf<float> loss_scratch;        // snp_loss_3dgs: moment / SSIM-derivative maps
     DevBuf<uint32_t> bw_skip;          // K7: composited hits K5's grad mode already emitted, per pixel
     DevBuf<float> bw_fwd;              // K7: the forward image when the caller does not pass it
+    DevBuf<FwdEntry> rec_entries;      // snp_set_record: the forward's composited hits (K5 record mode)
+    bool record_mode = false;
+    bool recorded = false;             // the last render recorded them (this projection, one camera batch)
+    int32_t rec_colour = 0;            //   in this colour mode
+    int64_t rec_chunks = 0;            //   in this many entry chunks
     DevBuf<float4> tight;              // K1a -> K2, tight binning (SNP_BIN_*): per item, see tight_geom
     DevBuf<float4> intr;               //   per view (1/fx, 1/fy, cx, cy)
     int32_t bin_flags = 0;             // snp_set_binning (applies from the next snp_project)
@@ -301,6 +306,7 @@ snp_status snp_update_scene(snp_scene s, const snp_scene_desc *d, void *cuda_str
         SNP_CUDA(cudaStreamWaitEvent((cudaStream_t)cuda_stream, s->ev_join, 0));
         s->join_pending = false;
     }
+    s->recorded = false;
     r = upload_and_validate(s, d, (cudaStream_t)cuda_stream);
     if (r != SNP_OK) return r;
     s->state = kCreated;   // parameters changed: project again
@@ -427,6 +433,7 @@ snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, 
     SNP_CUDA(cudaEventRecord(s->ev_join, s->side));
     s->join_pending = true;
     s->state = kProjected;
+    s->recorded = false;
     return SNP_OK;
 }
 
@@ -615,6 +622,33 @@ static snp_status render_device(snp_scene s, const snp_render_opts *opts, float 
     a.out = dout;
     a.fallback = s->fallback.p;
     a.fallback_capacity = s->fallback_capacity;
+    // record mode (training): K5 also writes its composited hits for the next backward;
+    // one camera batch, the whole image
+    const bool rec = s->record_mode && s->cams.size() == 1 && s->n > 0 && s->stripe_rows > 0 &&
+                     s->row_begin == 0 && s->row_stride == 1;
+    s->recorded = false;
+    if (rec) {
+        const int64_t npix_batch = (int64_t)s->cams[0].nv * s->W * s->H;
+        int dev_sms = 148;
+        SNP_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device));
+        const int64_t chunks = (12 * npix_batch + kGradChunk - 1) / kGradChunk + 2 * 8 * (int64_t)dev_sms;
+        SNP_CUDA(s->rec_entries.ensure((size_t)(chunks * kGradChunk)));
+        SNP_CUDA(s->grad_fill.ensure((size_t)chunks));
+        SNP_CUDA(s->grad_keys.ensure((size_t)(chunks * kGradChunk)));
+        SNP_CUDA(s->bw_queue.ensure((size_t)std::max<int64_t>(1, 3 * npix_batch)));
+        SNP_CUDA(s->bw_skip.ensure((size_t)std::max<int64_t>(1, npix_batch)));
+        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdQueue, 0, sizeof(unsigned long long), st));
+        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGradEntries, 0, 2 * sizeof(unsigned long long), st));
+        a.record = 1;
+        a.rec_entries = s->rec_entries.p;
+        a.grad_fill = s->grad_fill.p;
+        a.grad_chunks = chunks;
+        a.grad_keys = s->grad_keys.p;
+        a.bw_queue = s->bw_queue.p;
+        a.bw_skip = s->bw_skip.p;
+        s->rec_chunks = chunks;
+        s->rec_colour = opts->colour_mode;
+    }
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     a.k5_grid = render_grid(s->n_hidden, a.colour_ray != 0, a.eager_emit != 0,
                             s->tiles_x * s->stripe_rows * (s->cams.empty() ? 0 : s->cams[0].nv));
@@ -627,6 +661,7 @@ static snp_status render_device(snp_scene s, const snp_render_opts *opts, float 
         // (SNP_DEBUG bit 2 skips K6: timing experiments only, overflowed pixels stay unwritten)
         if (s->n > 0 && !(a.debug_flags & 2)) SNP_CUDA(launch_fallback(a, s->cams.data(), (int)s->cams.size(), st));
     }
+    s->recorded = rec;
     return SNP_OK;
 }
 
@@ -713,13 +748,18 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
         if (r != SNP_OK) return r;
         fwd = s->bw_fwd.p;
     }
+    // the forward recorded its composited hits (snp_set_record, one camera batch, this
+    // colour mode): no gradient-mode traversal; K7s forms dL/dI and dL/dc from them
+    const bool from_fwd = s->recorded && s->rec_colour == opts->colour_mode && s->cams.size() == 1 &&
+                          !std::getenv("SNP_K7F_UNSORTED");
     // K5 in grad mode: one GradEntry per composited hit, in per-warp chunks (12 per pixel
     // of a camera batch, plus a partly filled chunk per resident consumer warp, before the
     // path falls back to the per-pixel K7 for every pixel)
     int dev_sms = 148;
     SNP_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device));
-    const int64_t chunks = (12 * npix_batch + kGradChunk - 1) / kGradChunk + 2 * 8 * (int64_t)dev_sms;
-    SNP_CUDA(s->grad_entries.ensure((size_t)(chunks * kGradChunk)));
+    const int64_t chunks = from_fwd ? s->rec_chunks
+                                    : (12 * npix_batch + kGradChunk - 1) / kGradChunk + 2 * 8 * (int64_t)dev_sms;
+    if (!from_fwd) SNP_CUDA(s->grad_entries.ensure((size_t)(chunks * kGradChunk)));
     SNP_CUDA(s->grad_fill.ensure((size_t)chunks));
     RenderArgs a = render_args(s, opts);
     a.bw_queue = s->bw_queue.p;
@@ -729,6 +769,8 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
     a.grad_entries = s->grad_entries.p;
     a.grad_fill = s->grad_fill.p;
     a.grad_chunks = chunks;
+    a.rec_entries = s->rec_entries.p;
+    a.from_fwd = from_fwd ? 1 : 0;
     // K7s (default; SNP_K7F_UNSORTED=1: K7f in slot order, A/B)
     const bool unsorted = [] {
         const char *e = std::getenv("SNP_K7F_UNSORTED");
@@ -760,10 +802,12 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
             SNP_CUDA(cudaMemsetAsync(a.gc_acc, 0, (size_t)s->cams[k].nv * (size_t)s->n * sizeof(float4), st));
         if (a.grad_count)
             SNP_CUDA(cudaMemsetAsync(a.grad_count, 0, (size_t)s->cams[k].nv * (size_t)s->n * sizeof(uint32_t), st));
-        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdQueue, 0, sizeof(unsigned long long), st));
-        SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGradEntries, 0, 2 * sizeof(unsigned long long), st));
         a.tile_order = s->tile_order.p + k * order_stride;
-        if (s->n > 0) SNP_CUDA(launch_render_grad(a, s->cams[k], st));
+        if (!from_fwd) {
+            SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntBwdQueue, 0, sizeof(unsigned long long), st));
+            SNP_CUDA(cudaMemsetAsync(s->counters.p + kCntGradEntries, 0, 2 * sizeof(unsigned long long), st));
+            if (s->n > 0) SNP_CUDA(launch_render_grad(a, s->cams[k], st));
+        }
         // K7s over the entries, and beside it (side stream) the per-pixel K7 for the pixels
         // K5 queued (latency-bound long pixels: they overlap K7s; joined before the next
         // batch reuses the queue)
@@ -796,10 +840,18 @@ snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n
 
 snp_status snp_loss_3dgs(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views, int32_t height,
                          int32_t width, float lambda_dssim, float *grad_rgba, float *loss, void *cuda_stream) {
+    return snp_loss_3dgs_part(s, out_rgba, target_rgb, n_views, height, width, n_views, lambda_dssim, grad_rgba, loss,
+                              cuda_stream);
+}
+
+snp_status snp_loss_3dgs_part(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views,
+                              int32_t height, int32_t width, int32_t step_views, float lambda_dssim, float *grad_rgba,
+                              float *loss, void *cuda_stream) {
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
     if (n_views < 0 || height < 0 || width < 0) return fail(SNP_ERR_INVALID_ARGUMENT, "negative image size");
+    if (step_views < n_views) return fail(SNP_ERR_INVALID_ARGUMENT, "step_views < n_views");
     if (!(lambda_dssim >= 0.f && lambda_dssim <= 1.f))
         return fail(SNP_ERR_INVALID_ARGUMENT, "lambda_dssim must be in [0, 1]");
     const int64_t total = (int64_t)n_views * height * width;
@@ -807,7 +859,7 @@ snp_status snp_loss_3dgs(snp_scene s, const float *out_rgba, const float *target
     if (!out_rgba || !target_rgb || !grad_rgba || !loss) return fail(SNP_ERR_INVALID_ARGUMENT, "a pointer is NULL");
     SNP_CUDA(s->loss_scratch.ensure(loss_3dgs_scratch_floats(n_views, height, width)));
     SNP_CUDA(launch_loss_3dgs(out_rgba, target_rgb, n_views, height, width, lambda_dssim, grad_rgba, loss,
-                              s->loss_scratch.p, (cudaStream_t)cuda_stream));
+                              s->loss_scratch.p, (int64_t)step_views * height * width, (cudaStream_t)cuda_stream));
     return SNP_OK;
 }
 
@@ -902,6 +954,7 @@ snp_status snp_destroy(snp_scene s) {
     s->bw_skip.release();
     s->bw_fwd.release();
     s->grad_entries.release();
+    s->rec_entries.release();
     s->tight.release();
     s->intr.release();
     s->grad_fill.release();
@@ -1001,8 +1054,16 @@ snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *c
     SNP_CUDA(cudaStreamSynchronize(st));
     for (int i = 0; i < n; ++i) out[i] = s->h_counters[i];
     // the instrumented slots accumulate until read: clear them for the next measurement
-    SNP_CUDA(cudaMemsetAsync(s->counters.p + 16, 0, sizeof(unsigned long long) * (kCntDeadKeysAcc - 16), st));
+    SNP_CUDA(cudaMemsetAsync(s->counters.p + 16, 0, sizeof(unsigned long long) * (kCntBwdQueue2 - 16), st));
     SNP_CUDA(cudaStreamSynchronize(st));
+    return SNP_OK;
+}
+
+snp_status snp_set_record(snp_scene s, int32_t on) {
+    g_err.clear();
+    if (!s) return fail(SNP_ERR_INVALID_ARGUMENT, "scene handle is NULL");
+    s->record_mode = on != 0;
+    if (!s->record_mode) s->recorded = false;
     return SNP_OK;
 }
 

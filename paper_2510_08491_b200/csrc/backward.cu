@@ -25,6 +25,7 @@
 // only beyond that (tile lists of more than 16384 hits per ray) is a pixel skipped,
 // counted in counters[kCntBwdSkipped] (reset by every call, reported by snp_get_stats).
 #include <algorithm>
+#include <type_traits>
 
 #include "hit.cuh"
 #include "snp_internal.cuh"
@@ -1077,7 +1078,7 @@ __global__ void __launch_bounds__(256) k_entry_count(RenderArgs a, uint32_t *__r
     }
 }
 
-template <int N, bool kRay>
+template <int N, bool kRay, bool kFromFwd>   // kFromFwd: entries recorded by the forward (FwdEntry)
 __global__ void __launch_bounds__(128) k_grad_sorted(RenderArgs a, CamBatch cb, const uint32_t *__restrict__ sorted,
                                                      const unsigned long long *scnt, BackwardGrads gr, float omega) {
     if (a.counters[kCntGradOverflow]) return;
@@ -1093,14 +1094,17 @@ __global__ void __launch_bounds__(128) k_grad_sorted(RenderArgs a, CamBatch cb, 
     const RowDesc fd[2] = {row_desc<N>(gr, a, lane, 0, N / 4, GR), row_desc<N>(gr, a, lane + 32, 0, N / 4, GR)};
     const int64_t step = (int64_t)gridDim.x * 4 * 32;
     int64_t base = ((int64_t)blockIdx.x * 4 + wid) * 32;
-    GradEntry en{};   // (the next iteration's entry, loaded one iteration ahead)
-    if (base + lane < n) en = a.grad_entries[sorted[base + lane]];
+    using Entry = typename std::conditional<kFromFwd, FwdEntry, GradEntry>::type;
+    const Entry *ent = kFromFwd ? reinterpret_cast<const Entry *>(a.rec_entries)
+                                : reinterpret_cast<const Entry *>(a.grad_entries);
+    Entry en{};   // (the next iteration's entry, loaded one iteration ahead)
+    if (base + lane < n) en = ent[sorted[base + lane]];
     for (; base < n; base += step) {
         const int64_t pos = base + lane;
         const bool valid = pos < n;
-        const GradEntry e = en;   // (zero on lanes past the end)
-        en = GradEntry{};
-        if (base + step + lane < n) en = a.grad_entries[sorted[base + step + lane]];
+        const Entry e = en;   // (zero on lanes past the end)
+        en = Entry{};
+        if (base + step + lane < n) en = ent[sorted[base + step + lane]];
         const int vloc = valid ? (int)(e.pix >> 24) : 0;
         SNP_CHECK(!valid || (vloc < cb.nv && (int64_t)e.id < a.n));
         const uint32_t k2 = valid ? (uint32_t)vloc * (uint32_t)a.n + e.id : 0xffffffffu;
@@ -1111,8 +1115,22 @@ __global__ void __launch_bounds__(128) k_grad_sorted(RenderArgs a, CamBatch cb, 
         const int y = (int)(p / (uint32_t)cam.W), x = (int)(p - (uint32_t)y * (uint32_t)cam.W);
         const Ray ray = make_ray(cam, x, y);
         const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + e.id) * rec_f4(N);
-        const float gc[3] = {e.gc0, e.gc1, e.gc2};   // (zero on invalid lanes)
-        hit_grad_rows<N, kRay>(rec, ray, e.gI, omega, valid, a, gr, cam.xi_t, e.id, k2, gc, s, ends,
+        float gI, gc[3];   // (zero on invalid lanes)
+        if constexpr (kFromFwd) {   // dL/dI, dL/dc from dL/d(out), the forward's out and the recorded hit
+            gI = 0.f;
+            gc[0] = gc[1] = gc[2] = 0.f;
+            if (valid) {
+                const int64_t gi = ((int64_t)(cb.view0 + vloc) * cam.H + y) * cam.W + x;
+                const float4 rgb = hit_rgb<kRay>(rec, a.sh, a.sh_degree, e.id, ray);
+                hit_out_grads(a.grad_in[gi], a.fwd[gi], e.T, e.kap, rgb, e.cr, e.cg, e.cb, gI, gc);
+            }
+        } else {
+            gI = e.gI;
+            gc[0] = e.gc0;
+            gc[1] = e.gc1;
+            gc[2] = e.gc2;
+        }
+        hit_grad_rows<N, kRay>(rec, ray, gI, omega, valid, a, gr, cam.xi_t, e.id, k2, gc, s, ends,
                                (N / 4) * GR + (gr.mu ? 11 : 1) + (kRay ? 0 : 3) <= kRedRows ? fd : nullptr);
         if (kRay) {   // SH at the pixel's ray direction: 3 ncoef (<= 48) values, one flush
             const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
@@ -1164,7 +1182,8 @@ cudaError_t launch_grad_entries_n(const RenderArgs &a, const CamBatch &cb, const
         k_key_top<<<1, 1024, 0, st>>>(es->bsum, nb, es->cnt);
         k_key_apply<<<(unsigned)nb, 1024, 0, st>>>(a.grad_count, nk, es->bsum);
         k_entry_count<true><<<(unsigned)(sms * 8), 256, 0, st>>>(a, a.grad_count, es->sorted, nk);
-        k_grad_sorted<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, es->sorted, es->cnt, g, omega);
+        if (a.from_fwd) k_grad_sorted<N, kRay, true><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, es->sorted, es->cnt, g, omega);
+        else k_grad_sorted<N, kRay, false><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, es->sorted, es->cnt, g, omega);
     } else {
         k_grad_entries<N, kRay><<<(unsigned)(sms * 8), 128, 0, st>>>(a, cb, a.grad_entries, g, omega);
     }

@@ -89,6 +89,25 @@ __device__ __forceinline__ float rcp_fast(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+
+// dL/dI and dL/dc of one composited hit (K5 grad mode; K7s from recorded hits -- the same
+// arithmetic in both): out = sum_j T_j k_j c_j + T_end bg, so the light behind the hit is
+// U = F - (colour accumulated up to and including it); dL/dk = G_rgb . (T c - U / (1 - k))
+// + G_a T_end / (1 - k), dL/dI = (1 - k) dL/dk for I > 0 (Eq. 9), dL/dc = T k G_rgb on
+// unclamped channels.  G = dL/d(out), F = out, Tb = T before the hit, rgb in .yzw.
+__device__ __forceinline__ void hit_out_grads(const float4 &G, const float4 &F, float Tb, float kap, const float4 &rgb,
+                                              float cr, float cg, float cb, float &gI, float gc[3]) {
+    const float iom = rcp_fast(fmaxf(1.0f - kap, 1e-20f));
+    float dk = G.w * (1.0f - F.w) * iom;
+    dk = fmaf(G.x, fmaf(-(F.x - cr), iom, Tb * rgb.y), dk);
+    dk = fmaf(G.y, fmaf(-(F.y - cg), iom, Tb * rgb.z), dk);
+    dk = fmaf(G.z, fmaf(-(F.z - cb), iom, Tb * rgb.w), dk);
+    const float w = Tb * kap;
+    gI = kap > 0.f ? dk * (1.0f - kap) : 0.f;
+    gc[0] = rgb.y > 0.f ? w * G.x : 0.f;
+    gc[1] = rgb.z > 0.f ? w * G.y : 0.f;
+    gc[2] = rgb.w > 0.f ? w * G.z : 0.f;
+}
 __device__ __forceinline__ float sinc_f(float x) {
     const float x2 = x * x;
     // 1 - x^2/6 + x^4/120; the dropped x^6/5040 term is < 5e-8 below |x| = 0.25

@@ -160,6 +160,8 @@ struct PixelState {
 struct GradCtx {
     float4 G, F;
     GradEntry *chunk;     // this warp's current chunk of a.grad_entries (nullptr: none)
+    FwdEntry *rchunk;     //   (record mode) of a.rec_entries
+    int64_t cbase;        //   its first slot (keys)
     int *cnt;             // its fill count (shared; read and written warp-synchronously)
     uint32_t pix;         // view within the batch << 24 | y * W + x
 };
@@ -204,16 +206,14 @@ __device__ __forceinline__ void emit(Smem<N> &sm, PixelState &ps, Pending &pd, f
     pd.head = h;
 }
 
-// K5 grad mode's emission: the same blend (same order and arithmetic), warp-synchronous
-// (every lane of the warp calls it; `active` = this lane's pixel emits) so that the
-// entries' chunk slots come from a ballot instead of shared-memory atomics.  Each
-// composited hit of a pixel with a nonzero dL/d(out) becomes a GradEntry:
-// out = sum_j T_j k_j c_j + T_end bg, so the light behind this hit is U = out - (colour
-// accumulated up to and including it); then (K7's formulas) dL/dk = G_rgb . (T c -
-// U / (1 - k)) + G_a T_end / (1 - k), dL/dI = (1 - k) dL/dk for I > 0 (Eq. 9),
-// dL/dc = T k G_rgb on unclamped channels.
-template <int N, bool kRay>
-__device__ __forceinline__ void emit_grad(Smem<N> &sm, PixelState &ps, Pending &pd, bool active, float L,
+// K5 grad / record mode's emission: the same blend (same order and arithmetic) as emit(),
+// warp-synchronous (every lane of the warp calls it; `active` = this lane's pixel emits)
+// so that the entries' chunk slots come from a ballot instead of shared-memory atomics.
+// Grad mode: each composited hit of a pixel with a nonzero dL/d(out) becomes a GradEntry
+// (hit_out_grads); record mode: every composited hit becomes a FwdEntry (T in front of
+// it, kappa, the colour accumulated up to and including it).
+template <int N, bool kRay, bool kRecord>
+__device__ __forceinline__ void emit_sync(Smem<N> &sm, PixelState &ps, Pending &pd, bool active, float L,
                                           float t_floor, const float4 *recs, const RenderArgs &a, const Ray &ray,
                                           GradCtx &gx) {
     const int tid = threadIdx.x, lane = tid & 31;
@@ -222,10 +222,11 @@ __device__ __forceinline__ void emit_grad(Smem<N> &sm, PixelState &ps, Pending &
     int h = pd.head;
     bool more = active && n > 0;
     int fill = *gx.cnt;   // (warp-uniform: grad_reserve synchronised the warp)
-    const bool has_g = gx.G.x != 0.f || gx.G.y != 0.f || gx.G.z != 0.f || gx.G.w != 0.f;
+    const bool has_g = kRecord || gx.G.x != 0.f || gx.G.y != 0.f || gx.G.z != 0.f || gx.G.w != 0.f;
     while (__any_sync(0xffffffffu, more)) {
         bool write = false;
-        GradEntry e{};
+        uint32_t wid_ = 0;
+        float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f;   // the entry's payload
         if (more) {
             const float t = sm.p_thi[h][tid];
             if (!(t < L)) {
@@ -236,7 +237,7 @@ __device__ __forceinline__ void emit_grad(Smem<N> &sm, PixelState &ps, Pending &
                 const uint32_t pid = word & kIdMask;
                 SNP_CHECK(h >= 0 && h < kPend && n <= kPend && (int64_t)pid < a.n);
                 const int gexp = (int)((word >> 24) & 7u);
-                if (gexp && (gexp == 7 || ps.T * (float)(1 << gexp) > 2.0f)) {   // -> K7 per pixel
+                if (gexp && (gexp == 7 || ps.T * (float)(1 << gexp) > 2.0f)) {   // -> K6 / K7 per pixel
                     atomicAdd(a.counters + kCntGraze, 1ull);
                     ps.overflow = true;
                     ps.done = true;
@@ -249,19 +250,15 @@ __device__ __forceinline__ void emit_grad(Smem<N> &sm, PixelState &ps, Pending &
                     ps.cg = fmaf(w, rgb.z, ps.cg);
                     ps.cb = fmaf(w, rgb.w, ps.cb);
                     if (has_g) {
-                        const float4 G = gx.G, F = gx.F;
-                        const float iom = rcp_fast(fmaxf(1.0f - kap, 1e-20f));
-                        float dk = G.w * (1.0f - F.w) * iom;
-                        dk = fmaf(G.x, fmaf(-(F.x - ps.cr), iom, Tb * rgb.y), dk);
-                        dk = fmaf(G.y, fmaf(-(F.y - ps.cg), iom, Tb * rgb.z), dk);
-                        dk = fmaf(G.z, fmaf(-(F.z - ps.cb), iom, Tb * rgb.w), dk);
-                        e.pix = gx.pix;
-                        e.id = pid;
-                        e.gI = kap > 0.f ? dk * (1.0f - kap) : 0.f;
-                        e.gc0 = rgb.y > 0.f ? w * G.x : 0.f;
-                        e.gc1 = rgb.z > 0.f ? w * G.y : 0.f;
-                        e.gc2 = rgb.w > 0.f ? w * G.z : 0.f;
+                        wid_ = pid;
                         write = true;
+                        if (kRecord) {
+                            v0 = Tb; v1 = kap; v2 = ps.cr; v3 = ps.cg; v4 = ps.cb;
+                        } else {
+                            float gc[3];
+                            hit_out_grads(gx.G, gx.F, Tb, kap, rgb, ps.cr, ps.cg, ps.cb, v0, gc);
+                            v1 = gc[0]; v2 = gc[1]; v3 = gc[2];
+                        }
                     }
                     ps.T *= (1.0f - kap);
                     ++ps.composited;
@@ -279,10 +276,18 @@ __device__ __forceinline__ void emit_grad(Smem<N> &sm, PixelState &ps, Pending &
         if (write) {
             const int slot = fill + __popc(wm & lt_mask);
             SNP_CHECK(slot >= 0 && slot < kGradChunk);
-            if (gx.chunk) {
-                gx.chunk[slot] = e;
+            if (kRecord ? gx.rchunk != nullptr : gx.chunk != nullptr) {
+                if (kRecord) {
+                    FwdEntry e;
+                    e.pix = gx.pix; e.id = wid_; e.T = v0; e.kap = v1; e.cr = v2; e.cg = v3; e.cb = v4; e.pad = v5;
+                    gx.rchunk[slot] = e;
+                } else {
+                    GradEntry e;
+                    e.pix = gx.pix; e.id = wid_; e.gI = v0; e.gc0 = v1; e.gc1 = v2; e.gc2 = v3;
+                    gx.chunk[slot] = e;
+                }
                 if (a.grad_keys)   // K7s's counting sort key
-                    a.grad_keys[(gx.chunk - a.grad_entries) + slot] = (gx.pix >> 24) * (uint32_t)a.n + e.id;
+                    a.grad_keys[gx.cbase + slot] = (gx.pix >> 24) * (uint32_t)a.n + wid_;
             }
         }
         fill += __popc(wm);
@@ -332,11 +337,12 @@ __device__ __forceinline__ void insert_local(Smem<N> &sm, Pending &pd, int plimi
 // current chunk of a.grad_entries (kGradChunk entries, one global atomic per chunk; fill
 // counts in a.grad_fill); an overflowing pixel is queued for K7 with its count of already
 // emitted hits.  Two CTAs per SM, as in the forward.
-template <int N, bool kRay, bool kEager, bool kGrad = false>
+template <int N, bool kRay, bool kEager, int kMode = 0>   // 0 forward, 1 grad mode, 2 record mode
 #ifndef SNP_AB_K5_CTAS
 #define SNP_AB_K5_CTAS 2
 #endif
 __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs a, CamBatch cb) {
+    constexpr bool kGrad = kMode == 1, kRecord = kMode == 2, kEntries = kGrad || kRecord;
     constexpr int kStages = Cfg<N>::kStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
@@ -346,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
     const int stripe_tiles = a.tiles_x * a.stripe_rows;
     const int total_tiles = stripe_tiles * cb.nv;
 
-    if (kGrad && tid < kConsumers) gcount[tid] = 0;
+    if (kEntries && tid < kConsumers) gcount[tid] = 0;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
     float pxf = 0.f, pyf = 0.f, bx0 = 0.f, by0 = 0.f;
     PixelState ps{1.f, 0.f, 0.f, 0.f, true, false, 0u};
     Pending pd{0, 0, 0.f, 0u, false};
-    GradCtx gx{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), nullptr, gcount + wid, 0u};
+    GradCtx gx{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), nullptr, nullptr, 0, gcount + wid, 0u};
     int64_t gchunk = -1;   // (kGrad) index of gx.chunk; -2: the chunk table is exhausted
     // (kGrad) switch to a fresh chunk when this emission call (need entries at most)
     // might not fit: the old one's fill goes to a.grad_fill (warp-uniform)
@@ -519,7 +525,9 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
             *gx.cnt = 0;
         }
         gchunk = __shfl_sync(0xffffffffu, k, 0);
-        gx.chunk = gchunk >= 0 ? a.grad_entries + gchunk * kGradChunk : nullptr;
+        gx.cbase = gchunk >= 0 ? gchunk * kGradChunk : 0;
+        if (kRecord) gx.rchunk = gchunk >= 0 ? a.rec_entries + gx.cbase : nullptr;
+        else gx.chunk = gchunk >= 0 ? a.grad_entries + gx.cbase : nullptr;
         __syncwarp();
     };
     int64_t gpi = 0;   // (kGrad) pixel index within the camera batch
@@ -533,6 +541,11 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
             }
         } else if (inside) {
             if (ps.overflow) {
+                if (kRecord) {   // the backward's per-pixel K7 takes it from its recorded hits on
+                    const unsigned long long qb = atomicAdd(a.counters + kCntBwdQueue, 1ull);
+                    a.bw_queue[qb] = (uint32_t)gpi;
+                    a.bw_skip[gpi] = ps.composited;
+                }
                 const unsigned long long q = atomicAdd(a.counters + kCntFallbackQueue, 1ull);
                 if ((int64_t)q < a.fallback_capacity)
                     atomicExch(a.fallback + q, (1ull << 63) | ((unsigned long long)view << 32) |
@@ -587,11 +600,13 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
             by0 = (float)by + 0.5f;
             ps = PixelState{1.f, 0.f, 0.f, 0.f, !inside, false, 0u};
             pd = Pending{0, 0, 0.f, 0u, false};
-            if (kGrad) {
+            if (kEntries) {
                 gpi = ((int64_t)vloc * cam->H + y) * cam->W + x;
-                const int64_t gi = ((int64_t)view * cam->H + y) * cam->W + x;
-                gx.G = inside ? a.grad_in[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
-                gx.F = inside ? a.fwd[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (kGrad) {
+                    const int64_t gi = ((int64_t)view * cam->H + y) * cam->W + x;
+                    gx.G = inside ? a.grad_in[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    gx.F = inside ? a.fwd[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
                 gx.pix = ((uint32_t)vloc << 24) | (uint32_t)(inside ? y * cam->W + x : 0);
             }
             sm.p_in[tid] = 0u;
@@ -767,9 +782,9 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
                 // kEager: after every exact round -- shorter pending lists (fewer K6
                 // pixels), earlier termination; chosen per scene from the overflow rate
                 const bool do_emit = !ps.done && (batch_end || pd.n > (kEager ? 0 : plimit - 4));
-                if (kGrad) {
+                if (kEntries) {
                     grad_reserve(__reduce_add_sync(0xffffffffu, do_emit ? (uint32_t)pd.n : 0u));
-                    emit_grad<N, kRay>(sm, ps, pd, do_emit,
+                    emit_sync<N, kRay, kRecord>(sm, ps, pd, do_emit,
                                        batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
                                        a.t_floor, recs, a, ray, gx);
                 } else if (do_emit) {
@@ -825,9 +840,11 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
     }
 #endif
     __syncwarp();
-    if (kGrad) {   // (the backward's traversal leaves the forward's statistics alone)
+    if (kEntries) {
         __syncwarp();
         if (lane == 0 && gchunk >= 0) a.grad_fill[gchunk] = *gx.cnt;
+    }
+    if (kGrad) {   // (the backward's traversal leaves the forward's statistics alone)
         warp_exit();
         return;
     }
@@ -1348,7 +1365,21 @@ template <int N, bool kRay, bool kEager>
 cudaError_t launch_render_n(const RenderArgs &a, const CamBatch &cams, int tiles, cudaStream_t st) {
     const int smem = (int)sizeof(Smem<N>);
     const int grid = render_grid_n<N, kRay, kEager>(tiles);   // (sets the attribute on this device)
-    k_render<N, kRay, kEager><<<grid, kThreads, smem, st>>>(a, cams);
+    if (a.record) {   // (same grid: K6w counts K5's CTAs; + the warps' chunk fill counts)
+        static bool attr[kMaxDevices] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        bool &done = attr[dev < kMaxDevices ? dev : 0];
+        if (!done) {
+            cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay, kEager, 2>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem + 64);
+            if (e != cudaSuccess) return e;
+            done = true;
+        }
+        k_render<N, kRay, kEager, 2><<<grid, kThreads, smem + 64, st>>>(a, cams);
+    } else {
+        k_render<N, kRay, kEager><<<grid, kThreads, smem, st>>>(a, cams);
+    }
     return cudaGetLastError();
 }
 
@@ -1409,14 +1440,14 @@ cudaError_t launch_render_grad_n(const RenderArgs &a, const CamBatch &cams, cuda
     if (!resident) {
         int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay, false, true>,
+        cudaError_t e = cudaFuncSetAttribute(k_render<N, kRay, false, 1>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N, kRay, false, true>, kThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<N, kRay, false, 1>, kThreads, smem);
         resident = std::max(1, sms) * std::max(1, per_sm);
     }
     const int tiles = a.tiles_x * a.stripe_rows * cams.nv;
-    k_render<N, kRay, false, true><<<std::min(tiles, resident), kThreads, smem, st>>>(a, cams);
+    k_render<N, kRay, false, 1><<<std::min(tiles, resident), kThreads, smem, st>>>(a, cams);
     return cudaGetLastError();
 }
 template <int N>

@@ -205,6 +205,15 @@ cudaError_t launch_onesweep(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *
 // one global atomic (>= the 32 x kPend entries one emission call can produce)
 constexpr int kGradChunk = 1024;
 
+// K5 record mode (training: the forward render also records its composited hits, so that
+// the backward needs no second traversal): per hit the transmittance in front of it, its
+// kappa and the colour accumulated up to and including it
+struct FwdEntry {
+    uint32_t pix;      // view within the camera batch << 24 | y * W + x
+    uint32_t id;       // primitive
+    float T, kap, cr, cg, cb, pad;
+};
+
 struct GradEntry {
     uint32_t pix;      // view within the camera batch << 24 | y * W + x
     uint32_t id;       // primitive
@@ -227,6 +236,9 @@ struct RenderArgs {
     GradEntry *grad_entries;       // K5 grad mode: entry buffer, grad_chunks chunks of kGradChunk
     int32_t *grad_fill;            //   entries used per chunk
     uint32_t *grad_keys;           //   per slot: vloc * n + primitive (K7s)
+    FwdEntry *rec_entries;         // K5 record mode: entry buffer (same chunks, fills and keys)
+    int32_t record;                // K5: record the composited hits (forward render)
+    int32_t from_fwd;              // K7s: the entries are rec_entries (no grad-mode traversal)
     uint32_t *grad_count;          //   [nv * n] entries per key -> offsets (K7s; zeroed per batch)
     int64_t grad_chunks;
     float4 *gc_acc;                // K7f, primitive colour mode: [batch views][n] summed dL/dc
@@ -294,8 +306,10 @@ cudaError_t launch_l1(const float *out_rgba, const float *target_rgb, int64_t n,
                       cudaStream_t st);
 cudaError_t launch_scale_reg(const float *s, int64_t n, float w, float *grad_s, float *loss, cudaStream_t st);
 size_t loss_3dgs_scratch_floats(int V, int H, int W);
+// (norm_total: the pixel count the means divide by -- V H W, or the whole step's when the
+//  step's views are taken in parts)
 cudaError_t launch_loss_3dgs(const float *out_rgba, const float *target_rgb, int V, int H, int W, float lam,
-                             float *grad_rgba, float *loss, float *scratch, cudaStream_t st);
+                             float *grad_rgba, float *loss, float *scratch, int64_t norm_total, cudaStream_t st);
 cudaError_t launch_adam(float *p, const float *g, float *m, float *v, int64_t count, float lr, float b1, float b2,
                         float eps, int step, bool log_space, cudaStream_t st);   // K5's persistent grid for `tiles` work units
 

@@ -231,10 +231,12 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_back(const float4 *__rest
 }
 static_assert(kTx * kTy == 2 * kSsimThreads, "k_ssim_back: two output pixels per thread");
 
-__global__ void k_ssim_loss(const float *sums, int64_t total, float lam, float *loss) {
-    // sums[0] = sum of SSIM, sums[1] = sum of |x - y| over the 3 V H W values
+__global__ void k_ssim_loss(const float *sums, int64_t part, int64_t total, float lam, float *loss) {
+    // sums[0] = sum of SSIM, sums[1] = sum of |x - y| over this call's 3 V H W values (part
+    // pixels of the step's total): its share of (1 - lam) mean|x - y| + lam (1 - mean SSIM)
     const float m = 3.0f * (float)total;
-    if (threadIdx.x == 0) atomicAdd(loss, (1.0f - lam) * (sums[1] / m) + lam * (1.0f - sums[0] / m));
+    if (threadIdx.x == 0)
+        atomicAdd(loss, (1.0f - lam) * (sums[1] / m) + lam * (((float)part - sums[0] / 3.0f) * 3.0f / m));
 }
 
 unsigned grid_for(int64_t n) {
@@ -272,7 +274,7 @@ namespace snp {
 size_t loss_3dgs_scratch_floats(int V, int H, int W) { return (size_t)V * H * W * 9 + 2; }
 
 cudaError_t launch_loss_3dgs(const float *out_rgba, const float *target_rgb, int V, int H, int W, float lam,
-                             float *grad_rgba, float *loss, float *scratch, cudaStream_t st) {
+                             float *grad_rgba, float *loss, float *scratch, int64_t norm_total, cudaStream_t st) {
     const int64_t total = (int64_t)V * H * W;
     if (total == 0) return cudaSuccess;
     float *d = scratch;                      // [V][3 channels][3 maps][H][W]
@@ -290,8 +292,8 @@ cudaError_t launch_loss_3dgs(const float *out_rgba, const float *target_rgb, int
     k_ssim_fwd<<<grid, kSsimThreads, 0, st>>>(reinterpret_cast<const float4 *>(out_rgba), target_rgb, H, W, g, d,
                                               sums);
     k_ssim_back<<<grid, kSsimThreads, 0, st>>>(reinterpret_cast<const float4 *>(out_rgba), target_rgb, d, H, W,
-                                               total, lam, g, reinterpret_cast<float4 *>(grad_rgba));
-    k_ssim_loss<<<1, 32, 0, st>>>(sums, total, lam, loss);
+                                               norm_total, lam, g, reinterpret_cast<float4 *>(grad_rgba));
+    k_ssim_loss<<<1, 32, 0, st>>>(sums, total, norm_total, lam, loss);
     return cudaGetLastError();
 }
 }  // namespace snp

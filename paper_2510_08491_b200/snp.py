@@ -32,7 +32,8 @@ EXPORTS = ("snp_version", "snp_create_scene", "snp_update_scene", "snp_project",
            "snp_render_views", "snp_destroy", "snp_last_error", "snp_get_binning", "snp_get_stats",
            "snp_set_pending_limit", "snp_get_debug_counters", "snp_set_temporal", "snp_project_at",
            "snp_render_backward", "snp_loss_l1", "snp_scale_regularizer", "snp_adam_step", "snp_get_params",
-           "snp_set_temporal_grad", "snp_loss_3dgs", "snp_render_backward_ex", "snp_set_binning")
+           "snp_set_temporal_grad", "snp_loss_3dgs", "snp_render_backward_ex", "snp_set_binning", "snp_set_record",
+           "snp_loss_3dgs_part")
 
 
 class SnpError(RuntimeError):
@@ -93,6 +94,7 @@ def lib():
             L.snp_get_stats.argtypes = [vp, C.POINTER(Stats), vp]
             L.snp_set_pending_limit.argtypes = [vp, C.c_int32]
             L.snp_set_binning.argtypes = [vp, C.c_int32]
+            L.snp_set_record.argtypes = [vp, C.c_int32]
             L.snp_set_temporal.argtypes = [vp, vp, C.c_int32, vp]
             L.snp_render_backward.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
             L.snp_render_backward_ex.argtypes = [vp, C.POINTER(RenderOpts), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
@@ -102,6 +104,8 @@ def lib():
             L.snp_set_temporal_grad.argtypes = [vp, vp]
             L.snp_scale_regularizer.argtypes = [vp, C.c_float, vp, vp, vp]
             L.snp_loss_3dgs.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_float, vp, vp, vp]
+            L.snp_loss_3dgs_part.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, vp, vp,
+                                             vp]
             L.snp_adam_step.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_float), C.c_float, C.c_float, C.c_float,
                                         C.c_int32, vp]
             L.snp_project_at.argtypes = [vp, C.POINTER(Camera), C.c_int32, vp, vp]
@@ -270,12 +274,18 @@ def loss_l1(out_rgba, target_rgb, grad_rgba, loss, stream=None):
     _check(lib().snp_loss_l1(_ptr(out_rgba), _ptr(target_rgb), n, _ptr(grad_rgba), _ptr(loss), _stream(stream)))
 
 
-def loss_3dgs(h, out_rgba, target_rgb, grad_rgba, loss, lambda_dssim=0.2, stream=None):
+def loss_3dgs(h, out_rgba, target_rgb, grad_rgba, loss, lambda_dssim=0.2, stream=None, step_views=None):
     """3DGS's loss (1 - lambda) L1 + lambda (1 - SSIM): out [V, H, W, 4], target
-    [V, H, W, 3] CUDA tensors; writes dL/d(out) into grad_rgba, adds L to loss."""
+    [V, H, W, 3] CUDA tensors; writes dL/d(out) into grad_rgba, adds L to loss.  With
+    step_views (snp_loss_3dgs_part) the means divide by that many views: parts of a
+    step add up to the whole step's loss and gradient."""
     V, H, W = int(out_rgba.shape[0]), int(out_rgba.shape[1]), int(out_rgba.shape[2])
-    _check(lib().snp_loss_3dgs(h, _ptr(out_rgba), _ptr(target_rgb), V, H, W, float(lambda_dssim), _ptr(grad_rgba),
-                               _ptr(loss), _stream(stream)))
+    if step_views is None:
+        _check(lib().snp_loss_3dgs(h, _ptr(out_rgba), _ptr(target_rgb), V, H, W, float(lambda_dssim),
+                                   _ptr(grad_rgba), _ptr(loss), _stream(stream)))
+    else:
+        _check(lib().snp_loss_3dgs_part(h, _ptr(out_rgba), _ptr(target_rgb), V, H, W, int(step_views),
+                                        float(lambda_dssim), _ptr(grad_rgba), _ptr(loss), _stream(stream)))
 
 
 def scale_regularizer(h, weight, grad_scales, loss, stream=None):
@@ -306,6 +316,12 @@ def destroy(h):
 
 def set_pending_limit(h, k):
     _check(lib().snp_set_pending_limit(h, int(k)))
+
+
+def set_record(h, on=True):
+    """snp_set_record: renders of one camera batch also record their composited hits for
+    the next backward (training)."""
+    _check(lib().snp_set_record(h, 1 if on else 0))
 
 
 def set_binning(h, flags):

@@ -10,6 +10,8 @@ import numpy as np
 
 from . import snp
 
+CAMERA_BATCH = 32   # kCamsPerLaunch: the views one render / backward launch covers
+
 
 def flat_grads(scene, device):
     """One contiguous float32 buffer with a view per parameter array (FIELDS order), so
@@ -53,22 +55,29 @@ class Trainer:
         self.flat, self.grads = flat_grads(scene, device)
         self.loss = torch.zeros(1, device=device)
         self.step_count = 0
+        # the forward records its composited hits, so that the backward needs no second
+        # traversal (snp_set_record); a step runs one camera batch (<= 32 views) at a time
+        snp.set_record(h, True)
 
     def step(self, cams, target_rgb, group=None):
         """One training step on this rank's views (target_rgb [n_views, H, W, 3]); returns
         this rank's loss (a device scalar, read by the caller when it wants it)."""
         self.flat.zero_()
         self.loss.zero_()
-        snp.render_views(self.h, cams, self.opts, self.out)
-        if self.dssim_lambda > 0.0:
-            snp.loss_3dgs(self.h, self.out, target_rgb, self.gout, self.loss, self.dssim_lambda)
-        else:
-            snp.loss_l1(self.out, target_rgb, self.gout, self.loss)
-        snp.render_backward(self.h, self.opts, self.gout, self.grads, fwd_rgba=self.out)
-        if self.check_every and self.step_count % self.check_every == 0:
-            skipped = snp.get_stats(self.h)["backward_skipped"]   # (synchronises)
-            if skipped:
-                raise RuntimeError(f"snp_render_backward skipped {skipped} pixels with more than 16384 hits")
+        V = len(cams)
+        for v0 in range(0, V, CAMERA_BATCH):   # render + loss + backward per camera batch
+            v1 = min(V, v0 + CAMERA_BATCH)
+            out, gout = self.out[v0:v1], self.gout[v0:v1]
+            snp.render_views(self.h, cams[v0:v1], self.opts, out)
+            if self.dssim_lambda > 0.0 or V > CAMERA_BATCH:   # (the means are the whole step's)
+                snp.loss_3dgs(self.h, out, target_rgb[v0:v1], gout, self.loss, self.dssim_lambda, step_views=V)
+            else:
+                snp.loss_l1(out, target_rgb, gout, self.loss)
+            snp.render_backward(self.h, self.opts, gout, self.grads, fwd_rgba=out)
+            if self.check_every and self.step_count % self.check_every == 0:
+                skipped = snp.get_stats(self.h)["backward_skipped"]   # (synchronises; per backward call)
+                if skipped:
+                    raise RuntimeError(f"snp_render_backward skipped {skipped} pixels with more than 16384 hits")
         if self.reg > 0.0:
             snp.scale_regularizer(self.h, self.reg, self.grads["scales"], self.loss)
         allreduce_mean(self.flat, group)

@@ -1130,3 +1130,76 @@ def test_tight_binning_deep_overlap(orc):
     ref, st0 = _render_with_binning(scene, [cam], (0.0, 0.0, 0.0), 0)
     both, st3 = _render_with_binning(scene, [cam], (0.0, 0.0, 0.0), 3)
     assert np.abs(both - ref).max() <= 1e-5
+
+
+@pytest.mark.parametrize("colour_mode", [0, 1])
+def test_backward_from_recorded_forward(colour_mode):
+    """snp_set_record: the forward render records its composited hits and the backward
+    forms dL/dI, dL/dc from them (no second traversal).  Same frame as without recording
+    (bit-identical), and the same gradients as the gradient-mode traversal on every
+    parameter (up to atomic order), on a C2-shaped 2-view frame with forced pending
+    overflow (limit 3: K6 / the per-pixel K7 take those pixels from their recorded hits on)
+    and on the dense grazing scene."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    rng = np.random.default_rng(93)
+    cases = [(synth.make_scene(1, 2000, scale_mult=1.5, box=1.0), synth.orbit_cameras(2, 4.0, 160, 120, 220.0), 3)]
+    n = 150
+    sc = synth.make_scene(32, n, box=0.6)
+    sc.centers[:] = rng.uniform(-0.4, 0.4, (n, 3)).astype(np.float32)
+    sc.scales[:] = rng.uniform(0.04, 0.1, (n, 3)).astype(np.float32)
+    sc.w2[:] = 0.0
+    sc.b2[:] = (50.0 / sc.scales.max(1)).astype(np.float32)
+    cases.append((sc, [synth.look_at((0.3, -3.0, 0.4), (0.0, 0.0, 0.0), 200, 150, 750.0)], 0))
+    for scene, cams, limit in cases:
+        V, H, W = len(cams), cams[0].height, cams[0].width
+        G = torch.from_numpy(rng.normal(size=(V, H, W, 4)).astype(np.float32)).cuda()
+        res, frames = {}, {}
+        for record in (0, 1):
+            h = snp.create_scene(torch_scene(scene), 0)
+            try:
+                snp.set_record(h, record)
+                if limit:
+                    snp.set_pending_limit(h, limit)
+                opts = snp.make_opts((0.2, 0.3, 0.4), colour_mode=colour_mode)
+                out = torch.zeros((V, H, W, 4), device="cuda")
+                snp.render_views(h, cams, opts, out)
+                grads = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in snp.FIELDS}
+                snp.render_backward(h, opts, G, grads, fwd_rgba=out)
+                torch.cuda.synchronize()
+                frames[record] = out.cpu().numpy()
+                res[record] = {f: v.cpu().numpy().astype(np.float64) for f, v in grads.items()}
+                if limit:
+                    assert snp.get_stats(h)["overflow_pixels"] > 0
+            finally:
+                snp.destroy(h)
+        assert np.array_equal(frames[0], frames[1])
+        for f in snp.FIELDS:
+            a, b = res[1][f], res[0][f]
+            scale = np.abs(b).max()
+            assert np.abs(a - b).max() <= 2e-4 * scale + 1e-7, (f, np.abs(a - b).max(), scale)
+
+
+def test_loss_3dgs_parts_add_up():
+    """snp_loss_3dgs_part: a step's views taken in two parts (as Trainer.step does per
+    camera batch) give the loss and dL/d(out) of snp_loss_3dgs over the whole step."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    rng = np.random.default_rng(78)
+    V, H, W = 5, 40, 52
+    out = torch.from_numpy(rng.uniform(0, 1, (V, H, W, 4)).astype(np.float32)).cuda()
+    tgt = torch.from_numpy(rng.uniform(0, 1, (V, H, W, 3)).astype(np.float32)).cuda()
+    h = snp.create_scene(torch_scene(synth.make_scene(1, 4)), 0)
+    try:
+        g_all, l_all = torch.zeros_like(out), torch.zeros(1, device="cuda")
+        snp.loss_3dgs(h, out, tgt, g_all, l_all, 0.2)
+        g_p, l_p = torch.zeros_like(out), torch.zeros(1, device="cuda")
+        for v0, v1 in ((0, 2), (2, 5)):
+            snp.loss_3dgs(h, out[v0:v1], tgt[v0:v1], g_p[v0:v1], l_p, 0.2, step_views=V)
+        torch.cuda.synchronize()
+    finally:
+        snp.destroy(h)
+    assert abs(l_p.item() - l_all.item()) <= 1e-6 * abs(l_all.item())
+    assert torch.equal(g_p, g_all)
