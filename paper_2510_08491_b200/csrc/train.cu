@@ -90,25 +90,31 @@ constexpr int kSsimThreads = 256;
 __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const float4 *__restrict__ out,
                                                            const float *__restrict__ target, int H, int W, Gauss g,
                                                            float *__restrict__ d, float *sums) {
-    __shared__ float sx[kHy][kHx], sy[kHy][kHx];
+    __shared__ float sx3[3][kHy][kHx], sy3[3][kHy][kHx];
     __shared__ float hb[5][kHy][kTx];
     const int v = blockIdx.z, x0 = blockIdx.x * kTx - kHalf, y0 = blockIdx.y * kTy - kHalf;
     const int64_t hw = (int64_t)H * W;
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
     float ssum = 0.f, l1sum = 0.f;
-    for (int c = 0; c < 3; ++c) {
-        for (int i = threadIdx.x; i < kHx * kHy; i += kSsimThreads) {
-            const int r = i / kHx, q = i - r * kHx, gy = y0 + r, gx = x0 + q;
-            float xv = 0.f, yv = 0.f;
-            if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-                const int64_t pi = (int64_t)v * hw + (int64_t)gy * W + gx;
-                xv = reinterpret_cast<const float *>(out)[4 * pi + c];
-                yv = target[3 * pi + c];
-            }
-            sx[r][q] = xv;
-            sy[r][q] = yv;
+    // the tile and its halo, all three channels at once (one 16-byte load per pixel)
+    for (int i = threadIdx.x; i < kHx * kHy; i += kSsimThreads) {
+        const int r = i / kHx, q = i - r * kHx, gy = y0 + r, gx = x0 + q;
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+        if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+            const int64_t pi = (int64_t)v * hw + (int64_t)gy * W + gx;
+            o = out[pi];
+            t0 = target[3 * pi];
+            t1 = target[3 * pi + 1];
+            t2 = target[3 * pi + 2];
         }
-        __syncthreads();
+        sx3[0][r][q] = o.x; sx3[1][r][q] = o.y; sx3[2][r][q] = o.z;
+        sy3[0][r][q] = t0; sy3[1][r][q] = t1; sy3[2][r][q] = t2;
+    }
+    __syncthreads();
+    for (int c = 0; c < 3; ++c) {
+        float(*sx)[kHx] = sx3[c];
+        float(*sy)[kHx] = sy3[c];
         for (int i = threadIdx.x; i < kHy * kTx; i += kSsimThreads) {   // x pass
             const int r = i / kTx, q = i - r * kTx;
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
@@ -174,6 +180,24 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_back(const float4 *__rest
     const int64_t hw = (int64_t)H * W;
     const float inv = 1.0f / (3.0f * (float)total);
     float gacc[2][3];   // (2 output pixels per thread)
+    float xo[2][3], yo[2][3];   // their render and target values (one 16-byte load per pixel)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int i = threadIdx.x + t * kSsimThreads;
+        const int r = i / kTx, q = i - r * kTx, gy = y0 + kHalf + r, gx = x0 + kHalf + q;
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+        if (gy < H && gx < W) {
+            const int64_t pi = (int64_t)v * hw + (int64_t)gy * W + gx;
+            o = out[pi];
+            t0 = target[3 * pi];
+            t1 = target[3 * pi + 1];
+            t2 = target[3 * pi + 2];
+        }
+        xo[t][0] = o.x; xo[t][1] = o.y; xo[t][2] = o.z;
+        yo[t][0] = t0; yo[t][1] = t1; yo[t][2] = t2;
+    }
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
         for (int i = threadIdx.x; i < kHx * kHy; i += kSsimThreads) {
             const int r = i / kHx, q = i - r * kHx, gy = y0 + r, gx = x0 + q;
@@ -212,8 +236,7 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_back(const float4 *__rest
                 b1 = fmaf(w, hb[1][r + k][q], b1);
                 b2 = fmaf(w, hb[2][r + k][q], b2);
             }
-            const int64_t pi = (int64_t)v * hw + (int64_t)gy * W + gx;
-            const float x = reinterpret_cast<const float *>(out)[4 * pi + c], y = target[3 * pi + c];
+            const float x = xo[t][c], y = yo[t][c];
             const float dssim = b0 + 2.f * x * b1 + y * b2;
             const float dl = x - y;
             const float l1 = dl > 0.f ? inv : (dl < 0.f ? -inv : 0.f);
