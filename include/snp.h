@@ -230,9 +230,11 @@ snp_status snp_loss_l1(const float *out_rgba, const float *target_rgb, int64_t n
                        void *cuda_stream);
 snp_status snp_loss_3dgs(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views, int32_t height,
                          int32_t width, float lambda_dssim, float *grad_rgba, float *loss, void *cuda_stream);
-/* snp_loss_3dgs over n_views of a training step of step_views (>= n_views) views: the
- * means (loss and gradient) divide by step_views x height x width, so that the parts of
- * a step taken one camera batch at a time add up to snp_loss_3dgs over the whole step. */
+/* snp_loss_3dgs over n_views of a training step of step_views (>= n_views)
+ * views: the means (loss and gradient) divide by step_views x height x width, and the
+ * constant of (1 - SSIM) is taken in proportion, so that the parts of a step taken one
+ * camera batch at a time add up to snp_loss_3dgs over the whole step.  step_views <
+ * n_views: SNP_ERR_INVALID_ARGUMENT. */
 snp_status snp_loss_3dgs_part(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views,
                               int32_t height, int32_t width, int32_t step_views, float lambda_dssim, float *grad_rgba,
                               float *loss, void *cuda_stream);
