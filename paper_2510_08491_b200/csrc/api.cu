@@ -8,9 +8,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "snp_internal.cuh"
 
 using namespace snp;
+
+namespace {
+// NVTX range per API call (SURVEY §5 "Tracing / profiling"): visible in Nsight Systems /
+// Compute timelines; a no-op without an attached tool
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -292,6 +303,7 @@ snp_status snp_create_scene(const snp_scene_desc *d, int device, void *cuda_stre
 }
 
 snp_status snp_update_scene(snp_scene s, const snp_scene_desc *d, void *cuda_stream) {
+    NvtxRange nvtx_("snp_update_scene");
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -361,6 +373,7 @@ snp_status snp_set_temporal_grad(snp_scene s, float *grad_w_t) {
 
 snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, const float *xi_t,
                           void *cuda_stream) {
+    NvtxRange nvtx_("snp_project_at");
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -438,6 +451,7 @@ snp_status snp_project_at(snp_scene s, const snp_camera *cams, int32_t n_views, 
 }
 
 snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_stream) {
+    NvtxRange nvtx_("snp_bin_sort");
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -666,6 +680,7 @@ static snp_status render_device(snp_scene s, const snp_render_opts *opts, float 
 }
 
 snp_status snp_render(snp_scene s, const snp_render_opts *opts, float *out_rgba, void *cuda_stream) {
+    NvtxRange nvtx_("snp_render");
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -702,6 +717,7 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
                                   const float *grad_rgba, float *grad_w1, float *grad_b1, float *grad_w2,
                                   float *grad_b2, float *grad_sh, float *grad_centers, float *grad_rotations,
                                   float *grad_scales, void *cuda_stream) {
+    NvtxRange nvtx_("snp_render_backward_ex");
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -847,6 +863,7 @@ snp_status snp_loss_3dgs(snp_scene s, const float *out_rgba, const float *target
 snp_status snp_loss_3dgs_part(snp_scene s, const float *out_rgba, const float *target_rgb, int32_t n_views,
                               int32_t height, int32_t width, int32_t step_views, float lambda_dssim, float *grad_rgba,
                               float *loss, void *cuda_stream) {
+    NvtxRange nvtx_("snp_loss_3dgs_part");
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
@@ -875,6 +892,7 @@ snp_status snp_scale_regularizer(snp_scene s, float weight, float *grad_scales, 
 
 snp_status snp_adam_step(snp_scene s, const float *const *grads, const float *lr, float beta1, float beta2, float eps,
                          int32_t step, void *cuda_stream) {
+    NvtxRange nvtx_("snp_adam_step");
     g_err.clear();
     snp_status r = check_scene(s);
     if (r != SNP_OK) return r;
