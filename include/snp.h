@@ -279,7 +279,8 @@ snp_status snp_get_debug_counters(snp_scene s, uint64_t *out, int32_t n, void *c
  * batch (<= 32 views) and the whole image also records its composited hits (per hit: the
  * pixel, the primitive, the transmittance in front of it, its kappa and the colour
  * accumulated up to it; about 32 B per hit), and the next snp_render_backward_ex of the
- * same projection and colour mode forms dL/dI and dL/dc from them (Eq. 4, 9)
+ * same projection, colour mode and transmittance floor forms dL/dI and dL/dc from them
+ * (Eq. 4, 9)
  * instead of traversing the frame again -- the same gradients.  A new snp_project or
  * snp_update_scene drops the record.  Off (0) by default. */
 snp_status snp_set_record(snp_scene s, int32_t on);

@@ -99,6 +99,7 @@ struct snp_scene_s {
     bool record_mode = false;
     bool recorded = false;             // the last render recorded them (this projection, one camera batch)
     int32_t rec_colour = 0;            //   in this colour mode
+    float rec_floor = 0.f;             //   with this transmittance floor (its stop rule)
     int64_t rec_chunks = 0;            //   in this many entry chunks
     DevBuf<float4> tight;              // K1a -> K2, tight binning (SNP_BIN_*): per item, see tight_geom
     DevBuf<float4> intr;               //   per view (1/fx, 1/fy, cx, cy)
@@ -662,6 +663,7 @@ static snp_status render_device(snp_scene s, const snp_render_opts *opts, float 
         a.bw_skip = s->bw_skip.p;
         s->rec_chunks = chunks;
         s->rec_colour = opts->colour_mode;
+        s->rec_floor = opts->transmittance_floor;
     }
     const size_t order_stride = (size_t)kCamsPerLaunch * (size_t)(s->tiles_x * s->stripe_rows);
     a.k5_grid = render_grid(s->n_hidden, a.colour_ray != 0, a.eager_emit != 0,
@@ -766,7 +768,8 @@ snp_status snp_render_backward_ex(snp_scene s, const snp_render_opts *opts, cons
     }
     // the forward recorded its composited hits (snp_set_record, one camera batch, this
     // colour mode): no gradient-mode traversal; K7s forms dL/dI and dL/dc from them
-    const bool from_fwd = s->recorded && s->rec_colour == opts->colour_mode && s->cams.size() == 1 &&
+    const bool from_fwd = s->recorded && s->rec_colour == opts->colour_mode &&
+                          s->rec_floor == opts->transmittance_floor && s->cams.size() == 1 &&
                           !std::getenv("SNP_K7F_UNSORTED");
     // K5 in grad mode: one GradEntry per composited hit, in per-warp chunks (12 per pixel
     // of a camera batch, plus a partly filled chunk per resident consumer warp, before the
