@@ -1203,3 +1203,39 @@ def test_loss_3dgs_parts_add_up():
         snp.destroy(h)
     assert abs(l_p.item() - l_all.item()) <= 1e-6 * abs(l_all.item())
     assert torch.equal(g_p, g_all)
+
+
+def test_record_reuse_guards():
+    """A record is used only by a backward of the same projection (and colour mode and
+    transmittance floor): after a new projection the backward takes the gradient-mode
+    traversal and gives that path's gradients."""
+    import torch
+    from paper_2510_08491_b200 import snp
+    from gpu_util import torch_scene
+    scene = synth.make_scene(3, 800, box=0.7)
+    cams = synth.orbit_cameras(2, 3.0, 96, 72, 120.0)
+    G = torch.from_numpy(np.random.default_rng(5).normal(size=(2, 72, 96, 4)).astype(np.float32)).cuda()
+    opts = snp.make_opts((0.1, 0.1, 0.1))
+
+    def grads_of(record, reproject):
+        h = snp.create_scene(torch_scene(scene), 0)
+        try:
+            snp.set_record(h, record)
+            out = torch.zeros((2, 72, 96, 4), device="cuda")
+            snp.render_views(h, cams, opts, out)
+            if reproject:   # a new projection (same cameras) drops the record
+                snp.project(h, snp.make_cameras(cams))
+                snp.bin_sort(h, opts)
+            gr = {f: torch.zeros(getattr(scene, f).shape, device="cuda") for f in snp.FIELDS}
+            snp.render_backward(h, opts, G, gr, fwd_rgba=out)
+            torch.cuda.synchronize()
+            return {f: v.cpu().numpy().astype(np.float64) for f, v in gr.items()}
+        finally:
+            snp.destroy(h)
+
+    ref = grads_of(0, False)
+    for record, reproject in ((1, True), (1, False)):
+        got = grads_of(record, reproject)
+        for f in snp.FIELDS:
+            scale = np.abs(ref[f]).max()
+            assert np.abs(got[f] - ref[f]).max() <= 2e-4 * scale + 1e-7, (record, reproject, f)
