@@ -262,7 +262,7 @@ def run_c3(args):
         g.replay()
     torch.cuda.synchronize()
     passes = (19 + int(np.ceil(np.log2(((W + 15) // 16) * ((H + 15) // 16)))) + 7) // 8
-    launches_per_step = 7 + passes   # K1a, K1b, K2, K3 x passes, K4, tile order, K5, K6
+    launches_per_step = 8 + passes   # K1a, K1b, K2, K3 x passes, K4, tile order, K5, K6w, K6
     total_ms, clocks = _timed(args, lambda i: g.replay(), st, 1, dev, flush)
     ms_per_step = total_ms / args.steps
     fps = args.steps / (total_ms / 1e3)
@@ -427,6 +427,16 @@ def e2e_resident_c3(args, scene, cams_c, bg, W, H, local):
                     "wall clock"}
 
 
+def c4_launches_per_step(nv, W, H):
+    """Kernels one snp_render_views of nv views launches: per camera batch (<= 32 views)
+    K1a, K1b, the tile order, K5, K6w, K6; once K2 and K4; K3 once per 8-bit digit of
+    the (view | tile | depth) key."""
+    batches = (nv + 31) // 32
+    bits = lambda v: int(np.ceil(np.log2(v))) if v > 1 else 0   # (bits_for in api.cu)
+    passes = (19 + bits(((W + 15) // 16) * ((H + 15) // 16)) + bits(nv) + 7) // 8
+    return 6 * batches + 2 + passes
+
+
 def run_c4(args):
     """Config C4 on N ranks: 64 orbit views of the C3 scene, contiguous blocks of 64/N views
     per GPU, one snp_render_views per rank per step; X2 gathers the frames to rank 0 on a
@@ -546,7 +556,7 @@ def run_c4(args):
             "workload_stats_rank0": stats,
             "roofline": roof,
             "e2e": e2e,
-            "gpu_launches": (8 + 5) * args.steps,
+            "gpu_launches": c4_launches_per_step(len(views), W, H) * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line))
