@@ -41,9 +41,12 @@ snp_status fail(snp_status st, const std::string &msg) {
     } while (0)
 
 enum State { kCreated = 0, kProjected = 1, kBinned = 2 };
-// K5 emits after every exact round when the tile lists average more keys than this
-// (DESIGN.md "K5 design" 7: C5 221 keys/tile -> eager; C3 90, C2 18 -> default)
+// K5 emits after every exact round when the tile lists average more keys than this, or
+// the visible primitives more keys (tiles) each than kEagerKeysPerVisible -- large
+// footprints, deep overlapping lists (DESIGN.md "K5 design" 7: C5 221 keys/tile and 2.9
+// keys/primitive, C2 4.5 and C1 3.1 keys/primitive -> eager; C3 90 and 1.9 -> default)
 constexpr double kEagerKeysPerTile = 150.0;
+constexpr double kEagerKeysPerVisible = 2.5;
 
 // Device buffer that only grows.
 template <typename T>
@@ -523,10 +526,12 @@ snp_status snp_bin_sort(snp_scene s, const snp_render_opts *opts, void *cuda_str
     b.vals = s->vals0.p;
     SNP_CUDA(launch_dup(b, st));
     if (opts->sync_check) {
-        SNP_CUDA(cudaMemcpyAsync(s->h_counters + kCntDup, s->counters.p + kCntDup, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
+        static_assert(kCntVisible + 1 == kCntDup, "one copy reads both counters");
+        SNP_CUDA(cudaMemcpyAsync(s->h_counters + kCntVisible, s->counters.p + kCntVisible,
+                                 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         SNP_CUDA(cudaStreamSynchronize(st));
-        s->eager_emit = (double)s->h_counters[kCntDup] > kEagerKeysPerTile * (double)slots;
+        s->eager_emit = (double)s->h_counters[kCntDup] > kEagerKeysPerTile * (double)slots ||
+                        (double)s->h_counters[kCntDup] > kEagerKeysPerVisible * (double)s->h_counters[kCntVisible];
         const int64_t ndup = (int64_t)s->h_counters[kCntDup];
         s->known_ndup = ndup;
         if (ndup > s->key_capacity) {

@@ -877,9 +877,9 @@ def test_backward_temporal_weights_vs_finite_differences(orc):
 
 def test_eager_emission_rule(orc, monkeypatch):
     """K5's eager mid-batch emission (kEager) is chosen from the binning alone (mean keys
-    per tile > 150): on for C5 (221), off for C3 (90); on C5 it hands fewer pixels to K6
-    than the forced default mode, on C3 nothing changes, and the C5 fallback pixels keep
-    parity."""
+    per tile > 150, or keys per visible primitive > 2.5): on for C5 (221; 2.9), off for
+    C3 (90; 1.9); on C5 it hands fewer pixels to K6 than the forced default mode, on C3
+    nothing changes, and the C5 fallback pixels keep parity."""
     scene5, cams5, bg5 = synth.make_config("C5")
     eager = gpu_render(scene5, cams5, bg5)
     monkeypatch.setenv("SNP_EAGER_EMIT", "0")
