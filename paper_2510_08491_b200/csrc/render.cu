@@ -783,10 +783,13 @@ __global__ void __launch_bounds__(kThreads, SNP_AB_K5_CTAS) k_render(RenderArgs 
                 // pixels), earlier termination; chosen per scene from the overflow rate
                 const bool do_emit = !ps.done && (batch_end || pd.n > (kEager ? 0 : plimit - 4));
                 if (kEntries) {
-                    grad_reserve(__reduce_add_sync(0xffffffffu, do_emit ? (uint32_t)pd.n : 0u));
-                    emit_sync<N, kRay, kRecord>(sm, ps, pd, do_emit,
-                                       batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
-                                       a.t_floor, recs, a, ray, gx);
+                    const uint32_t need = __reduce_add_sync(0xffffffffu, do_emit ? (uint32_t)pd.n : 0u);
+                    if (need) {   // (warp-uniform: rounds without an emitting lane skip both)
+                        grad_reserve((int)need);
+                        emit_sync<N, kRay, kRecord>(sm, ps, pd, do_emit,
+                                           batch_end ? ((flags & 2) ? INFINITY : sm.L[slot][cnt]) : sm.L[slot][jn],
+                                           a.t_floor, recs, a, ray, gx);
+                    }
                 } else if (do_emit) {
 #ifdef SNP_INSTRUMENT
                     long long _e0 = clock64();
