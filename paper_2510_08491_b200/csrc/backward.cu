@@ -1149,21 +1149,68 @@ __global__ void __launch_bounds__(128) k_grad_sorted(RenderArgs a, CamBatch cb, 
 }
 
 // Primitive colour mode: the colour gradients of every (view, primitive) from the summed
-// dL/dc of its composited hits (colour_grads is linear in dL/dc).
+// dL/dc of its composited hits (colour_grads is linear in dL/dc).  One thread per
+// primitive sums over the batch's views -- dL/dsh = sum_v Y(dir_v) (x) dL/dc_v and the
+// mu-through-dir_v terms -- and adds once (a view's direction is the record's
+// compensated camera-relative centre, as in colour_grads).
 template <int N>
 __global__ void __launch_bounds__(128) k_colour_finalize(RenderArgs a, CamBatch cb, BackwardGrads gr) {
     if (a.counters[kCntGradOverflow]) return;
-    const int64_t total = (int64_t)cb.nv * a.n;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const float4 g = a.gc_acc[i];
-        if (g.x == 0.f && g.y == 0.f && g.z == 0.f) continue;
-        const int64_t vloc = i / a.n;
-        const uint32_t id = (uint32_t)(i - vloc * a.n);
-        // (a composited primitive is visible in the view: its record exists)
-        const float4 *rec = a.records + ((size_t)(cb.view0 + vloc) * (size_t)a.n + id) * rec_f4(N);
-        const float gc[3] = {g.x, g.y, g.z};
-        const Ray unused{0, 0, 1, 0, 0, 0, 0, 0};
-        colour_grads<false>(a, rec, unused, id, gc, gr);
+    const int ncoef = (a.sh_degree + 1) * (a.sh_degree + 1);
+    for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < a.n; id += (int64_t)gridDim.x * blockDim.x) {
+        float acc[48];
+#pragma unroll
+        for (int f = 0; f < 48; ++f) acc[f] = 0.f;
+        float gmu[3] = {0.f, 0.f, 0.f};
+        bool any = false;
+        const float *shp = a.sh + 48 * (size_t)id;
+        for (int v = 0; v < cb.nv; ++v) {
+            const float4 g = a.gc_acc[(size_t)v * a.n + id];
+            if (g.x == 0.f && g.y == 0.f && g.z == 0.f) continue;
+            any = true;
+            // (a composited primitive is visible in the view: its record exists)
+            const float4 *rec = a.records + ((size_t)(cb.view0 + v) * (size_t)a.n + id) * rec_f4(N);
+            const float4 mh = rec[kRecMh], ml = rec[kRecMl];
+            const float vx = mh.x + ml.x, vy = mh.y + ml.y, vz = mh.z + ml.z;
+            const float nrm = sqrtf(vx * vx + vy * vy + vz * vz);
+            const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
+            const float dxv = nrm > 0.f ? vx * inv : 0.f, dyv = nrm > 0.f ? vy * inv : 0.f,
+                        dzv = nrm > 0.f ? vz * inv : 1.f;
+            float Y[16];
+            sh_basis_f(dxv, dyv, dzv, Y);
+            const float gcv[3] = {g.x, g.y, g.z};
+#pragma unroll
+            for (int f = 0; f < 48; ++f) acc[f] = fmaf(Y[f / 3], gcv[f % 3], acc[f]);
+            if (gr.mu && nrm > 0.f) {   // dir = (mu - C) / |mu - C|: dL/dmu = (I - dir dir^T) dL/ddir / |mu - C|
+                float dY[16][3];
+                sh_basis_grad(dxv, dyv, dzv, dY);
+                float gd[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (i < ncoef) {
+                        const float e = shp[3 * i] * g.x + shp[3 * i + 1] * g.y + shp[3 * i + 2] * g.z;
+                        gd[0] = fmaf(dY[i][0], e, gd[0]);
+                        gd[1] = fmaf(dY[i][1], e, gd[1]);
+                        gd[2] = fmaf(dY[i][2], e, gd[2]);
+                    }
+                const float dd = dxv * gd[0] + dyv * gd[1] + dzv * gd[2];
+                gmu[0] += (gd[0] - dxv * dd) * inv;
+                gmu[1] += (gd[1] - dyv * dd) * inv;
+                gmu[2] += (gd[2] - dzv * dd) * inv;
+            }
+        }
+        if (!any) continue;
+        float *gs = gr.sh + 48 * (size_t)id;
+#pragma unroll
+        for (int f0 = 0; f0 < 48; f0 += 4)
+            if (f0 < 3 * ncoef)
+                add4(gs + f0, acc[f0], f0 + 1 < 3 * ncoef ? acc[f0 + 1] : 0.f, f0 + 2 < 3 * ncoef ? acc[f0 + 2] : 0.f,
+                     f0 + 3 < 3 * ncoef ? acc[f0 + 3] : 0.f, gr.vec);
+        if (gr.mu) {
+            atomicAdd(gr.mu + 3 * (size_t)id + 0, gmu[0]);
+            atomicAdd(gr.mu + 3 * (size_t)id + 1, gmu[1]);
+            atomicAdd(gr.mu + 3 * (size_t)id + 2, gmu[2]);
+        }
     }
 }
 
